@@ -1,0 +1,157 @@
+/*
+ * pdmg_b200.h -- C ABI of the B200-native batched shifted-Laplacian multigrid (libpdmg_b200.so).
+ *
+ * Drop-in boundary for the reference `pdmg` solver path (He & Liu, arXiv 2203.11154).  The reference
+ * exposes this path as C++ in namespace pdmg, linked statically (proj/src/CMakeLists.txt:1-12); it has
+ * no FFI.  Each entry point below replaces the reference interface cited beside it; the C++ facade
+ * include/pdmg_b200.hpp restores the reference's class shapes and exception types on top of it.
+ *
+ * Conventions
+ *  - Plain C types only.  pdmg_c128 is layout-compatible with std::complex<double> and double2.
+ *  - Host grid arrays use the reference layout (proj/include/pdmg/grid.hpp:54-91): per shift, the
+ *    (n-1)x(n-1) interior nodes, row-major with x fastest; shifts are stacked shift-major.
+ *  - Status codes mirror proj/include/pdmg/errors.hpp:10-28: 0 OK, 1 ConfigError, 2
+ *    SingularOperatorError, 3 runtime (CUDA) error.  pdmg_last_error() returns the message of the
+ *    last failing call on the calling thread (same text as the reference's exception what()).
+ *  - Non-convergence is data (converged[] = 0), never an error (proj/src/multigrid.cpp:93-106).
+ *  - Every solve runs on the GPU; there is no CPU fallback.  A missing/unusable GPU is status 3.
+ */
+#ifndef PDMG_B200_H
+#define PDMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDMG_B200_ABI_VERSION 1
+
+typedef struct {
+  double re, im;
+} pdmg_c128;
+
+enum {
+  PDMG_OK = 0,
+  PDMG_ERR_CONFIG = 1,   /* pdmg::ConfigError           (errors.hpp:12-15) */
+  PDMG_ERR_SINGULAR = 2, /* pdmg::SingularOperatorError (errors.hpp:20-23) */
+  PDMG_ERR_RUNTIME = 3   /* CUDA / device failure                          */
+};
+enum { PDMG_CYCLE_V = 0, PDMG_CYCLE_W = 1 };              /* pdmg::CycleKind    (multigrid.hpp:12) */
+enum { PDMG_SMOOTHER_VANKA = 0, PDMG_SMOOTHER_JACOBI = 1 }; /* pdmg::SmootherKind (smoother.hpp:28) */
+enum { PDMG_PREC_C128 = 0, PDMG_PREC_C64 = 1 };
+
+/* pdmg::MultigridConfig (proj/include/pdmg/multigrid.hpp:14-32) with its SmootherConfig
+ * (proj/include/pdmg/smoother.hpp:30-38) flattened in. */
+typedef struct {
+  int32_t cycle;      /* PDMG_CYCLE_V / PDMG_CYCLE_W                 */
+  int32_t nu1, nu2;   /* pre / post smoothing sweeps                 */
+  int32_t coarsest_n; /* coarsest level mesh width 1/coarsest_n      */
+  double tol;         /* relative residual reduction target          */
+  int32_t max_iter;
+  int32_t smoother;   /* PDMG_SMOOTHER_VANKA / PDMG_SMOOTHER_JACOBI  */
+  double omega;       /* real relaxation weight (smoother.hpp:34)    */
+} pdmg_mg_config;
+
+/* Reference defaults: W(1,0), coarsest_n 8, tol 1e-8, max_iter 200, Vanka omega 24/25
+ * (multigrid.hpp:14-23, smoother.hpp:32-36). */
+void pdmg_mg_config_default(pdmg_mg_config* cfg);
+
+/* A batch of hierarchies sharing one fine grid and config, one per shift.  Replaces constructing one
+ * pdmg::MultigridHierarchy(Grid2D(n), Shift{lambda_j}, cfg) per shift (multigrid.hpp:52,
+ * multigrid.cpp:24-61) inside paradiag_solve's loop (paradiag.cpp:207-236). */
+typedef struct {
+  int32_t n;                /* Grid2D.n of the finest grid (h = 1/n)       */
+  int32_t n_shifts;         /* >= 1                                        */
+  const pdmg_c128* lambdas; /* host [n_shifts]: Shift.lambda (grid.hpp:44) */
+  pdmg_mg_config cfg;
+  int32_t precision;        /* PDMG_PREC_C128 (the reference's type)       */
+  int32_t device;           /* CUDA device ordinal                         */
+} pdmg_batch_desc;
+
+typedef struct pdmg_ctx pdmg_ctx;
+
+/* Per-shift outputs of MultigridHierarchy::solve (pdmg::SolveReport, multigrid.hpp:34-44).  Any pointer
+ * may be NULL.  residual_history is [n_shifts][max_iter+1]; entries past iterations[s] are 0. */
+typedef struct {
+  int32_t* iterations;
+  uint8_t* converged;
+  double* residual_history;
+  double* rate;
+  double seconds; /* wall time of the call (SolveReport.seconds) */
+} pdmg_solve_report;
+
+const char* pdmg_last_error(void);
+int pdmg_abi_version(void);
+
+/* Builds the hierarchy for every shift: validates cfg (multigrid.hpp:25-31), the level list
+ * (multigrid.cpp:27-44), the smoother on every non-coarsest level (multigrid.cpp:47-58, throws
+ * "level l (n = N): ..."), factors each coarsest operator (dense.cpp:82-88) and allocates device
+ * storage.  Config and singular-smoother errors are reported before any CUDA call. */
+int pdmg_create(const pdmg_batch_desc* desc, pdmg_ctx** out);
+void pdmg_destroy(pdmg_ctx* ctx);
+int pdmg_num_levels(const pdmg_ctx* ctx);           /* MultigridHierarchy::num_levels */
+int pdmg_level_n(const pdmg_ctx* ctx, int level);   /* level_grid(level).n             */
+int pdmg_num_shifts(const pdmg_ctx* ctx);
+/* 1 if shift s's coarsest operator is singular (DenseShiftedSolver::singular, dense.hpp:40). */
+int pdmg_coarse_singular(const pdmg_ctx* ctx, int shift);
+
+/* MultigridHierarchy::solve for all shifts from u = 0 (multigrid.cpp:85-110): b, u host arrays of
+ * n_shifts*(n-1)^2.  A singular coarsest operator fails with status 2 (dense.cpp:90-94). */
+int pdmg_solve(pdmg_ctx* ctx, const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* report);
+/* Same with b, u already resident in device memory of ctx's device (compact layout as above). */
+int pdmg_solve_device(pdmg_ctx* ctx, const void* d_b, void* d_u, pdmg_solve_report* report);
+
+/* MultigridHierarchy::cycle: one cycle applied in place to every shift's u (multigrid.cpp:79-83). */
+int pdmg_cycle(pdmg_ctx* ctx, pdmg_c128* u, const pdmg_c128* b);
+
+/* Level operators, batched over all shifts of ctx at hierarchy level `level` (0 = finest).  They use
+ * ctx's level buffers as scratch.  Host arrays are n_shifts * (level_n-1)^2. */
+int pdmg_apply_smoother(pdmg_ctx* ctx, int level, const pdmg_c128* u, const pdmg_c128* b,
+                        pdmg_c128* out);                                   /* smoother.cpp:49-67 */
+int pdmg_residual(pdmg_ctx* ctx, int level, const pdmg_c128* b, const pdmg_c128* u,
+                  pdmg_c128* r);                                           /* grid.cpp:92-100    */
+int pdmg_restrict_full_weighting(pdmg_ctx* ctx, int level, const pdmg_c128* fine,
+                                 pdmg_c128* coarse);                       /* grid.cpp:102-121   */
+int pdmg_prolong_bilinear(pdmg_ctx* ctx, int level, const pdmg_c128* coarse,
+                          pdmg_c128* fine);                                /* grid.cpp:123-153   */
+int pdmg_norm(pdmg_ctx* ctx, int level, const pdmg_c128* v, double* norms); /* grid.cpp:7-11    */
+int pdmg_coarse_solve(pdmg_ctx* ctx, const pdmg_c128* b, pdmg_c128* u);      /* dense.cpp:90-100 */
+
+/* ParaDIAG step with the alpha-circulant backward-Euler time matrix C_alpha = (1/dt)(I - Sigma_alpha)
+ * (restated; the reference's three-step driver is paradiag.cpp:185-248):
+ *   g = ifft_t(alpha^(t/nt) f);  (A + lambda_k I) w_k = g_k, lambda_k = (1 - alpha^(1/nt) e^(2 pi i k/nt))/dt;
+ *   u = alpha^(-t/nt) fft_k(w);  relres = ||f - (C_alpha (x) I + I (x) A) u|| / ||f||.
+ * f, u: host [nt][(n-1)^2].  cfg as for pdmg_create.  report arrays are per time slot k. */
+int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg,
+                            int32_t device, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* report,
+                            double* relres);
+
+/* Host helpers (no GPU needed). */
+/* tools/pdmg.cpp:137-147 random_rhs: std::mt19937(seed), uniform_real_distribution<double>(lo,hi),
+ * re then im per node; `count` complex values. */
+void pdmg_random_rhs(uint32_t seed, double lo, double hi, int64_t count, pdmg_c128* out);
+/* lambda_j = (1 - alpha^(1/nt) e^(2 pi i j/nt))/dt for j = j0 .. j0+count-1 (BASELINE.json shifts). */
+void pdmg_circulant_shifts(double alpha, int32_t nt, double dt, int32_t j0, int32_t count, pdmg_c128* out);
+/* Pinned host memory for fast host<->device staging. */
+void* pdmg_host_alloc(size_t bytes);
+void pdmg_host_free(void* p);
+
+/* Instrumentation.  When profiling is on, every kernel launch is bracketed by CUDA events on ctx's
+ * stream and attributed to a kernel class; stats accumulate until reset. */
+void* pdmg_stream(pdmg_ctx* ctx); /* the cudaStream_t all of ctx's work runs on */
+int pdmg_set_profiling(pdmg_ctx* ctx, int on);
+void pdmg_reset_stats(pdmg_ctx* ctx);
+int64_t pdmg_launch_count(const pdmg_ctx* ctx); /* kernels launched since the last reset */
+/* Kernel class i: name, launches, total device ms, total algorithmic DRAM bytes.  Returns 0 while i is
+ * valid, 1 past the end. */
+int pdmg_kernel_stats(const pdmg_ctx* ctx, int i, char* name, size_t name_len, int64_t* launches,
+                      double* total_ms, double* algo_bytes);
+/* Grid-point smoother updates performed by the last solve (sum over shifts and cycles). */
+double pdmg_last_updates(const pdmg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDMG_B200_H */

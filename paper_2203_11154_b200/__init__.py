@@ -1,0 +1,14 @@
+"""paper_2203_11154_b200 -- B200-native batched complex-shifted-Laplacian multigrid (Vanka V-cycles).
+
+Host mirror of the reference `pdmg` solver interface over libpdmg_b200.so (sm_100a CUDA + C ABI,
+include/pdmg_b200.h).  See DESIGN.md.
+"""
+from .multigrid import (BatchedMultigridHierarchy, ConfigError, CycleKind, DeviceError, Grid2D, MultigridConfig,
+                        MultigridHierarchy, Shift, ShiftKind, SingularOperatorError, SmootherConfig, SmootherKind,
+                        SolveReport, circulant_shifts, multigrid_solve, random_rhs)
+
+__all__ = [
+    "BatchedMultigridHierarchy", "ConfigError", "CycleKind", "DeviceError", "Grid2D", "MultigridConfig",
+    "MultigridHierarchy", "Shift", "ShiftKind", "SingularOperatorError", "SmootherConfig", "SmootherKind",
+    "SolveReport", "circulant_shifts", "multigrid_solve", "random_rhs",
+]

@@ -1,0 +1,1050 @@
+// pdmg_capi.cu -- host orchestration (C++) and the extern "C" boundary of libpdmg_b200.so.
+//
+// Mirrors the reference solver path (proj/src/multigrid.cpp, proj/src/paradiag.cpp) for a BATCH of
+// shifts: one pdmg_ctx holds, for every shift, what one pdmg::MultigridHierarchy holds (level list,
+// per-level smoother coefficients, coarsest factorization) plus device storage for all levels.  Every
+// cycle is a short sequence of batched k_level launches (pdmg_kernels.cuh) over all still-active
+// shifts; convergence is decided on the device per shift (k_finalize) exactly as in
+// MultigridHierarchy::solve, so per-shift cycle counts match the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pdmg_b200.h"
+#include "pdmg_kernels.cuh"
+
+using cplx = std::complex<double>;
+
+namespace pdmg_b200 {
+
+// ---------------------------------------------------------------------------------------------
+// Error taxonomy (proj/include/pdmg/errors.hpp:10-28) carried through the C ABI as status codes.
+// ---------------------------------------------------------------------------------------------
+struct ConfigError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct SingularOperatorError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+thread_local std::string g_last_error;
+
+#define CK(x)                                                                                        \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess)                                                                           \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" +          \
+                      std::to_string(__LINE__) + ")");                                               \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PDMG_OK;
+  } catch (const ConfigError& e) {
+    g_last_error = e.what();
+    return PDMG_ERR_CONFIG;
+  } catch (const SingularOperatorError& e) {
+    g_last_error = e.what();
+    return PDMG_ERR_SINGULAR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PDMG_ERR_RUNTIME;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host-side setup math (fp64), restating the reference formulas.
+// ---------------------------------------------------------------------------------------------
+constexpr double kSingularTol = 1e-12;  // smoother.cpp:6
+
+cplx checked_inverse(cplx z, const char* what) {  // smoother.cpp:8-15
+  if (std::abs(z) <= kSingularTol)
+    throw SingularOperatorError(std::string("vanka_coeffs: patch eigenvalue ") + what + " is singular for this shift");
+  return cplx(1.0, 0.0) / z;
+}
+
+struct Vanka {
+  cplx a, b, c;
+};
+Vanka vanka_coeffs(cplx eta) {  // smoother.cpp:18-29
+  const cplx i2 = checked_inverse(cplx(2.0, 0.0) + eta, "2+eta");
+  const cplx i4 = checked_inverse(cplx(4.0, 0.0) + eta, "4+eta");
+  const cplx i6 = checked_inverse(cplx(6.0, 0.0) + eta, "6+eta");
+  return {0.25 * (i2 + 2.0 * i4 + i6), 0.25 * (i2 - i6), 0.25 * (i2 - 2.0 * i4 + i6)};
+}
+cplx jacobi_weight(cplx eta, double h) {  // smoother.cpp:42-47
+  const cplx d = cplx(4.0, 0.0) + eta;
+  if (std::abs(d) <= kSingularTol) throw SingularOperatorError("jacobi_weight: 4+eta is singular for this shift");
+  return cplx(h * h, 0.0) / d;
+}
+
+// Dense A + lambda I on the coarsest grid (dense.cpp:18-39), partial-pivot LU with the reference's
+// singularity rule min|U_ii| > 1e-14 ||A||_F (dense.cpp:82-88), then A^{-1} for the batched kernel.
+struct CoarseFactor {
+  bool singular = false;
+  std::vector<cplx> inv;  // N x N row-major
+};
+CoarseFactor factor_coarse(int n, cplx lambda) {
+  if (n > 128)
+    throw ConfigError("dense_shifted_operator: dense assembly refused for n = " + std::to_string(n) + " (limit 128)");
+  const int m = n - 1, N = m * m;
+  const double h = 1.0 / n, inv_h2 = 1.0 / (h * h);
+  const cplx diag = (cplx(4.0, 0.0) + lambda * (h * h)) * inv_h2, off(-inv_h2, 0.0);
+  std::vector<cplx> A(static_cast<size_t>(N) * N, cplx(0.0, 0.0));
+  auto idx = [m](int i, int j) { return (j - 1) * m + (i - 1); };
+  for (int j = 1; j <= m; ++j)
+    for (int i = 1; i <= m; ++i) {
+      const int r = idx(i, j);
+      A[(size_t)r * N + r] = diag;
+      if (i > 1) A[(size_t)r * N + idx(i - 1, j)] = off;
+      if (i < m) A[(size_t)r * N + idx(i + 1, j)] = off;
+      if (j > 1) A[(size_t)r * N + idx(i, j - 1)] = off;
+      if (j < m) A[(size_t)r * N + idx(i, j + 1)] = off;
+    }
+  double fro = 0.0;
+  for (const cplx& z : A) fro += std::norm(z);
+  fro = std::sqrt(fro);
+  std::vector<int> piv(N);
+  double min_pivot = INFINITY;
+  for (int k = 0; k < N; ++k) {
+    int p = k;
+    double best = std::abs(A[(size_t)k * N + k]);
+    for (int r = k + 1; r < N; ++r)
+      if (std::abs(A[(size_t)r * N + k]) > best) best = std::abs(A[(size_t)r * N + k]), p = r;
+    piv[k] = p;
+    if (p != k)
+      for (int c = 0; c < N; ++c) std::swap(A[(size_t)k * N + c], A[(size_t)p * N + c]);
+    const cplx pv = A[(size_t)k * N + k];
+    min_pivot = std::min(min_pivot, std::abs(pv));
+    if (pv == cplx(0.0, 0.0)) continue;
+    for (int r = k + 1; r < N; ++r) {
+      const cplx f = A[(size_t)r * N + k] / pv;
+      A[(size_t)r * N + k] = f;
+      for (int c = k + 1; c < N; ++c) A[(size_t)r * N + c] -= f * A[(size_t)k * N + c];
+    }
+  }
+  CoarseFactor cf;
+  cf.singular = !(min_pivot > 1e-14 * fro);
+  cf.inv.assign(static_cast<size_t>(N) * N, cplx(0.0, 0.0));
+  if (cf.singular) return cf;
+  std::vector<cplx> x(N);
+  for (int col = 0; col < N; ++col) {
+    std::fill(x.begin(), x.end(), cplx(0.0, 0.0));
+    x[col] = 1.0;
+    for (int k = 0; k < N; ++k)
+      if (piv[k] != k) std::swap(x[k], x[piv[k]]);
+    for (int r = 0; r < N; ++r)
+      for (int c = 0; c < r; ++c) x[r] -= A[(size_t)r * N + c] * x[c];
+    for (int r = N - 1; r >= 0; --r) {
+      for (int c = r + 1; c < N; ++c) x[r] -= A[(size_t)r * N + c] * x[c];
+      x[r] /= A[(size_t)r * N + r];
+    }
+    for (int r = 0; r < N; ++r) cf.inv[(size_t)r * N + col] = x[r];
+  }
+  return cf;
+}
+
+void validate(const pdmg_mg_config& c) {  // multigrid.hpp:25-31
+  if (c.nu1 < 0 || c.nu2 < 0) throw ConfigError("MultigridConfig: negative smoothing counts");
+  if (c.nu1 + c.nu2 == 0) throw ConfigError("MultigridConfig: nu1 + nu2 must be positive");
+  if (c.coarsest_n < 2) throw ConfigError("MultigridConfig: coarsest_n must be >= 2");
+  if (!(c.tol > 0.0)) throw ConfigError("MultigridConfig: tol must be positive");
+  if (c.max_iter < 1) throw ConfigError("MultigridConfig: max_iter must be >= 1");
+  if (c.cycle != PDMG_CYCLE_V && c.cycle != PDMG_CYCLE_W) throw ConfigError("MultigridConfig: unknown cycle kind");
+  if (c.smoother != PDMG_SMOOTHER_VANKA && c.smoother != PDMG_SMOOTHER_JACOBI)
+    throw ConfigError("SmootherConfig: unknown smoother kind");
+}
+
+std::vector<int> level_list(int n, const pdmg_mg_config& c) {  // multigrid.cpp:27-44
+  if (n < 2) throw ConfigError("Grid2D: need at least 2 subdivisions per side, got " + std::to_string(n));
+  validate(c);
+  if (n < c.coarsest_n)
+    throw ConfigError("MultigridHierarchy: fine grid n = " + std::to_string(n) + " is finer than coarsest_n = " +
+                      std::to_string(c.coarsest_n) + " allows");
+  std::vector<int> lv{n};
+  int g = n;
+  while (g > c.coarsest_n) {
+    if (!(g % 2 == 0 && g >= 4))
+      throw ConfigError("MultigridHierarchy: grid n = " + std::to_string(g) + " cannot be coarsened to reach coarsest_n = " +
+                        std::to_string(c.coarsest_n));
+    g /= 2;
+    lv.push_back(g);
+  }
+  if (g != c.coarsest_n)
+    throw ConfigError("MultigridHierarchy: coarsening from n = " + std::to_string(n) + " reaches n = " + std::to_string(g) +
+                      ", not coarsest_n = " + std::to_string(c.coarsest_n));
+  return lv;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Kernel variant table: flags -> instantiation of k_level.
+// ---------------------------------------------------------------------------------------------
+struct Variant {
+  bool loadu, prolong, sweep;
+  int post;
+  bool store, jacobi;
+  int key() const {
+    return (loadu ? 1 : 0) | (prolong ? 2 : 0) | (sweep ? 4 : 0) | (post << 3) | (store ? 32 : 0) | (jacobi ? 64 : 0);
+  }
+  std::string name() const {
+    std::string s;
+    if (prolong) s += loadu ? "prolong+" : "prolong0+";
+    else if (!loadu) s += "zero+";
+    if (sweep) s += jacobi ? "jacobi" : "vanka";
+    else if (!prolong) s += "pass";
+    else s.pop_back();
+    if (post == POST_NORM) s += "+norm";
+    if (post == POST_RESTRICT) s += "+restrict";
+    if (post == POST_RESID) s += "+resid";
+    return s;
+  }
+};
+
+template <class T>
+struct KernelEntry {
+  void (*fn)(LevelArgs<T>) = nullptr;
+  size_t smem = 0;
+};
+
+template <class T>
+struct KernelTable {
+  KernelEntry<T> e[128];
+  template <bool LU, bool PR, bool SW, int PO, bool ST, bool JA>
+  void reg() {
+    const int k = (LU ? 1 : 0) | (PR ? 2 : 0) | (SW ? 4 : 0) | (PO << 3) | (ST ? 32 : 0) | (JA ? 64 : 0);
+    e[k].fn = &k_level<T, LU, PR, SW, PO, ST, JA>;
+    e[k].smem = LevelSmem<T, SW, PO>::bytes;
+  }
+  template <bool LU, bool PR, int PO, bool JA>
+  void reg_sweep() {
+    reg<LU, PR, true, PO, true, JA>();
+  }
+  template <bool LU, bool PR, int PO>
+  void reg_sweep2() {
+    reg_sweep<LU, PR, PO, false>();
+    reg_sweep<LU, PR, PO, true>();
+  }
+  template <int PO>
+  void reg_sweep4() {
+    reg_sweep2<false, false, PO>();
+    reg_sweep2<true, false, PO>();
+    reg_sweep2<false, true, PO>();
+    reg_sweep2<true, true, PO>();
+  }
+  KernelTable() {
+    reg_sweep4<POST_NONE>();
+    reg_sweep4<POST_NORM>();
+    reg_sweep4<POST_RESTRICT>();
+    // prolongate-and-correct without a sweep (nu2 == 0)
+    reg<false, true, false, POST_NONE, true, false>();
+    reg<true, true, false, POST_NONE, true, false>();
+    reg<false, true, false, POST_NORM, true, false>();
+    reg<true, true, false, POST_NORM, true, false>();
+    // residual passes without a sweep (nu1 == 0, convergence norm, level operators)
+    reg<false, false, false, POST_NORM, false, false>();
+    reg<true, false, false, POST_NORM, false, false>();
+    reg<false, false, false, POST_RESTRICT, false, false>();
+    reg<true, false, false, POST_RESTRICT, false, false>();
+    reg<true, false, false, POST_RESID, false, false>();
+  }
+  const KernelEntry<T>& get(const Variant& v) const {
+    const KernelEntry<T>& k = e[v.key()];
+    if (!k.fn) throw std::logic_error("pdmg_b200: no kernel instantiated for variant " + v.name());
+    return k;
+  }
+};
+
+// ---------------------------------------------------------------------------------------------
+// Engine: one batch of shifts on one device.
+// ---------------------------------------------------------------------------------------------
+struct Stat {
+  int64_t launches = 0;
+  double ms = 0.0, bytes = 0.0;
+};
+
+struct CtxBase {
+  virtual ~CtxBase() = default;
+};
+
+template <class T>
+struct Engine {
+  using V = typename vec2<T>::type;
+  struct Level {
+    int n = 0, m = 0;
+    int64_t ss = 0;  // shift stride (elements)
+    size_t elems = 0;
+    V* u[2] = {nullptr, nullptr};
+    V* b = nullptr;
+    int ntx = 0, nty = 0, ntiles = 0, H = 0;
+    LevelCoef<T>* coef = nullptr;
+    int cur = 0;
+    bool uzero = false;
+  };
+
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int S = 0;
+  pdmg_mg_config cfg{};
+  std::vector<int> ln;
+  std::vector<cplx> lambdas;
+  std::vector<Level> lv;
+  std::vector<uint8_t> coarse_singular;
+  bool any_singular = false;
+  V* d_ainv = nullptr;
+  int coarse_N = 0;
+  int *d_active = nullptr, *d_iters = nullptr, *d_conv = nullptr, *d_nactive = nullptr, *d_parity = nullptr;
+  int* d_ones = nullptr;
+  double *d_r0 = nullptr, *d_hist = nullptr, *d_partial = nullptr, *d_norms = nullptr;
+  V* d_stage = nullptr;
+  size_t stage_elems = 0;
+  int* h_nactive = nullptr;
+  int n_active_host = 0;
+  const KernelTable<T>* table = nullptr;
+  // instrumentation
+  bool profiling = false;
+  int64_t launches = 0;
+  std::map<std::string, Stat> stats;
+  struct Pending {
+    std::string cls;
+    cudaEvent_t e0, e1;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double last_updates = 0.0;
+
+  static const KernelTable<T>& kernels() {
+    static KernelTable<T> t;
+    return t;
+  }
+
+  ~Engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& L : lv) {
+      cudaFree(L.u[0]);
+      cudaFree(L.u[1]);
+      cudaFree(L.b);
+      cudaFree(L.coef);
+    }
+    cudaFree(d_ainv);
+    cudaFree(d_active);
+    cudaFree(d_iters);
+    cudaFree(d_conv);
+    cudaFree(d_nactive);
+    cudaFree(d_parity);
+    cudaFree(d_ones);
+    cudaFree(d_r0);
+    cudaFree(d_hist);
+    cudaFree(d_partial);
+    cudaFree(d_norms);
+    cudaFree(d_stage);
+    if (h_nactive) cudaFreeHost(h_nactive);
+    for (auto& p : pending) {
+      cudaEventDestroy(p.e0);
+      cudaEventDestroy(p.e1);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ---- construction: host validation first (no CUDA), then device allocation ----------------
+  void setup_host(const pdmg_batch_desc& d) {
+    if (d.n_shifts < 1) throw ConfigError("pdmg_create: n_shifts must be >= 1");
+    if (d.n_shifts > 65535) throw ConfigError("pdmg_create: n_shifts must be <= 65535 per context");
+    if (!d.lambdas) throw ConfigError("pdmg_create: lambdas is NULL");
+    cfg = d.cfg;
+    ln = level_list(d.n, cfg);
+    S = d.n_shifts;
+    lambdas.resize(S);
+    for (int s = 0; s < S; ++s) lambdas[s] = cplx(d.lambdas[s].re, d.lambdas[s].im);
+    // smoother validity on every non-coarsest level (multigrid.cpp:47-58), in shift order
+    for (int s = 0; s < S; ++s)
+      for (size_t l = 0; l + 1 < ln.size(); ++l) {
+        const double h = 1.0 / ln[l];
+        try {
+          if (cfg.smoother == PDMG_SMOOTHER_VANKA) (void)vanka_coeffs(lambdas[s] * (h * h));
+          else (void)jacobi_weight(lambdas[s] * (h * h), h);
+        } catch (const SingularOperatorError& e) {
+          throw SingularOperatorError("level " + std::to_string(l) + " (n = " + std::to_string(ln[l]) + "): " + e.what());
+        }
+      }
+    if (ln.back() > 128)
+      throw ConfigError("dense_shifted_operator: dense assembly refused for n = " + std::to_string(ln.back()) +
+                        " (limit 128)");
+  }
+
+  void setup_device(int dev) {
+    device = dev;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (dev < 0 || dev >= ndev) throw CudaError("pdmg_create: CUDA device " + std::to_string(dev) + " not available");
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    table = &kernels();
+    const int L = (int)ln.size();
+    lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+      Level& Lv = lv[l];
+      Lv.n = ln[l];
+      Lv.m = Lv.n - 1;
+      Lv.ss = (int64_t)(Lv.n + 1) * Lv.n;
+      Lv.elems = (size_t)Lv.ss * S + Lv.n + 2;  // + guard so the last shift's ghost reads stay in bounds
+      for (V** p : {&Lv.u[0], &Lv.u[1], &Lv.b}) {
+        CK(cudaMalloc(p, Lv.elems * sizeof(V)));
+        CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
+      }
+      Lv.H = std::min(64, Lv.n + (Lv.n & 1));
+      Lv.ntx = (Lv.n + TILE_W - 1) / TILE_W;
+      Lv.nty = (Lv.n + Lv.H - 1) / Lv.H;
+      Lv.ntiles = Lv.ntx * Lv.nty;
+      // coefficients (multigrid.cpp:47-58 per level; smoother.cpp:31-40 stencil; grid.cpp:73 diagonal)
+      std::vector<LevelCoef<T>> hc(S);
+      const double h = 1.0 / Lv.n;
+      for (int s = 0; s < S; ++s) {
+        const cplx eta = lambdas[s] * (h * h);
+        const cplx dd = cplx(4.0, 0.0) + eta;
+        cplx k0(0, 0), k1(0, 0), k2(0, 0);
+        if (l + 1 < L) {
+          if (cfg.smoother == PDMG_SMOOTHER_VANKA) {
+            const Vanka v = vanka_coeffs(eta);
+            const double sc = cfg.omega * (h * h / 4.0);
+            k0 = sc * (4.0 * v.a);
+            k1 = sc * (2.0 * v.b);
+            k2 = sc * v.c;
+          } else {
+            k0 = cfg.omega * jacobi_weight(eta, h);
+          }
+        }
+        LevelCoef<T>& c = hc[s];
+        c.d.x = (T)dd.real(), c.d.y = (T)dd.imag();
+        c.k0.x = (T)k0.real(), c.k0.y = (T)k0.imag();
+        c.k1.x = (T)k1.real(), c.k1.y = (T)k1.imag();
+        c.k2.x = (T)k2.real(), c.k2.y = (T)k2.imag();
+        c.inv_h2 = (T)(1.0 / (h * h));
+        c.pad_ = 0;
+      }
+      CK(cudaMalloc(&Lv.coef, sizeof(LevelCoef<T>) * S));
+      CK(cudaMemcpyAsync(Lv.coef, hc.data(), sizeof(LevelCoef<T>) * S, cudaMemcpyHostToDevice, stream));
+    }
+    // coarsest factorizations (dense.cpp:82-88), one per shift
+    const int nc = ln.back(), mc = nc - 1;
+    coarse_N = mc * mc;
+    coarse_singular.assign(S, 0);
+    std::vector<V> hinv((size_t)S * coarse_N * coarse_N);
+    for (int s = 0; s < S; ++s) {
+      CoarseFactor cf = factor_coarse(nc, lambdas[s]);
+      coarse_singular[s] = cf.singular;
+      any_singular |= cf.singular;
+      for (size_t q = 0; q < cf.inv.size(); ++q) {
+        hinv[(size_t)s * coarse_N * coarse_N + q].x = (T)cf.inv[q].real();
+        hinv[(size_t)s * coarse_N * coarse_N + q].y = (T)cf.inv[q].imag();
+      }
+    }
+    CK(cudaMalloc(&d_ainv, sizeof(V) * hinv.size()));
+    CK(cudaMemcpyAsync(d_ainv, hinv.data(), sizeof(V) * hinv.size(), cudaMemcpyHostToDevice, stream));
+    // solve state
+    int maxtiles = 1;
+    for (auto& Lv : lv) maxtiles = std::max(maxtiles, Lv.ntiles);
+    CK(cudaMalloc(&d_active, sizeof(int) * S));
+    CK(cudaMalloc(&d_iters, sizeof(int) * S));
+    CK(cudaMalloc(&d_conv, sizeof(int) * S));
+    CK(cudaMalloc(&d_nactive, sizeof(int)));
+    CK(cudaMalloc(&d_parity, sizeof(int) * (cfg.max_iter + 1)));
+    CK(cudaMalloc(&d_ones, sizeof(int) * S));
+    CK(cudaMalloc(&d_r0, sizeof(double) * S));
+    CK(cudaMalloc(&d_hist, sizeof(double) * S * (size_t)(cfg.max_iter + 1)));
+    CK(cudaMalloc(&d_partial, sizeof(double) * S * (size_t)maxtiles));
+    CK(cudaMalloc(&d_norms, sizeof(double) * S));
+    std::vector<int> ones(S, 1);
+    CK(cudaMemcpyAsync(d_ones, ones.data(), sizeof(int) * S, cudaMemcpyHostToDevice, stream));
+    CK(cudaMallocHost(&h_nactive, sizeof(int)));
+    for (auto& kv : table->e)
+      if (kv.fn) CK(cudaFuncSetAttribute(kv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.smem));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // ---- instrumentation ---------------------------------------------------------------------
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  template <class F>
+  void timed(const std::string& cls, double bytes, F&& launch) {
+    ++launches;
+    if (!profiling) {
+      launch();
+      return;
+    }
+    Pending p{cls, get_event(), get_event(), bytes};
+    CK(cudaEventRecord(p.e0, stream));
+    launch();
+    CK(cudaEventRecord(p.e1, stream));
+    pending.push_back(p);
+  }
+  void drain_stats() {
+    if (pending.empty()) return;
+    CK(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, p.e0, p.e1));
+      Stat& st = stats[p.cls];
+      st.launches += 1;
+      st.ms += ms;
+      st.bytes += p.bytes;
+      event_pool.push_back(p.e0);
+      event_pool.push_back(p.e1);
+    }
+    pending.clear();
+  }
+
+  // ---- kernel launch ------------------------------------------------------------------------
+  void level_pass(int l, const Variant& v, const V* uin, V* uout, const V* b, const V* ec, V* bc, const int* active,
+                  int n_act) {
+    const Level& Lv = lv[l];
+    LevelArgs<T> a{};
+    a.u_in = uin;
+    a.u_out = uout;
+    a.b = b;
+    a.ec = ec;
+    a.bc = bc;
+    a.partial = d_partial;
+    a.coef = Lv.coef;
+    a.active = active;
+    a.n = Lv.n;
+    a.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
+    a.ss = Lv.ss;
+    a.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
+    a.ntx = Lv.ntx;
+    a.ntiles = Lv.ntiles;
+    a.H = Lv.H;
+    const KernelEntry<T>& k = table->get(v);
+    const double pts = (double)n_act * Lv.m * Lv.m, S_ = sizeof(V);
+    double bpp = 0;  // algorithmic DRAM bytes per point
+    if (v.loadu) bpp += S_;
+    if (v.sweep || v.post != POST_NONE) bpp += S_;  // b
+    if (v.prolong) bpp += S_ / 4;
+    if (v.store || v.post == POST_RESID) bpp += S_;
+    if (v.post == POST_RESTRICT) bpp += S_ / 4;
+    const std::string cls = "L" + std::to_string(l) + ":" + v.name();
+    dim3 grid(Lv.ntiles, S);
+    timed(cls, pts * bpp, [&] { k.fn<<<grid, NTHREADS, k.smem, stream>>>(a); });
+  }
+
+  void coarse_solve(const V* b, V* u, const int* active) {
+    const Level& Lv = lv.back();
+    const int thr = std::min(1024, std::max(32, ((coarse_N + 31) / 32) * 32));
+    const double bytes = (double)S * coarse_N * (coarse_N + 2) * sizeof(V);
+    timed("coarse_solve", bytes, [&] {
+      k_coarse_solve<T><<<S, thr, coarse_N * sizeof(V), stream>>>(b, u, d_ainv, active, Lv.n, Lv.ss);
+    });
+  }
+
+  // ---- one cycle on level l (multigrid.cpp:63-77) -------------------------------------------
+  // zero: u on this level is known to be zero on entry (ec = 0 before recursing, multigrid.cpp:72;
+  // u = 0 before the first fine cycle, multigrid.cpp:90).  fuse_norm: leave ||b - L u||^2 partials of
+  // the updated fine iterate in d_partial (returns whether it did).
+  bool cycle_level(int l, bool zero, const int* active, int n_act, bool want_norm) {
+    Level& Lv = lv[l];
+    const int L = (int)lv.size();
+    const bool jac = cfg.smoother == PDMG_SMOOTHER_JACOBI;
+    if (l + 1 == L) {
+      coarse_solve(Lv.b, Lv.u[Lv.cur], active);
+      Lv.uzero = false;
+      return false;
+    }
+    Level& Lc = lv[l + 1];
+    if (zero) Lv.uzero = true;
+    for (int k = 0; k < cfg.nu1; ++k) {
+      const bool last = k == cfg.nu1 - 1;
+      Variant v{!Lv.uzero, false, true, last ? POST_RESTRICT : POST_NONE, true, jac};
+      level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, nullptr, Lc.b, active, n_act);
+      Lv.cur ^= 1;
+      Lv.uzero = false;
+    }
+    if (cfg.nu1 == 0) {
+      Variant v{!Lv.uzero, false, false, POST_RESTRICT, false, false};
+      level_pass(l, v, Lv.u[Lv.cur], nullptr, Lv.b, nullptr, Lc.b, active, n_act);
+    }
+    const int gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+    for (int g = 0; g < gamma; ++g) cycle_level(l + 1, g == 0, active, n_act, false);
+    const V* ec = Lc.u[Lc.cur];
+    bool normed = false;
+    if (cfg.nu2 > 0) {
+      for (int k = 0; k < cfg.nu2; ++k) {
+        const bool last = k == cfg.nu2 - 1;
+        const int post = (last && want_norm) ? POST_NORM : POST_NONE;
+        Variant v{k == 0 ? !Lv.uzero : true, k == 0, true, post, true, jac};
+        level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, k == 0 ? ec : nullptr, nullptr, active, n_act);
+        Lv.cur ^= 1;
+        Lv.uzero = false;
+        normed = post == POST_NORM;
+      }
+    } else {
+      Variant v{!Lv.uzero, true, false, want_norm ? POST_NORM : POST_NONE, true, false};
+      level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, ec, nullptr, active, n_act);
+      Lv.cur ^= 1;
+      Lv.uzero = false;
+      normed = want_norm;
+    }
+    return normed;
+  }
+
+  void finalize(int k, int ntiles) {
+    CK(cudaMemsetAsync(d_nactive, 0, sizeof(int), stream));
+    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive, S, cfg.max_iter, cfg.tol};
+    const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
+    timed("finalize", 0.0, [&] { k_finalize<<<blocks, threads, 0, stream>>>(d_partial, ntiles, k, st); });
+    CK(cudaMemcpyAsync(h_nactive, d_nactive, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    n_active_host = *h_nactive;
+  }
+
+  void unpack(const V* src, V* dst, int l) {
+    const Level& Lv = lv[l];
+    const int64_t total = (int64_t)S * Lv.m * Lv.m;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    timed("unpack", (double)total * 2 * sizeof(V),
+          [&] { k_unpack<T><<<blocks, 256, 0, stream>>>(src, dst, Lv.n, Lv.ss, total); });
+  }
+  void pack(const V* b0, const V* b1, const int* iters, const int* parity, V* dst, int l) {
+    const Level& Lv = lv[l];
+    const int64_t total = (int64_t)S * Lv.m * Lv.m;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    timed("pack", (double)total * 2 * sizeof(V),
+          [&] { k_pack<T><<<blocks, 256, 0, stream>>>(b0, b1, iters, parity, dst, Lv.n, Lv.ss, total); });
+  }
+
+  // ---- MultigridHierarchy::solve for all shifts (multigrid.cpp:85-110) -----------------------
+  void solve_device(const V* d_b, V* d_u, pdmg_solve_report* rep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(device));
+    Level& F = lv[0];
+    const int H = cfg.max_iter + 1;
+    unpack(d_b, F.b, 0);
+    CK(cudaMemsetAsync(F.u[0], 0, F.elems * sizeof(V), stream));
+    F.cur = 0;
+    CK(cudaMemcpyAsync(d_active, d_ones, sizeof(int) * S, cudaMemcpyDeviceToDevice, stream));
+    CK(cudaMemsetAsync(d_iters, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_conv, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_hist, 0, sizeof(double) * S * (size_t)H, stream));
+    // r0 = ||b|| (multigrid.cpp:91): residual of the zero guess
+    level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
+               nullptr, S);
+    finalize(0, F.ntiles);
+    std::vector<int> parity(H, 0);
+    if (any_singular && n_active_host > 0) {
+      std::vector<int> act(S);
+      CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < S; ++s)
+        if (act[s] && coarse_singular[s])
+          throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
+    }
+    double cycles_done = 0.0;  // sum over shifts of cycles run
+    for (int k = 1; k <= cfg.max_iter && n_active_host > 0; ++k) {
+      const int n_act = n_active_host;
+      const bool normed = cycle_level(0, k == 1, d_active, n_act, true);
+      if (!normed)
+        level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr, nullptr,
+                   d_active, n_act);
+      parity[k] = F.cur;
+      cycles_done += n_act;
+      finalize(k, F.ntiles);
+    }
+    CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
+    pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+    // updates per cycle per shift: (nu1+nu2) * sum_l m_l^2 * gamma^l over non-coarsest levels
+    double per_cycle = 0.0, visits = 1.0;
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+      per_cycle += (cfg.nu1 + cfg.nu2) * (double)lv[l].m * lv[l].m * visits;
+      if (cfg.cycle == PDMG_CYCLE_W) visits *= 2;
+    }
+    last_updates = per_cycle * cycles_done;
+    std::vector<int> it(S), cv(S);
+    std::vector<double> hist;
+    CK(cudaMemcpyAsync(it.data(), d_iters, sizeof(int) * S, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(cv.data(), d_conv, sizeof(int) * S, cudaMemcpyDeviceToHost, stream));
+    const bool need_hist = rep && (rep->residual_history || rep->rate);
+    if (need_hist) {
+      hist.resize((size_t)S * H);
+      CK(cudaMemcpyAsync(hist.data(), d_hist, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost, stream));
+    }
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    drain_stats();
+    if (rep) {
+      for (int s = 0; s < S; ++s) {
+        if (rep->iterations) rep->iterations[s] = it[s];
+        if (rep->converged) rep->converged[s] = (uint8_t)cv[s];
+        if (rep->residual_history)
+          std::memcpy(rep->residual_history + (size_t)s * H, hist.data() + (size_t)s * H, sizeof(double) * H);
+        if (rep->rate) rep->rate[s] = measured_rate(hist.data() + (size_t)s * H, it[s]);
+      }
+      rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  }
+
+  static double measured_rate(const double* hist, int iters) {  // multigrid.cpp:9-21
+    if (iters <= 0) return 0.0;
+    int count = std::min(5, iters - 1);
+    if (count == 0) count = 1;
+    double log_sum = 0.0;
+    for (int k = iters - count + 1; k <= iters; ++k) {
+      if (hist[k] == 0.0) return 0.0;
+      if (hist[k - 1] == 0.0) return 0.0;
+      log_sum += std::log(hist[k] / hist[k - 1]);
+    }
+    return std::exp(log_sum / count);
+  }
+
+  // ---- host I/O staging --------------------------------------------------------------------
+  V* stage(size_t elems) {
+    if (elems > stage_elems) {
+      cudaFree(d_stage);
+      d_stage = nullptr;
+      CK(cudaMalloc(&d_stage, elems * sizeof(V)));
+      stage_elems = elems;
+    }
+    return d_stage;
+  }
+  size_t compact_elems(int l) const { return (size_t)S * lv[l].m * lv[l].m; }
+  void h2d(const pdmg_c128* src, V* dst, size_t elems) {
+    static_assert(sizeof(V) == sizeof(pdmg_c128), "c128 host I/O only for c128 engines");
+    CK(cudaMemcpyAsync(dst, src, elems * sizeof(V), cudaMemcpyHostToDevice, stream));
+  }
+  void d2h(const V* src, pdmg_c128* dst, size_t elems) {
+    CK(cudaMemcpyAsync(dst, src, elems * sizeof(V), cudaMemcpyDeviceToHost, stream));
+  }
+  void check_level(int l, int need_coarser) const {
+    if (l < 0 || l + need_coarser >= (int)lv.size())
+      throw ConfigError("level index " + std::to_string(l) + " out of range for a " + std::to_string(lv.size()) +
+                        "-level hierarchy");
+  }
+
+  void solve_host(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) {
+    CK(cudaSetDevice(device));
+    const size_t N = compact_elems(0);
+    V* st = stage(2 * N);
+    h2d(b, st, N);
+    solve_device(st, st + N, rep);
+    d2h(st + N, u, N);
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  void cycle_host(pdmg_c128* u, const pdmg_c128* b) {
+    CK(cudaSetDevice(device));
+    if (any_singular)
+      throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
+    Level& F = lv[0];
+    const size_t N = compact_elems(0);
+    V* st = stage(2 * N);
+    h2d(b, st, N);
+    h2d(u, st + N, N);
+    unpack(st, F.b, 0);
+    F.cur = 0;
+    unpack(st + N, F.u[0], 0);
+    cycle_level(0, false, nullptr, S, false);
+    pack(F.u[F.cur], F.u[F.cur], nullptr, nullptr, st + N, 0);
+    d2h(st + N, u, N);
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    drain_stats();
+  }
+
+  // level operators ----------------------------------------------------------------------------
+  void op_smooth(int l, const pdmg_c128* u, const pdmg_c128* b, pdmg_c128* out) {
+    check_level(l, 1);
+    CK(cudaSetDevice(device));
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    V* st = stage(2 * N);
+    h2d(u, st, N);
+    h2d(b, st + N, N);
+    unpack(st, Lv.u[0], l);
+    unpack(st + N, Lv.b, l);
+    level_pass(l, Variant{true, false, true, POST_NONE, true, cfg.smoother == PDMG_SMOOTHER_JACOBI}, Lv.u[0], Lv.u[1],
+               Lv.b, nullptr, nullptr, nullptr, S);
+    pack(Lv.u[1], Lv.u[1], nullptr, nullptr, st, l);
+    d2h(st, out, N);
+    finish();
+  }
+  void op_residual(int l, const pdmg_c128* b, const pdmg_c128* u, pdmg_c128* r) {
+    check_level(l, 0);
+    CK(cudaSetDevice(device));
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    V* st = stage(2 * N);
+    h2d(u, st, N);
+    h2d(b, st + N, N);
+    unpack(st, Lv.u[0], l);
+    unpack(st + N, Lv.b, l);
+    level_pass(l, Variant{true, false, false, POST_RESID, false, false}, Lv.u[0], Lv.u[1], Lv.b, nullptr, nullptr,
+               nullptr, S);
+    pack(Lv.u[1], Lv.u[1], nullptr, nullptr, st, l);
+    d2h(st, r, N);
+    finish();
+  }
+  void op_restrict(int l, const pdmg_c128* fine, pdmg_c128* coarse) {
+    check_level(l, 1);
+    CK(cudaSetDevice(device));
+    Level &Lv = lv[l], &Lc = lv[l + 1];
+    const size_t N = compact_elems(l), Nc = compact_elems(l + 1);
+    V* st = stage(N + Nc);
+    h2d(fine, st, N);
+    unpack(st, Lv.b, l);
+    level_pass(l, Variant{false, false, false, POST_RESTRICT, false, false}, nullptr, nullptr, Lv.b, nullptr, Lc.b,
+               nullptr, S);
+    pack(Lc.b, Lc.b, nullptr, nullptr, st + N, l + 1);
+    d2h(st + N, coarse, Nc);
+    finish();
+  }
+  void op_prolong(int l, const pdmg_c128* coarse, pdmg_c128* fine) {
+    check_level(l, 1);
+    CK(cudaSetDevice(device));
+    Level &Lv = lv[l], &Lc = lv[l + 1];
+    const size_t N = compact_elems(l), Nc = compact_elems(l + 1);
+    V* st = stage(N + Nc);
+    h2d(coarse, st + N, Nc);
+    unpack(st + N, Lc.u[0], l + 1);
+    level_pass(l, Variant{false, true, false, POST_NONE, true, false}, nullptr, Lv.u[1], Lv.b, Lc.u[0], nullptr,
+               nullptr, S);
+    pack(Lv.u[1], Lv.u[1], nullptr, nullptr, st, l);
+    d2h(st, fine, N);
+    finish();
+  }
+  void op_norm(int l, const pdmg_c128* v, double* norms) {
+    check_level(l, 0);
+    CK(cudaSetDevice(device));
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    V* st = stage(N);
+    h2d(v, st, N);
+    unpack(st, Lv.b, l);
+    level_pass(l, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, Lv.b, nullptr, nullptr,
+               nullptr, S);
+    const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
+    timed("sum_partials", 0.0,
+          [&] { k_sum_partials<<<blocks, threads, 0, stream>>>(d_partial, Lv.ntiles, S, d_norms); });
+    CK(cudaMemcpyAsync(norms, d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, stream));
+    finish();
+  }
+  void op_coarse_solve(const pdmg_c128* b, pdmg_c128* u) {
+    CK(cudaSetDevice(device));
+    if (any_singular)
+      throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
+    const int l = (int)lv.size() - 1;
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    V* st = stage(2 * N);
+    h2d(b, st, N);
+    unpack(st, Lv.b, l);
+    coarse_solve(Lv.b, Lv.u[0], nullptr);
+    pack(Lv.u[0], Lv.u[0], nullptr, nullptr, st + N, l);
+    d2h(st + N, u, N);
+    finish();
+  }
+  void finish() {
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    drain_stats();
+  }
+};
+
+}  // namespace pdmg_b200
+
+using namespace pdmg_b200;
+
+struct pdmg_ctx {
+  std::unique_ptr<Engine<double>> e;
+};
+
+// ---------------------------------------------------------------------------------------------
+// extern "C" boundary
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* pdmg_last_error(void) { return g_last_error.c_str(); }
+int pdmg_abi_version(void) { return PDMG_B200_ABI_VERSION; }
+
+void pdmg_mg_config_default(pdmg_mg_config* c) {
+  c->cycle = PDMG_CYCLE_W;
+  c->nu1 = 1;
+  c->nu2 = 0;
+  c->coarsest_n = 8;
+  c->tol = 1e-8;
+  c->max_iter = 200;
+  c->smoother = PDMG_SMOOTHER_VANKA;
+  c->omega = 24.0 / 25.0;
+}
+
+int pdmg_create(const pdmg_batch_desc* d, pdmg_ctx** out) {
+  return guarded([&] {
+    if (!d || !out) throw ConfigError("pdmg_create: NULL argument");
+    *out = nullptr;
+    if (d->precision != PDMG_PREC_C128)
+      throw ConfigError("pdmg_create: precision " + std::to_string(d->precision) + " not supported (use PDMG_PREC_C128)");
+    auto e = std::make_unique<Engine<double>>();
+    e->device = -1;
+    e->setup_host(*d);  // all ConfigError / SingularOperatorError paths run before any CUDA call
+    e->setup_device(d->device);
+    auto* c = new pdmg_ctx;
+    c->e = std::move(e);
+    *out = c;
+  });
+}
+
+void pdmg_destroy(pdmg_ctx* c) { delete c; }
+int pdmg_num_levels(const pdmg_ctx* c) { return c ? (int)c->e->lv.size() : 0; }
+int pdmg_level_n(const pdmg_ctx* c, int l) {
+  return (c && l >= 0 && l < (int)c->e->lv.size()) ? c->e->lv[l].n : -1;
+}
+int pdmg_num_shifts(const pdmg_ctx* c) { return c ? c->e->S : 0; }
+int pdmg_coarse_singular(const pdmg_ctx* c, int s) {
+  return (c && s >= 0 && s < c->e->S) ? (int)c->e->coarse_singular[s] : -1;
+}
+
+#define NEED_CTX(c) \
+  if (!(c)) throw ConfigError("NULL pdmg_ctx")
+
+int pdmg_solve(pdmg_ctx* c, const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) {
+  return guarded([&] {
+    NEED_CTX(c);
+    if (!b || !u) throw ConfigError("pdmg_solve: NULL b or u");
+    c->e->solve_host(b, u, rep);
+  });
+}
+int pdmg_solve_device(pdmg_ctx* c, const void* d_b, void* d_u, pdmg_solve_report* rep) {
+  return guarded([&] {
+    NEED_CTX(c);
+    if (!d_b || !d_u) throw ConfigError("pdmg_solve_device: NULL b or u");
+    c->e->solve_device(static_cast<const double2*>(d_b), static_cast<double2*>(d_u), rep);
+  });
+}
+int pdmg_cycle(pdmg_ctx* c, pdmg_c128* u, const pdmg_c128* b) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->cycle_host(u, b);
+  });
+}
+int pdmg_apply_smoother(pdmg_ctx* c, int l, const pdmg_c128* u, const pdmg_c128* b, pdmg_c128* out) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->op_smooth(l, u, b, out);
+  });
+}
+int pdmg_residual(pdmg_ctx* c, int l, const pdmg_c128* b, const pdmg_c128* u, pdmg_c128* r) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->op_residual(l, b, u, r);
+  });
+}
+int pdmg_restrict_full_weighting(pdmg_ctx* c, int l, const pdmg_c128* f, pdmg_c128* co) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->op_restrict(l, f, co);
+  });
+}
+int pdmg_prolong_bilinear(pdmg_ctx* c, int l, const pdmg_c128* co, pdmg_c128* f) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->op_prolong(l, co, f);
+  });
+}
+int pdmg_norm(pdmg_ctx* c, int l, const pdmg_c128* v, double* norms) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->op_norm(l, v, norms);
+  });
+}
+int pdmg_coarse_solve(pdmg_ctx* c, const pdmg_c128* b, pdmg_c128* u) {
+  return guarded([&] {
+    NEED_CTX(c);
+    c->e->op_coarse_solve(b, u);
+  });
+}
+
+void pdmg_random_rhs(uint32_t seed, double lo, double hi, int64_t count, pdmg_c128* out) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> dist(lo, hi);
+  for (int64_t k = 0; k < count; ++k) {
+    const double re = dist(rng), im = dist(rng);
+    out[k].re = re;
+    out[k].im = im;
+  }
+}
+
+void pdmg_circulant_shifts(double alpha, int32_t nt, double dt, int32_t j0, int32_t count, pdmg_c128* out) {
+  const double g = std::pow(alpha, 1.0 / nt);
+  for (int q = 0; q < count; ++q) {
+    const double ang = 2.0 * M_PI * (double)(j0 + q) / (double)nt;
+    const cplx lam = (cplx(1.0, 0.0) - g * std::exp(cplx(0.0, ang))) / dt;
+    out[q].re = lam.real();
+    out[q].im = lam.imag();
+  }
+}
+
+void* pdmg_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+void pdmg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+void* pdmg_stream(pdmg_ctx* c) { return c ? (void*)c->e->stream : nullptr; }
+int pdmg_set_profiling(pdmg_ctx* c, int on) {
+  if (!c) return PDMG_ERR_CONFIG;
+  c->e->profiling = on != 0;
+  return PDMG_OK;
+}
+void pdmg_reset_stats(pdmg_ctx* c) {
+  if (!c) return;
+  c->e->stats.clear();
+  c->e->launches = 0;
+}
+int64_t pdmg_launch_count(const pdmg_ctx* c) { return c ? c->e->launches : 0; }
+int pdmg_kernel_stats(const pdmg_ctx* c, int i, char* name, size_t name_len, int64_t* launches, double* total_ms,
+                      double* algo_bytes) {
+  if (!c || i < 0 || i >= (int)c->e->stats.size()) return 1;
+  auto it = c->e->stats.begin();
+  std::advance(it, i);
+  if (name && name_len) {
+    std::strncpy(name, it->first.c_str(), name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (launches) *launches = it->second.launches;
+  if (total_ms) *total_ms = it->second.ms;
+  if (algo_bytes) *algo_bytes = it->second.bytes;
+  return 0;
+}
+double pdmg_last_updates(const pdmg_ctx* c) { return c ? c->e->last_updates : 0.0; }
+
+int pdmg_paradiag_circulant(int32_t, int32_t, double, double, const pdmg_mg_config*, int32_t, const pdmg_c128*,
+                            pdmg_c128*, pdmg_solve_report*, double*) {
+  g_last_error = "pdmg_paradiag_circulant: not implemented yet";
+  return PDMG_ERR_RUNTIME;
+}
+
+}  // extern "C"

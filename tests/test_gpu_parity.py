@@ -1,0 +1,178 @@
+"""GPU parity: every operator and full solves through the C ABI vs the CPU oracle (oracle/pdmg_oracle.c).
+
+Tolerances (BASELINE.json north_star): complex128 solution and residual history within 1e-10 relative,
+identical per-shift V-cycle counts.  Single operators agree to ~1e-14 (FMA contraction and a
+re-associated 9-point sum are the only differences), checked at 1e-12.
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import Cfg
+
+pytestmark = pytest.mark.gpu
+
+import paper_2203_11154_b200 as P  # noqa: E402
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.linalg.norm((a - b).ravel())
+    s = np.linalg.norm(b.ravel())
+    return d / s if s > 0 else d
+
+
+def mgcfg(c: Cfg) -> P.MultigridConfig:
+    sm = P.SmootherConfig.vanka(c.omega) if c.smoother == "vanka" else P.SmootherConfig.jacobi(c.omega)
+    return P.MultigridConfig(P.CycleKind.V if c.cycle == "V" else P.CycleKind.W, c.nu1, c.nu2, c.coarsest_n, c.tol,
+                             c.max_iter, sm)
+
+
+LAMS = [0.0, 8.959263353215057 - 15.395328029306036j, 1000 + 1000j, -50j, 31.4 + 2j]
+
+
+@pytest.mark.parametrize("n,coarsest", [(8, 4), (16, 8), (64, 4), (136, 17)])
+@pytest.mark.parametrize("kind", ["vanka", "jacobi"])
+def test_smoother_residual_parity(oracle, n, coarsest, kind):
+    """Includes a non-power-of-two grid (136 = 8*17) whose tiles are ragged at the right/top edges."""
+    cfg = Cfg(coarsest_n=coarsest, smoother=kind, omega=0.96 if kind == "vanka" else 0.8)
+    m = n - 1
+    S = len(LAMS)
+    u = oracle.random_complex(11, S * m * m).reshape(S, m, m)
+    b = oracle.random_complex(12, S * m * m).reshape(S, m, m)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), LAMS, mgcfg(cfg)) as H:
+        su = H.apply_smoother(0, u, b)
+        r = H.residual(0, b, u)
+        nr = H.norm(0, b)
+    for s, lam in enumerate(LAMS):
+        assert rel(su[s], oracle.smooth(n, lam, u[s], b[s], kind, cfg.omega)) < 1e-12
+        assert rel(r[s], oracle.residual(n, lam, b[s], u[s])) < 1e-12
+        assert abs(nr[s] - oracle.norm(n, b[s])) <= 1e-13 * oracle.norm(n, b[s])
+
+
+@pytest.mark.parametrize("n", [8, 64, 256])
+def test_transfer_parity(oracle, n):
+    m, mc = n - 1, n // 2 - 1
+    S = 3
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0] * S, P.MultigridConfig(coarsest_n=4)) as H:
+        f = oracle.random_complex(5, S * m * m).reshape(S, m, m)
+        c = oracle.random_complex(6, S * mc * mc).reshape(S, mc, mc)
+        R = H.restrict_full_weighting(0, f)
+        Pp = H.prolong_bilinear(0, c)
+    for s in range(S):
+        assert rel(R[s], oracle.restrict(n, f[s])) < 1e-14
+        assert rel(Pp[s], oracle.prolong(n // 2, c[s])) < 1e-15
+
+
+def test_coarse_solve_parity(oracle):
+    lams = [0.0, 3 + 4j, -100j]
+    with P.BatchedMultigridHierarchy(P.Grid2D(8), lams, P.MultigridConfig(coarsest_n=4)) as H:
+        b = oracle.random_complex(7, 3 * 9).reshape(3, 3, 3)
+        u = H.coarse_solve(b)
+    for s, lam in enumerate(lams):
+        r = oracle.residual(4, lam, b[s], u[s])
+        assert np.linalg.norm(r) <= 1e-12 * np.linalg.norm(b[s])
+
+
+@pytest.mark.parametrize("cyc", [Cfg(), Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8),
+                                 Cfg(nu1=2, nu2=2), Cfg(nu1=0, nu2=2), Cfg(nu1=2, nu2=0),
+                                 Cfg(smoother="jacobi", omega=0.8)])
+def test_one_cycle_parity(oracle, cyc):
+    n = 64
+    m = n - 1
+    lams = [0.0, 8.959263353215057 - 15.395328029306036j]
+    u = oracle.random_complex(21, 2 * m * m).reshape(2, m, m)
+    b = oracle.random_complex(22, 2 * m * m).reshape(2, m, m)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, mgcfg(cyc)) as H:
+        out = H.cycle(u, b)
+    for s, lam in enumerate(lams):
+        assert rel(out[s], oracle.cycle(n, lam, cyc, u[s], b[s])) < 1e-12
+
+
+def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10):
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, mgcfg(cfg)) as H:
+        u, reps = H.solve(b)
+    ref = oracle.solve_batch(n, np.asarray(lams, np.complex128), cfg, b, threads=8)
+    for s in range(len(lams)):
+        it = int(ref["iterations"][s])
+        assert reps[s].iterations == it, (s, reps[s].iterations, it)
+        assert reps[s].converged == bool(ref["converged"][s])
+        hist_ref = ref["hist"][s, : it + 1]
+        assert np.max(np.abs(reps[s].residual_history - hist_ref) / hist_ref[0]) < tol_rel
+        assert rel(u[s], ref["u"][s]) < tol_rel
+        # rate is a geometric mean of ratios of residuals ~1e-10 r0, so it inherits their relative error
+        assert abs(reps[s].rate - ref["rates"][s]) <= 1e-6 * ref["rates"][s]
+    return u, reps, ref
+
+
+def test_config1_single_shift(oracle):
+    """BASELINE config 1: h=1/64, lambda_3 of the n=32 circulant family, seed 0, V(1,1), tol 1e-10."""
+    lam = oracle.circulant_shifts(0.01, 32, 1 / 32, 3, 1)
+    b = oracle.random_complex(0, 63 * 63).reshape(1, 63, 63)
+    u, reps, ref = _check_solve(oracle, 64, lam, b, Cfg())
+    assert reps[0].iterations == 11
+
+
+def test_config2_batch32(oracle):
+    """BASELINE config 2: h=1/128, 32 shifts, seed 1 shift-major, V(1,1): 11-12 cycles per shift."""
+    lams = oracle.circulant_shifts(0.01, 32, 1 / 32)
+    b = oracle.random_complex(1, 32 * 127 * 127).reshape(32, 127, 127)
+    u, reps, ref = _check_solve(oracle, 128, lams, b, Cfg())
+    assert set(r.iterations for r in reps) <= {11, 12}
+
+
+def test_readme_w10_rates(oracle):
+    """proj/README.md:37-41: W(1,0) at h=1/64, lambda=0: Vanka 14 cycles (0.273), Jacobi 32 (0.590)."""
+    b = oracle.random_complex(123, 63 * 63).reshape(1, 63, 63)
+    _, rv, _ = _check_solve(oracle, 64, [0.0], b, Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8))
+    _, rj, _ = _check_solve(oracle, 64, [0.0], b, Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8,
+                                                       smoother="jacobi", omega=0.8))
+    assert rv[0].iterations == 14 and abs(rv[0].rate - 0.273) < 0.001
+    assert rj[0].iterations == 32 and abs(rj[0].rate - 0.590) < 0.001
+
+
+def test_config3_subset(oracle):
+    """BASELINE config 3 shape (h=1/512, V(2,2), alpha=1e-3, dt=1/256) on 4 of its 256 shifts."""
+    n, m = 512, 511
+    lams = oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, 256)[[0, 1, 128, 255]]
+    b = oracle.random_complex(2, 4 * m * m).reshape(4, m, m)
+    _check_solve(oracle, n, lams, b, Cfg(nu1=2, nu2=2))
+
+
+def test_edge_cases(oracle):
+    """multigrid test 'report edge cases' (test_multigrid.cpp:128-163) on the GPU path."""
+    n = 16
+    m = n - 1
+    b = np.zeros((3, m, m), np.complex128)
+    b[1] = oracle.random_complex(1, m * m).reshape(m, m)
+    b[2] = oracle.random_complex(2, m * m).reshape(m, m)
+    # shift 0: b = 0 converges at 0 iterations; others run
+    cfg = Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0, 0.0, 0.0], mgcfg(cfg)) as H:
+        u, reps = H.solve(b)
+    assert reps[0].converged and reps[0].iterations == 0 and reps[0].rate == 0.0
+    assert np.all(u[0] == 0)
+    assert list(reps[0].residual_history) == [0.0]
+    # max_iter exhaustion reports non-convergence
+    cfg2 = Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-14, max_iter=1)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0], mgcfg(cfg2)) as H:
+        u, reps = H.solve(b[2:3])
+    assert not reps[0].converged and reps[0].iterations == 1
+    h = reps[0].residual_history
+    assert abs(reps[0].rate - h[1] / h[0]) < 1e-12
+    # tol >= 1 converges with zero iterations
+    cfg3 = Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1.0)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0], mgcfg(cfg3)) as H:
+        u, reps = H.solve(b[1:2])
+    assert reps[0].converged and reps[0].iterations == 0
+
+
+def test_singular_coarse_detected():
+    """test_multigrid.cpp:174-185: lambda = -mu_11 of the coarsest grid raises at solve."""
+    cg = 8
+    h = 1 / cg
+    mu = (4 - 2 * np.cos(np.pi * h) - 2 * np.cos(np.pi * h)) / (h * h)
+    cfg = P.MultigridConfig()
+    with P.BatchedMultigridHierarchy(P.Grid2D(16), [-mu], cfg) as H:
+        assert H.coarse_singular(0)
+        with pytest.raises(P.SingularOperatorError, match="singular on grid n = 8"):
+            H.solve(P.random_rhs(16, 3).reshape(1, 15, 15))
