@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""Benchmark: batched complex-shifted-Laplacian multigrid solves on B200 (BASELINE.json metric).
+
+A "step" is one full batched solve (every shift to relative residual 1e-10) of the workload's shifts.
+Default workload = BASELINE config 3: h=1/512 (511x511 interior), n=256 shifts
+lambda_j = (1 - alpha^(1/n) e^(2 pi i j/n))/dt with alpha=1e-3, dt=1/256, RHS uniform[-1,1]^2 from
+std::mt19937(2) drawn shift-major, V(2,2) Vanka cycles (omega = 24/25), coarsest 3x3, complex128.
+Shifts are sharded contiguously over ranks (paradiag.cpp:217-236 chunking); there is no data-path
+collective, so `value` = all ranks' updates / max-over-ranks time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (n, n_shifts, alpha, n_t, dt, seed, nu1, nu2, description)
+    "c1": (64, 1, 0.01, 32, 1 / 32, 0, 1, 1, "C1: n=64 (63x63), 1 shift (j=3 of n_t=32, alpha=0.01, dt=1/32), V(1,1), seed 0"),
+    "c2": (128, 32, 0.01, 32, 1 / 32, 1, 1, 1, "C2: n=128 (127x127), 32 shifts (alpha=0.01, dt=1/32), V(1,1), seed 1"),
+    "c3": (512, 256, 1e-3, 256, 1 / 256, 2, 2, 2,
+           "C3: n=512 (511x511), 256 shifts (alpha=1e-3, dt=1/256), V(2,2), seed 2"),
+    "c4a": (1024, 1024, 0.01, 1024, 1 / 1024, 3, 1, 1,
+            "C4 set A: n=1024 (1023x1023), 1024 shifts (alpha=0.01, dt=1/1024), V(1,1), seed 3"),
+}
+METRIC = "complex grid-point smoother updates/sec"
+UNIT = "updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shifts", type=int, default=0, help="override the number of shifts (0 = config's)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(S: int, rank: int, world: int):
+    """Contiguous chunks of ceil(S/world) shifts, as paradiag_solve's thread pool (paradiag.cpp:222-224)."""
+    chunk = (S + world - 1) // world
+    b0 = min(S, rank * chunk)
+    return b0, min(S, b0 + chunk)
+
+
+def updates_per_cycle(n: int, nu1: int, nu2: int, coarsest: int = 4) -> float:
+    tot, g = 0.0, n
+    while g > coarsest:
+        tot += (nu1 + nu2) * (g - 1) ** 2
+        g //= 2
+    return tot
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_run(n, lams, nu1, nu2, b, threads):
+    """Reference CPU path: the reference's own grid.cpp/smoother.cpp (oracle/_ref) when built, else the C port.
+    Shifts split over `threads` std::threads in contiguous chunks (paradiag.cpp:217-236)."""
+    from oracle_lib import Cfg, Oracle, RefLib
+
+    cfg = Cfg(nu1=nu1, nu2=nu2)
+    try:
+        lib, kind = RefLib(), "reference"
+    except (FileNotFoundError, OSError):
+        lib, kind = Oracle(), "port"
+    t = time.perf_counter()
+    out = lib.solve_batch(n, lams, cfg, b, threads=threads)
+    dt = time.perf_counter() - t
+    return out, dt, kind
+
+
+def cpu_sample(n, lams_all, nu1, nu2, seed, threads, budget_s):
+    """Time a bounded, contiguous sample of the workload's shifts on the host cores."""
+    from oracle_lib import Oracle
+
+    o = Oracle()
+    m = n - 1
+    upc = updates_per_cycle(n, nu1, nu2)
+    b1 = o.random_complex(seed, m * m).reshape(1, m, m)
+    _, t1, _ = cpu_reference_run(n, lams_all[:1], nu1, nu2, b1, 1)  # calibrate one shift on one core
+    count = int(max(threads, min(len(lams_all), threads * max(1, round(budget_s / max(t1, 1e-3))))))
+    count = min(count, len(lams_all))
+    b = o.random_complex(seed, count * m * m).reshape(count, m, m)
+    out, dt, kind = cpu_reference_run(n, lams_all[:count], nu1, nu2, b, threads)
+    upd = float(np.sum(out["iterations"])) * upc
+    return dict(value=upd / dt, unit=UNIT, cores=threads, kind=kind,
+                sample=f"shifts 0..{count - 1} of the workload ({count} of {len(lams_all)}), "
+                       f"{threads} std::threads, {dt:.2f} s wall",
+                shifts_per_s=count / dt, seconds=dt)
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    n, S, alpha, nt, dt, seed, nu1, nu2, desc = CONFIGS[args.config]
+    from oracle_lib import Oracle
+
+    o = Oracle()
+    lams = o.circulant_shifts(alpha, nt, dt, 0, S)
+    threads = os.cpu_count() or 1
+    m = n - 1
+    upc = updates_per_cycle(n, nu1, nu2)
+    # per step: a bounded sample of `threads` shifts (one per core), cycling through the shift list
+    per = min(S, threads)
+    vals, times, kind = [], [], "port"
+    for step in range(args.warmup + args.steps):
+        j0 = (step * per) % S
+        idx = [(j0 + q) % S for q in range(per)]
+        b = o.random_complex(seed + 1000 * step, per * m * m).reshape(per, m, m)
+        out, t, kind = cpu_reference_run(n, lams[idx], nu1, nu2, b, threads)
+        if step >= args.warmup:
+            vals.append(float(np.sum(out["iterations"])) * upc / t)
+            times.append(t)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": desc, "sample_per_step": f"{per} shifts on {threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{per} shifts per step (one per core) of {args.config}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    rank, world, local = dist_env()
+    import torch
+
+    import paper_2203_11154_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, S, alpha, nt, dt, seed, nu1, nu2, desc = CONFIGS[args.config]
+    if args.shifts:
+        S = args.shifts
+    m = n - 1
+    b0, b1 = shard(S, rank, world)
+    Sr = b1 - b0
+    lams_all = P.circulant_shifts(alpha, nt, dt, 0, S)
+    lams = lams_all[b0:b1]
+    cfg = P.MultigridConfig(P.CycleKind.V, nu1, nu2, 4, 1e-10, 200, P.SmootherConfig.vanka())
+    # inputs: one mt19937(seed) stream, shift-major; each rank keeps its shard
+    b_all = P.random_rhs(n, seed, count=b1)
+    b_host = np.ascontiguousarray(b_all.reshape(b1, m, m)[b0:b1])
+    del b_all
+    H = P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg, device=local)
+    stream = torch.cuda.ExternalStream(H.stream)
+    d_b = torch.from_numpy(b_host.view(np.float64)).to(f"cuda:{local}")
+    d_u = torch.empty_like(d_b)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    # ---- warm-up ---------------------------------------------------------------------------
+    reps = None
+    for _ in range(args.warmup):
+        reps = H.solve_device(d_b.data_ptr(), d_u.data_ptr())
+    # ---- timed region: device-resident inputs, CUDA events on the library's stream ----------
+    H.reset_stats()
+    H.set_profiling(True)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+        upd = 0.0
+        for _ in range(args.steps):
+            reps = H.solve_device(d_b.data_ptr(), d_u.data_ptr())
+            upd += H.last_updates()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = H.launch_count()
+    stats = H.kernel_stats()
+    H.set_profiling(False)
+    ms_max = max_over_ranks(ms)
+    upd_all = sum_over_ranks(upd)
+    value = upd_all / (ms_max / 1e3)
+    shifts_per_s = args.steps * S / (ms_max / 1e3)
+    iters = [r.iterations for r in reps]
+    conv = all(r.converged for r in reps)
+
+    # ---- end to end through the host API: pinned host b -> device -> solve -> host u ----------
+    import ctypes
+
+    from paper_2203_11154_b200 import _native as N
+
+    nbytes = b_host.nbytes
+    hb = N.lib().pdmg_host_alloc(nbytes)
+    hu = N.lib().pdmg_host_alloc(nbytes)
+    ctypes.memmove(hb, b_host.ctypes.data, nbytes)
+    e_steps = max(1, min(args.steps, 3))
+    rep = N.SolveReport(0, 0, 0, 0, 0.0)
+    H.solve_device(d_b.data_ptr(), d_u.data_ptr(), want_reports=False)  # keep state warm
+    barrier()
+    t0 = time.perf_counter()
+    e_upd = 0.0
+    for _ in range(e_steps):
+        st = N.lib().pdmg_solve(H._h, hb, hu, ctypes.byref(rep))
+        assert st == 0, N.lib().pdmg_last_error()
+        e_upd += H.last_updates()
+    barrier()
+    e_s = time.perf_counter() - t0
+    e_s_max = max_over_ranks(e_s)
+    e_value = sum_over_ranks(e_upd) / e_s_max
+    N.lib().pdmg_host_free(hb)
+    N.lib().pdmg_host_free(hu)
+
+    # ---- roofline of the dominant kernel ------------------------------------------------------
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md 6650 GB/s)"
+    peak = peak or 6650.0
+    top_name, top = max(((k, v) for k, v in stats.items() if k.startswith("L")), key=lambda kv: kv[1]["ms"])
+    total_ms = sum(v["ms"] for v in stats.values())
+    achieved = top["bytes"] / (top["ms"] / 1e3) / 1e9
+    all_bytes = sum(v["bytes"] for v in stats.values())
+    roofline = {"bound": "hbm", "kernel": top_name, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "kernel_share_of_step": round(top["ms"] / total_ms, 4),
+                "launch_avg_ms": round(top["ms"] / top["launches"], 4),
+                "algo_bytes_per_launch": top["bytes"] / top["launches"],
+                "all_kernels_algorithmic_GBps": round(all_bytes / (total_ms / 1e3) / 1e9, 1)}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(args.config, {}).get(top_name)
+            if tr:
+                roofline["traffic"] = tr
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            lam_np = np.asarray(lams_all, np.complex128)
+            cpu = cpu_sample(n, lam_np, nu1, nu2, seed, os.cpu_count() or 1, budget_s=10.0)
+        except Exception as e:  # the baseline is reported, never required for the GPU number
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": desc + (f" [{S} shifts]" if args.shifts else ""), "shifts": S,
+                       "shifts_per_rank": Sr, "parallelism": f"shift-sharded x{world}",
+                       "l2": "inputs larger than L2 (each fine array %.2f GB)" % (S * (n + 1) * n * 16 / 1e9)
+                       if S * (n + 1) * n * 16 > 126e6 else "working set fits in L2 (latency-bound config)"},
+            "shifts_per_s": shifts_per_s, "cycles_per_shift": sorted(set(iters)), "all_converged": conv,
+            "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                    "steps": e_steps, "ms_per_step": 1e3 * e_s_max / e_steps},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                            "GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] > 0 else None}
+                        for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])[:12]},
+        }
+        print(json.dumps(line), flush=True)
+    H.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -229,7 +229,7 @@ struct KernelTable {
   void reg() {
     const int k = (LU ? 1 : 0) | (PR ? 2 : 0) | (SW ? 4 : 0) | (PO << 3) | (ST ? 32 : 0) | (JA ? 64 : 0);
     e[k].fn = &k_level<T, LU, PR, SW, PO, ST, JA>;
-    e[k].smem = LevelSmem<T, SW, PO>::bytes;
+    e[k].smem = LevelShape<T, LU || PR || !SW, SW, PO, PR>::bytes;
   }
   template <bool LU, bool PR, int PO, bool JA>
   void reg_sweep() {
@@ -409,7 +409,7 @@ struct Engine {
         CK(cudaMalloc(p, Lv.elems * sizeof(V)));
         CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
       }
-      Lv.H = std::min(64, Lv.n + (Lv.n & 1));
+      Lv.H = std::min(Lv.n >= 512 ? 128 : 64, Lv.n + (Lv.n & 1));
       Lv.ntx = (Lv.n + TILE_W - 1) / TILE_W;
       Lv.nty = (Lv.n + Lv.H - 1) / Lv.H;
       Lv.ntiles = Lv.ntx * Lv.nty;
