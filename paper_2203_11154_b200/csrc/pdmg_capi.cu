@@ -229,7 +229,7 @@ struct KernelTable {
   void reg() {
     const int k = (LU ? 1 : 0) | (PR ? 2 : 0) | (SW ? 4 : 0) | (PO << 3) | (ST ? 32 : 0) | (JA ? 64 : 0);
     e[k].fn = &k_level<T, LU, PR, SW, PO, ST, JA>;
-    e[k].smem = LevelShape<T, LU || PR || !SW, SW, PO, PR>::bytes;
+    e[k].smem = LevelShape<T, LU || PR, SW, PO, PR>::bytes;
   }
   template <bool LU, bool PR, int PO, bool JA>
   void reg_sweep() {
@@ -250,7 +250,9 @@ struct KernelTable {
   KernelTable() {
     reg_sweep4<POST_NONE>();
     reg_sweep4<POST_NORM>();
-    reg_sweep4<POST_RESTRICT>();
+    // restriction follows pre-smoothing only, which never prolongates
+    reg_sweep2<false, false, POST_RESTRICT>();
+    reg_sweep2<true, false, POST_RESTRICT>();
     // prolongate-and-correct without a sweep (nu2 == 0)
     reg<false, true, false, POST_NONE, true, false>();
     reg<true, true, false, POST_NONE, true, false>();

@@ -83,11 +83,12 @@ constexpr int TILE_W = 64;    // output columns per CTA
 constexpr int CHUNK = 16;     // rows each stage advances per step
 constexpr int RING = 18;      // rows of the r / delta rings (= CHUNK + 2: a stage reads its producer's rows -1..CHUNK)
 constexpr int RING_R = 20;    // ... when the restriction (which looks 2 more rows back) consumes them
-constexpr int ARING = 34;     // rows of the u_in ring: the 18 rows in use + the next chunk landing (cp.async)
+constexpr int ARING = 34;     // rows of the u_in ring: the 18 rows in use + the next chunk landing (TMA)
 constexpr int RPT = 4;        // rows per stencil task (register-blocked along the column)
 constexpr int RGROUPS = CHUNK / RPT;
 constexpr int NTHREADS = 288; // 9 warps >= (TILE_W + 2*hB) * RGROUPS tasks for every variant
 constexpr int CB_ROWS = 10, CB_COLS = 40;  // coarse block for prolongation (CHUNK/2 + 2 rows, (TILE_W+8)/2 + 4 cols)
+constexpr int VX_W = TILE_W + 2;           // restriction exchange row width
 
 template <class T>
 struct LevelArgs {
@@ -107,26 +108,31 @@ struct LevelArgs {
 
 __device__ __forceinline__ int floordiv2(int a) { return a >> 1; }  // arithmetic shift = floor(a/2)
 
-// 16-byte global->shared async copy; src_bytes = 0 zero-fills (used for every non-interior node, which
-// is how the homogeneous Dirichlet boundary enters the stencil stages).
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  const int nbytes = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(nbytes) : "memory");
+// ---- TMA bulk copies (cp.async.bulk, 1-D) completing on an mbarrier ------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// Circular row buffer: rows map to slots row mod NROWS (rows are >= -NROWS).
-template <class T, int HALO, int NROWS>
-struct Ring {
-  using V = typename vec2<T>::type;
-  static constexpr int WIDTH = TILE_W + 2 * HALO;
-  V* p;
-  int c_lo;  // storage column of local column 0
-  __device__ __forceinline__ V* row_ptr(int row) const { return p + ((row + NROWS) % NROWS) * WIDTH - c_lo; }
-  __device__ __forceinline__ V& at(int row, int col) const { return row_ptr(row)[col]; }
-};
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // Halo widths and shared-memory footprint of a k_level instantiation.
 template <class T, bool USE_A, bool SWEEP, int POST, bool PROLONG>
@@ -139,8 +145,9 @@ struct LevelShape {
   static constexpr int WA = TILE_W + 2 * hA, WB = TILE_W + 2 * hB, WC = TILE_W + 2 * hC;
   static constexpr int RR = POST == POST_RESTRICT ? RING_R : RING;  // rows of the r / delta rings
   static constexpr size_t elems = (size_t)(USE_A ? ARING * WA : 0) + (SWEEP ? (CHUNK + RR) * WB : 0) +
-                                  (SWEEP && HASD ? RR * WC : 0) + (PROLONG ? CB_ROWS * CB_COLS : 0);
-  static constexpr size_t bytes = elems * sizeof(typename vec2<T>::type) + 16 * sizeof(double);
+                                  (SWEEP && HASD ? RR * WC : 0) + (PROLONG ? CB_ROWS * CB_COLS : 0) +
+                                  (POST == POST_RESTRICT ? 2 * RGROUPS * VX_W : 0);
+  static constexpr size_t bytes = 32 + elems * sizeof(typename vec2<T>::type) + 16 * sizeof(double);
   // CTAs per SM the shared memory allows (227 KB usable); used as the register budget hint
   static constexpr int min_blocks = bytes <= 75 * 1024 ? 3 : 2;
   static_assert(!SWEEP || WB * RGROUPS <= NTHREADS, "stage-B tasks exceed the CTA");
@@ -150,17 +157,20 @@ struct LevelShape {
 // Stage row ranges: stage x (A=0, B=1, C=2, D=3) handles, in step t, rows [base - x + CHUNK t, +CHUNK)
 // clipped to [r0 - h_x, r0 + H + h_x), where base = r0 - hA.  Consecutive stages lag one row, so a
 // stage only ever reads rows its producer finished in this step or the previous one.  The inputs of
-// step t+1 (u rows, b rows, coarse block) are copied asynchronously while step t computes.
+// step t+1 (u rows, b rows, coarse block) stream in by TMA while step t computes.  Ring slots outside
+// the interior may hold stale data: every stage masks by interior(), and the one-node ghost ring that
+// the 5-point operator reads is zero in global memory (and copied).
 template <class T, bool LOADU, bool PROLONG, bool SWEEP, int POST, bool STORE, bool JACOBI>
-__global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG || !SWEEP, SWEEP, POST, PROLONG>::min_blocks))
+__global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWEEP, POST, PROLONG>::min_blocks))
     k_level(LevelArgs<T> a) {
   using V = typename vec2<T>::type;
-  constexpr bool USE_A = LOADU || PROLONG || !SWEEP;
+  constexpr bool USE_A = LOADU || PROLONG;  // otherwise u_in == 0
   using SH = LevelShape<T, USE_A, SWEEP, POST, PROLONG>;
   constexpr bool HASD = SH::HASD;
   constexpr int hA = SH::hA, hB = SH::hB, hC = SH::hC, hD = SH::hD;
   constexpr int WA = SH::WA, WB = SH::WB, WC = SH::WC, RR = SH::RR;
   constexpr int xD = SWEEP ? 3 : 1;  // stage index of D
+  constexpr int VB = (int)sizeof(V);
 
   const int shift = blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;  // converged shifts are frozen
@@ -172,17 +182,20 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG || !
   const int64_t sbase = (int64_t)shift * a.ss;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* sm = reinterpret_cast<V*>(smem_raw);
-  Ring<T, hA, ARING> RA{sm, c0 - hA};  // u_in (+ P e_c)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [2] chunk barriers
+  V* sm = reinterpret_cast<V*>(smem_raw + 32);
+  V* RA = sm;  // u_in (+ P e_c): ARING x WA, local col 0 = storage col c0 - hA
   if constexpr (USE_A) sm += ARING * WA;
-  V* Bb = sm;                           // b rows of the current B step, [CHUNK][WB]
+  V* Bb = sm;  // b rows of the current B step: CHUNK x WB
   if constexpr (SWEEP) sm += CHUNK * WB;
-  Ring<T, hB, RR> RB{sm, c0 - hB};     // r = b - L u_in
+  V* RB = sm;  // r = b - L u_in: RR x WB
   if constexpr (SWEEP) sm += RR * WB;
-  Ring<T, hC, RR> RC{sm, c0 - hC};     // delta = omega M r
+  V* RC = sm;  // delta = omega M r: RR x WC
   if constexpr (SWEEP && HASD) sm += RR * WC;
-  V* CB = sm;                           // coarse block for the prolongation
+  V* CB = sm;  // coarse block for the prolongation
   if constexpr (PROLONG) sm += CB_ROWS * CB_COLS;
+  V* VX = sm;  // vertical 1-2-1 sums exchanged for the restriction: [2*RGROUPS][VX_W]
+  if constexpr (POST == POST_RESTRICT) sm += 2 * RGROUPS * VX_W;
   double* red = reinterpret_cast<double*>(sm);
 
   const LevelCoef<T> cf = a.coef[shift];
@@ -191,50 +204,68 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG || !
   V* __restrict__ uout = a.u_out + sbase;
   const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
   const int nc = a.nc;
-
-  auto interior = [&](int row, int col) { return (unsigned)(row - 1) < (unsigned)m && (unsigned)(col - 1) < (unsigned)m; };
-  auto in_out = [&](int row, int col) {
-    return row >= r0 && row < r0 + H && col >= c0 && col < c0 + TILE_W && interior(row, col);
-  };
   const int base = r0 - hA;
   const int n_iter = (H + 2 * hA + CHUNK - 1) / CHUNK;
 
-  // ---- asynchronous staging of a step's inputs ------------------------------------------------
-  auto issue_A = [&](int t) {  // u rows of step t (zero outside the interior) and the coarse block
-    if constexpr (USE_A) {
-      const int k0 = base + CHUNK * t;
-      for (int q = tid; q < CHUNK * WA; q += NTHREADS) {
-        const int row = k0 + q / WA, col = c0 - hA + q % WA;
-        if (row >= r0 + H + hA) break;
-        V* dst = &RA.at(row, col);
-        if constexpr (LOADU) {
-          const bool ok = interior(row, col);
-          cp_async16(dst, ok ? (const void*)(uin + (int64_t)row * n + col) : (const void*)uin, ok);
-        } else {
-          *dst = cz<V>();
-        }
+  auto row_in = [&](int row) { return (unsigned)(row - 1) < (unsigned)m; };
+  // ring slot of a row (rows are > -NR); the callers step it incrementally
+  auto slot = [](int row, int NR) { return (row + 4 * NR) % NR; };
+
+  // ---- TMA issue of a step's inputs: warp 0, one bulk copy per row segment --------------------
+  auto issue = [&](int t, bool do_a, bool do_b) {
+    if (tid >= 32) return;
+    const int lane = tid;
+    unsigned bytes = 0;
+    // u rows of step t: storage rows [k0, k0+CHUNK) clipped to [0, n], cols [c0-hA, c0+W+hA) clipped to [0, n]
+    const int k0 = base + CHUNK * t;
+    const int ar_lo = max(k0, 0), ar_hi = min(min(k0 + CHUNK, r0 + H + hA), n + 1);
+    const int ac_lo = max(c0 - hA, 0), ac_hi = min(c0 + TILE_W + hA, n + 1);
+    const int kb0 = base - 1 + CHUNK * t;
+    const int br_lo = max(max(kb0, r0 - hB), 1), br_hi = min(min(kb0 + CHUNK, r0 + H + hB), m + 1);
+    const int bc_lo = max(c0 - hB, 1), bc_hi = min(c0 + TILE_W + hB, m + 1);
+    const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA);
+    const int er_lo = max(J0, 0), er_hi = min(J0 + CB_ROWS, nc + 1);
+    const int ec_lo = max(I0, 0), ec_hi = min(I0 + CB_COLS, nc + 1);
+    // One arrival per step and barrier phase, carrying the byte count of ALL of the step's copies (the
+    // b rows of a sweep are issued later, after stage B has consumed the previous ones).
+    const bool arrive = USE_A ? do_a : do_b;
+    if (arrive) {
+      if constexpr (LOADU) bytes += (unsigned)(max(ar_hi - ar_lo, 0) * max(ac_hi - ac_lo, 0) * VB);
+      if constexpr (PROLONG) bytes += (unsigned)(max(er_hi - er_lo, 0) * max(ec_hi - ec_lo, 0) * VB);
+      if constexpr (SWEEP) bytes += (unsigned)(max(br_hi - br_lo, 0) * max(bc_hi - bc_lo, 0) * VB);
+      if (lane == 0) mbar_arrive_expect_tx(&bar[t & 1], bytes);
+    }
+    __syncwarp();
+    if (do_a && USE_A) {
+      if constexpr (LOADU) {
+        if (ac_hi > ac_lo)
+          for (int row = ar_lo + lane; row < ar_hi; row += 32)
+            tma_load_1d(RA + slot(row, ARING) * WA + (ac_lo - (c0 - hA)), uin + (int64_t)row * n + ac_lo,
+                        (unsigned)((ac_hi - ac_lo) * VB), &bar[t & 1]);
       }
       if constexpr (PROLONG) {
-        const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA);
-        for (int q = tid; q < CB_ROWS * CB_COLS; q += NTHREADS) {
-          const int J = J0 + q / CB_COLS, I = I0 + q % CB_COLS;
-          const bool ok = (unsigned)J <= (unsigned)nc && (unsigned)I <= (unsigned)nc;
-          cp_async16(CB + q, ok ? (const void*)(ecs + (int64_t)J * nc + I) : (const void*)ecs, ok);
-        }
+        if (ec_hi > ec_lo)
+          for (int J = er_lo + lane; J < er_hi; J += 32)
+            tma_load_1d(CB + (J - J0) * CB_COLS + (ec_lo - I0), ecs + (int64_t)J * nc + ec_lo,
+                        (unsigned)((ec_hi - ec_lo) * VB), &bar[t & 1]);
       }
     }
-  };
-  auto issue_B = [&](int t) {  // b rows consumed by stage B in step t
-    if constexpr (SWEEP) {
-      const int k0 = base - 1 + CHUNK * t;
-      for (int q = tid; q < CHUNK * WB; q += NTHREADS) {
-        const int row = k0 + q / WB, col = c0 - hB + q % WB;
-        const bool ok = row >= r0 - hB && row < r0 + H + hB && interior(row, col);
-        cp_async16(Bb + q, ok ? (const void*)(bb + (int64_t)row * n + col) : (const void*)bb, ok);
-      }
+    if (do_b && SWEEP) {
+      if (bc_hi > bc_lo)
+        for (int row = br_lo + lane; row < br_hi; row += 32)
+          tma_load_1d(Bb + (row - kb0) * WB + (bc_lo - (c0 - hB)), bb + (int64_t)row * n + bc_lo,
+                      (unsigned)((bc_hi - bc_lo) * VB), &bar[t & 1]);
     }
   };
-  // b - (A + lambda I) u at an interior node from ring values (grid.cpp:69-100: d*u_c - W - E - S - N)
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // b - (A + lambda I) u at an interior node (grid.cpp:69-100 order: d*u_c - W - E - S - N)
   auto apply_res = [&](V bv, V uc, V uw, V ue, V us, V un) {
     V acc = cmul(cf.d, uc);
     acc = csub(acc, uw);
@@ -244,24 +275,28 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG || !
     return csub(bv, cscale(cf.inv_h2, acc));
   };
 
+  // fixed per-thread task geometry
+  const int rg = tid / (SWEEP ? WB : 1);  // (recomputed per stage below where widths differ)
+  (void)rg;
+
   double nacc = 0.0;
-  issue_A(0);
-  issue_B(0);
-  cp_async_commit();
+  issue(0, true, true);
 
   for (int t = 0; t < n_iter; ++t) {
-    cp_async_wait_all();
+    if (USE_A || SWEEP) mbar_wait(&bar[t & 1], (unsigned)((t >> 1) & 1));
     __syncthreads();
     // ---------------- stage A: u_in = [u] + P e_c (in place on the landed rows) -----------------
     if constexpr (PROLONG) {  // u += prolong_bilinear(e_c) (grid.cpp:123-153, multigrid.cpp:75)
       const int k0 = base + CHUNK * t;
       const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA);
+      const int rhi = min(k0 + CHUNK, r0 + H + hA);
       for (int q = tid; q < CHUNK * WA; q += NTHREADS) {
-        const int row = k0 + q / WA, col = c0 - hA + q % WA;
-        if (row >= r0 + H + hA) break;
-        V& slot = RA.at(row, col);
+        const int lr = q / WA, lc = q - lr * WA;
+        const int row = k0 + lr, col = c0 - hA + lc;
+        if (row >= rhi) break;
+        V* slotp = RA + slot(row, ARING) * WA + lc;
         V v = cz<V>();
-        if (interior(row, col)) {
+        if (row_in(row) && (unsigned)(col - 1) < (unsigned)m) {
           const V* e0 = CB + (floordiv2(row) - J0) * CB_COLS + (floordiv2(col) - I0);
           V p;
           if (!(col & 1) && !(row & 1)) {
@@ -274,183 +309,211 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG || !
             p = cscale((T)0.25, cadd(cadd(cadd(e0[0], e0[1]), e0[CB_COLS]), e0[CB_COLS + 1]));
           }
           v = p;
-          if constexpr (LOADU) v = cadd(slot, p);
+          if constexpr (LOADU) v = cadd(*slotp, p);
         }
-        slot = v;
+        *slotp = v;  // non-interior nodes become exact zeros (the ghost ring the stencil reads)
         if constexpr (!SWEEP && STORE) {
-          if (in_out(row, col)) uout[(int64_t)row * n + col] = v;
+          if (row >= r0 && row < r0 + H && row_in(row) && col >= c0 && col < c0 + TILE_W &&
+              (unsigned)(col - 1) < (unsigned)m)
+            uout[(int64_t)row * n + col] = v;
         }
       }
       __syncthreads();
     }
     if constexpr (SWEEP) {
-      if (t + 1 < n_iter) issue_A(t + 1);  // lands in ring rows no stage of step t touches
-      cp_async_commit();
-    }
-    if constexpr (SWEEP) {
+      if (t + 1 < n_iter) issue(t + 1, true, false);  // lands in ring rows no stage of step t touches
       // -------------- stage B: r = b - (A + lambda I) u_in  (grid.cpp:69-100) ---------------------
-      {
-        const int q = tid;
-        if (q < WB * RGROUPS) {
-          const int ci = q % WB, rg = q / WB;
-          const int kb = base - 1 + CHUNK * t + RPT * rg, col = c0 - hB + ci;
-          V am, ac, ap;  // rolling window of u_in down the column
-          if constexpr (USE_A) {
-            am = RA.at(kb - 1, col);
-            ac = RA.at(kb, col);
-          }
+      if (tid < WB * RGROUPS) {
+        const int g = tid / WB, ci = tid - g * WB;
+        const int kb = base - 1 + CHUNK * t + RPT * g, col = c0 - hB + ci;
+        const bool cin = (unsigned)(col - 1) < (unsigned)m;
+        int sa = slot(kb - 1, ARING), sb = slot(kb, RR);
+        const V* ap = RA + ci + 1;  // local col of `col` in the A ring
+        V* bp = RB + ci;
+        V am, ac, an;
+        if constexpr (USE_A) {
+          am = ap[sa * WA];
+          sa = sa + 1 == ARING ? 0 : sa + 1;
+          ac = ap[sa * WA];
+        }
 #pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            const int row = kb + i;
-            if constexpr (USE_A) ap = RA.at(row + 1, col);
-            if (row >= r0 - hB && row < r0 + H + hB) {
-              V r = cz<V>();
-              if (interior(row, col)) {
-                const V bv = Bb[(RPT * rg + i) * WB + ci];
-                if constexpr (USE_A) {
-                  const V* rp = RA.row_ptr(row);
-                  r = apply_res(bv, ac, rp[col - 1], rp[col + 1], am, ap);
-                } else {
-                  r = bv;  // zero initial guess: r = b
-                }
+        for (int i = 0; i < RPT; ++i) {
+          const int row = kb + i;
+          const int sn = sa + 1 == ARING ? 0 : sa + 1;
+          if constexpr (USE_A) an = ap[sn * WA];
+          if (row >= r0 - hB && row < r0 + H + hB) {
+            V r = cz<V>();
+            if (cin && row_in(row)) {
+              const V bv = Bb[(RPT * g + i) * WB + ci];
+              if constexpr (USE_A) {
+                r = apply_res(bv, ac, ap[sa * WA - 1], ap[sa * WA + 1], am, an);
+              } else {
+                r = bv;  // zero initial guess: r = b
               }
-              RB.at(row, col) = r;
             }
-            if constexpr (USE_A) am = ac, ac = ap;
+            bp[sb * WB] = r;
           }
+          if constexpr (USE_A) am = ac, ac = an;
+          sa = sn;
+          sb = sb + 1 == RR ? 0 : sb + 1;
         }
       }
       __syncthreads();
-      if (t + 1 < n_iter) issue_B(t + 1);
-      cp_async_commit();
+      if (t + 1 < n_iter) issue(t + 1, false, true);
       // -------------- stage C: delta = omega M r; u_out = u_in + delta  (smoother.cpp:49-67) -------
-      {
-        const int q = tid;
-        if (q < WC * RGROUPS) {
-          const int ci = q % WC, rg = q / WC;
-          const int kc = base - 2 + CHUNK * t + RPT * rg, col = c0 - hC + ci;
-          // rolling 3-row window over the column: r and the horizontal pair sum r(col-1)+r(col+1)
-          V rm, rc, rp, sm_, sc, sp;
-          auto fetch = [&](int row, V& r_, V& s_) {
-            const V* q_ = RB.row_ptr(row);
-            r_ = q_[col];
-            if constexpr (!JACOBI) s_ = cadd(q_[col - 1], q_[col + 1]);
-          };
-          fetch(kc - 1, rm, sm_);
-          fetch(kc, rc, sc);
+      if (tid < WC * RGROUPS) {
+        const int g = tid / WC, ci = tid - g * WC;
+        const int kc = base - 2 + CHUNK * t + RPT * g, col = c0 - hC + ci;
+        const bool cin = (unsigned)(col - 1) < (unsigned)m;
+        const bool cout = cin && col >= c0 && col < c0 + TILE_W;
+        const V* rpc = RB + (ci + (hB - hC));  // local col of `col` in the r ring
+        int s = slot(kc - 1, RR);
+        // rolling 3-row window over the column: r and the horizontal pair sum r(col-1)+r(col+1)
+        V rm, rc, rn, sm_, sc, sn_;
+        rm = rpc[s * WB];
+        if constexpr (!JACOBI) sm_ = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
+        s = s + 1 == RR ? 0 : s + 1;
+        rc = rpc[s * WB];
+        if constexpr (!JACOBI) sc = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
+        int sa = slot(kc, ARING), sd = slot(kc, RR);
+        V* outp = uout + (int64_t)kc * n + col;
 #pragma unroll
-          for (int i = 0; i < RPT; ++i) {
-            const int row = kc + i;
-            fetch(row + 1, rp, sp);
-            if (row >= r0 - hC && row < r0 + H + hC) {
-              V dl = cz<V>();
-              if (interior(row, col)) {
-                if constexpr (JACOBI) {
-                  dl = cmul(cf.k0, rc);
-                } else {  // (h^2/4)[c,2b,c;2b,4a,2b;c,2b,c] r with omega folded in (smoother.cpp:31-40)
-                  const V e1 = cadd(cadd(sc, rm), rp);
-                  const V e2 = cadd(sm_, sp);
-                  dl = cadd(cadd(cmul(cf.k0, rc), cmul(cf.k1, e1)), cmul(cf.k2, e2));
-                }
-              }
-              if constexpr (HASD) RC.at(row, col) = dl;
-              if constexpr (STORE) {
-                if (in_out(row, col)) {
-                  V uo = dl;
-                  if constexpr (USE_A) uo = cadd(RA.at(row, col), dl);
-                  uout[(int64_t)row * n + col] = uo;
-                }
+        for (int i = 0; i < RPT; ++i) {
+          const int row = kc + i;
+          s = s + 1 == RR ? 0 : s + 1;
+          rn = rpc[s * WB];
+          if constexpr (!JACOBI) sn_ = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
+          if (row >= r0 - hC && row < r0 + H + hC) {
+            V dl = cz<V>();
+            if (cin && row_in(row)) {
+              if constexpr (JACOBI) {
+                dl = cmul(cf.k0, rc);
+              } else {  // (h^2/4)[c,2b,c;2b,4a,2b;c,2b,c] r with omega folded in (smoother.cpp:31-40)
+                const V e1 = cadd(cadd(sc, rm), rn);
+                const V e2 = cadd(sm_, sn_);
+                dl = cadd(cadd(cmul(cf.k0, rc), cmul(cf.k1, e1)), cmul(cf.k2, e2));
               }
             }
-            rm = rc, sm_ = sc, rc = rp, sc = sp;
+            if constexpr (HASD) RC[sd * WC + ci] = dl;
+            if constexpr (STORE) {
+              if (cout && row >= r0 && row < r0 + H && row_in(row)) {
+                V uo = dl;
+                if constexpr (USE_A) uo = cadd(RA[sa * WA + ci + (hA - hC)], dl);
+                *outp = uo;
+              }
+            }
           }
+          rm = rc, sm_ = sc, rc = rn, sc = sn_;
+          sa = sa + 1 == ARING ? 0 : sa + 1;
+          sd = sd + 1 == RR ? 0 : sd + 1;
+          outp += n;
         }
       }
       if constexpr (HASD) __syncthreads();
     }
     // -------------- stage D: r2 = b - (A + lambda I) u_out ---------------------------------------------
-    // after a sweep r2 = r - (A + lambda I) delta (exact algebra; b is not read again)
-    auto Urow = [&](int row) -> const V* {
-      if constexpr (SWEEP) return RC.row_ptr(row);
-      else return RA.row_ptr(row);
-    };
-    auto r2_at = [&](int row, int col, V uc, V um, V up) {  // uc/um/up: u_out (or delta) at rows row, row-1, row+1
-      const V* rp = Urow(row);
-      V rb;
-      if constexpr (SWEEP) rb = RB.at(row, col);
-      else rb = bb[(int64_t)row * n + col];
-      return apply_res(rb, uc, rp[col - 1], rp[col + 1], um, up);
-    };
-    if constexpr (POST == POST_NORM || POST == POST_RESID) {
-      const int q = tid;
-      if (q < TILE_W * RGROUPS) {
-        const int ci = q % TILE_W, rg = q / TILE_W;
-        const int kd = base - xD + CHUNK * t + RPT * rg, col = c0 + ci;
-        V dm = Urow(kd - 1)[col], dc = Urow(kd)[col], dp;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          const int row = kd + i;
-          dp = Urow(row + 1)[col];
-          if (in_out(row, col)) {
-            const V r2 = r2_at(row, col, dc, dm, dp);
-            if constexpr (POST == POST_NORM) nacc += (double)r2.x * (double)r2.x + (double)r2.y * (double)r2.y;
-            if constexpr (POST == POST_RESID) uout[(int64_t)row * n + col] = r2;
-          }
-          dm = dc, dc = dp;
+    // after a sweep r2 = r - (A + lambda I) delta (exact algebra; b is not read again); without a sweep
+    // u_out = u_in (ring A, or zero) and b comes from global memory.
+    if constexpr (POST == POST_NORM || POST == POST_RESID || POST == POST_RESTRICT) {
+      constexpr int WU = SWEEP ? WC : WA;  // width of the ring holding u_out (or delta)
+      constexpr int NRU = SWEEP ? RR : ARING;
+      const V* U = SWEEP ? RC : RA;
+      constexpr int hU = SWEEP ? hC : hA;
+      // r2 down one column over rows [k, k+nr): rolls a 3-row window of U
+      auto r2_column = [&](int k, int col, int nr, auto&& consume) {
+        const int lc = col - (c0 - hU);
+        const V* up = U + lc;
+        int s = slot(k - 1, NRU);
+        int srb = slot(k, RR);
+        const bool cin = (unsigned)(col - 1) < (unsigned)m;
+        V um = cz<V>(), uc = cz<V>(), un = cz<V>();
+        if constexpr (USE_A || SWEEP) {
+          um = up[s * WU];
+          s = s + 1 == NRU ? 0 : s + 1;
+          uc = up[s * WU];
         }
-      }
-    }
-    if constexpr (POST == POST_RESTRICT) {
-      // ------------ stage D+E: b_c(I,J) = (1/16)[1 2 1;2 4 2;1 2 1] r2 around (2I,2J)  (grid.cpp:102-121)
-      // one coarse node per thread; r2 is formed on the 3x3 fine block in registers (no r2 ring).
-      const int kcur = min(base - xD + CHUNK * (t + 1), r0 + H + hD);
-      const int kprev = min(base - xD + CHUNK * t, r0 + H + hD);
-      const int mc = nc - 1;
-      int jlo = max(r0 >> 1, 1);
-      if (t > 0) jlo = max(jlo, floordiv2(kprev - 2) + 1);
-      const int jhi = min(min(floordiv2(kcur - 2), ((r0 + H) >> 1) - 1), mc);
-      V* __restrict__ bco = a.bc + (int64_t)shift * a.ssc;
-      const int q = tid;
-      if (q < (jhi - jlo + 1) * (TILE_W / 2)) {
-        const int J = jlo + q / (TILE_W / 2);
-        const int I = (c0 >> 1) + q % (TILE_W / 2);
-        if (I >= 1 && I <= mc) {
-          const int i = 2 * I, j = 2 * J;
-          V s = cz<V>();
-          V u_m[3], u_c[3], u_p[3];  // u (or delta) at rows j-2.., cols i-1..i+1, rolled down
+        const V* bg = bb + (int64_t)k * n + col;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            u_m[c] = Urow(j - 2)[i - 1 + c];
-            u_c[c] = Urow(j - 1)[i - 1 + c];
+        for (int i = 0; i < 5; ++i) {
+          if (i >= nr) break;
+          const int row = k + i;
+          const int sn = s + 1 == NRU ? 0 : s + 1;
+          if constexpr (USE_A || SWEEP) un = up[sn * WU];
+          V r2 = cz<V>();
+          if (cin && row_in(row)) {
+            V rb;
+            if constexpr (SWEEP) rb = RB[srb * WB + (col - (c0 - hB))];
+            else rb = bg[0];
+            if constexpr (USE_A || SWEEP) r2 = apply_res(rb, uc, up[s * WU - 1], up[s * WU + 1], um, un);
+            else r2 = rb;
           }
-#pragma unroll
-          for (int rr = 0; rr < 3; ++rr) {
-            const int row = j - 1 + rr;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) u_p[c] = Urow(row + 1)[i - 1 + c];
-            const T wr = rr == 1 ? (T)2 : (T)1;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const V r2 = r2_at(row, i - 1 + c, u_c[c], u_m[c], u_p[c]);
-              const T w = wr * (c == 1 ? (T)2 : (T)1);
-              s = cadd(s, cscale(w, r2));
-            }
-#pragma unroll
-            for (int c = 0; c < 3; ++c) u_m[c] = u_c[c], u_c[c] = u_p[c];
-          }
-          bco[(int64_t)J * nc + I] = cscale((T)(1.0 / 16.0), s);
+          consume(i, row, r2);
+          um = uc, uc = un;
+          s = sn;
+          srb = srb + 1 == RR ? 0 : srb + 1;
+          bg += n;
         }
-      }
-    }
-    if constexpr (!SWEEP) {  // D/E read u_in rows further back: refill only after they are done
-      if (t + 1 < n_iter) {
+      };
+      if constexpr (POST == POST_NORM || POST == POST_RESID) {
+        if (tid < TILE_W * RGROUPS) {
+          const int g = tid / TILE_W, ci = tid - g * TILE_W;
+          const int kd = base - xD + CHUNK * t + RPT * g, col = c0 + ci;
+          if (col <= m) {
+            r2_column(kd, col, RPT, [&](int, int row, V r2) {
+              if (row >= r0 && row < r0 + H && row_in(row) && col >= 1) {
+                if constexpr (POST == POST_NORM) nacc += (double)r2.x * (double)r2.x + (double)r2.y * (double)r2.y;
+                if constexpr (POST == POST_RESID) uout[(int64_t)row * n + col] = r2;
+              }
+            });
+          }
+        }
+      } else {
+        // ------------ restriction b_c(I,J) = (1/16)[1 2 1;2 4 2;1 2 1] r2 around (2I,2J) (grid.cpp:102-121)
+        // coarse rows J of this step are those whose fine rows 2J-1..2J+1 completed in it.
+        const int kcur = min(base - xD + CHUNK * (t + 1), r0 + H + hD);
+        const int kprev = min(base - xD + CHUNK * t, r0 + H + hD);
+        const int mc = nc - 1;
+        int jlo = max(r0 >> 1, 1);
+        if (t > 0) jlo = max(jlo, floordiv2(kprev - 2) + 1);
+        const int jhi = min(min(floordiv2(kcur - 2), ((r0 + H) >> 1) - 1), mc);
+        const int nj = jhi - jlo + 1;
+        // phase 1: per fine column f, vertical 1-2-1 sums of r2 for coarse rows (jlo+2g, jlo+2g+1)
+        if (tid < VX_W * RGROUPS) {
+          const int g = tid / VX_W, f = tid - g * VX_W;
+          const int Ja = jlo + 2 * g;
+          if (2 * g < nj) {
+            const int col = c0 - 1 + f;
+            const int nr = 2 * g + 1 < nj ? 5 : 3;
+            V acc_a = cz<V>(), acc_b = cz<V>();
+            r2_column(2 * Ja - 1, col, nr, [&](int i, int, V r2) {
+              if (i <= 2) acc_a = cadd(acc_a, i == 1 ? cscale((T)2, r2) : r2);
+              if (i >= 2) acc_b = cadd(acc_b, i == 3 ? cscale((T)2, r2) : r2);
+            });
+            VX[(2 * g) * VX_W + f] = acc_a;
+            VX[(2 * g + 1) * VX_W + f] = acc_b;
+          }
+        }
         __syncthreads();
-        issue_A(t + 1);
+        // phase 2: horizontal 1-2-1 of the column sums, one coarse node per thread
+        V* __restrict__ bco = a.bc + (int64_t)shift * a.ssc;
+        if (tid < nj * (TILE_W / 2)) {
+          const int jr = tid / (TILE_W / 2), il = tid - jr * (TILE_W / 2);
+          const int I = (c0 >> 1) + il, J = jlo + jr;
+          if (I >= 1 && I <= mc) {
+            const V* v = VX + jr * VX_W + 2 * il;  // fine col 2I - 1 is local f = 2*il
+            const V s = cadd(cadd(v[0], cscale((T)2, v[1])), v[2]);
+            bco[(int64_t)J * nc + I] = cscale((T)(1.0 / 16.0), s);
+          }
+        }
       }
-      cp_async_commit();
+    }
+    if constexpr (!SWEEP) {  // D read u_in rows further back: refill only after they are done
+      if (USE_A && t + 1 < n_iter) {
+        __syncthreads();
+        issue(t + 1, true, false);
+      }
     }
   }
-  cp_async_wait_all();
 
   if constexpr (POST == POST_NORM) {
     // deterministic block reduction: warp tree, then warp 0 over the per-warp sums
