@@ -61,13 +61,6 @@ def dist_env():
     return rank, world, local
 
 
-def shard(S: int, rank: int, world: int):
-    """Contiguous chunks of ceil(S/world) shifts, as paradiag_solve's thread pool (paradiag.cpp:222-224)."""
-    chunk = (S + world - 1) // world
-    b0 = min(S, rank * chunk)
-    return b0, min(S, b0 + chunk)
-
-
 def updates_per_cycle(n: int, nu1: int, nu2: int, coarsest: int = 4) -> float:
     tot, g = 0.0, n
     while g > coarsest:
@@ -204,6 +197,7 @@ def main():
     import torch
 
     import paper_2203_11154_b200 as P
+    from paper_2203_11154_b200.sharding import shard
 
     torch.cuda.set_device(local)
     if world > 1:

@@ -1,0 +1,172 @@
+// pdmg_b200.hpp -- header-only C++ facade over the C ABI (pdmg_b200.h), restoring the reference's
+// pdmg:: class shapes and exception types so reference call sites port with a namespace change:
+//
+//   reference (proj/include/pdmg/...)                       this facade
+//   Grid2D, Shift                 (grid.hpp:16-52)          pdmg_b200::Grid2D, Shift
+//   SmootherConfig                (smoother.hpp:30-38)      pdmg_b200::SmootherConfig
+//   MultigridConfig, SolveReport  (multigrid.hpp:14-44)     pdmg_b200::MultigridConfig, SolveReport
+//   MultigridHierarchy            (multigrid.hpp:50-78)     pdmg_b200::BatchedMultigridHierarchy (n shifts)
+//   multigrid_solve               (multigrid.hpp:82-83)     pdmg_b200::multigrid_solve
+//   ConfigError, SingularOperatorError (errors.hpp:12-23)   same names, same std:: bases
+//
+// Grid functions are std::vector<std::complex<double>> in the reference layout (interior nodes, x
+// fastest), stacked shift-major for batches.
+#pragma once
+
+#include <complex>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pdmg_b200.h"
+
+namespace pdmg_b200 {
+
+using cplx = std::complex<double>;
+static_assert(sizeof(cplx) == sizeof(pdmg_c128), "std::complex<double> must match pdmg_c128");
+
+class ConfigError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class SingularOperatorError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int status) {
+  if (status == PDMG_OK) return;
+  const std::string msg = pdmg_last_error();
+  if (status == PDMG_ERR_CONFIG) throw ConfigError(msg);
+  if (status == PDMG_ERR_SINGULAR) throw SingularOperatorError(msg);
+  throw DeviceError(msg);
+}
+
+struct Grid2D {
+  int n = 0;
+  Grid2D() = default;
+  explicit Grid2D(int subdivisions) : n(subdivisions) {
+    if (n < 2) throw ConfigError("Grid2D: need at least 2 subdivisions per side, got " + std::to_string(n));
+  }
+  double h() const { return 1.0 / n; }
+  int interior_per_side() const { return n - 1; }
+  long size() const { return static_cast<long>(n - 1) * (n - 1); }
+};
+
+struct Shift {
+  cplx lambda{0.0, 0.0};
+  int index = 0;
+};
+
+enum class CycleKind { V = PDMG_CYCLE_V, W = PDMG_CYCLE_W };
+enum class SmootherKind { Vanka = PDMG_SMOOTHER_VANKA, Jacobi = PDMG_SMOOTHER_JACOBI };
+
+struct SmootherConfig {
+  SmootherKind kind = SmootherKind::Vanka;
+  double omega = 24.0 / 25.0;
+  static SmootherConfig vanka(double w = 24.0 / 25.0) { return {SmootherKind::Vanka, w}; }
+  static SmootherConfig jacobi(double w = 4.0 / 5.0) { return {SmootherKind::Jacobi, w}; }
+};
+
+struct MultigridConfig {
+  CycleKind cycle = CycleKind::W;
+  int nu1 = 1;
+  int nu2 = 0;
+  int coarsest_n = 8;
+  double tol = 1e-8;
+  int max_iter = 200;
+  SmootherConfig smoother{};
+
+  pdmg_mg_config c() const {
+    return pdmg_mg_config{static_cast<int32_t>(cycle), nu1, nu2, coarsest_n, tol, max_iter,
+                          static_cast<int32_t>(smoother.kind), smoother.omega};
+  }
+};
+
+struct SolveReport {
+  bool converged = false;
+  int iterations = 0;
+  std::vector<double> residual_history;
+  double rate = 0.0;
+  double seconds = 0.0;
+};
+
+// One hierarchy per shift on a shared fine grid, all advanced together on one GPU.
+class BatchedMultigridHierarchy {
+ public:
+  BatchedMultigridHierarchy(Grid2D fine, const std::vector<Shift>& shifts, const MultigridConfig& cfg, int device = 0)
+      : grid_(fine), cfg_(cfg), S_(static_cast<int>(shifts.size())) {
+    std::vector<pdmg_c128> lam(shifts.size());
+    for (size_t s = 0; s < shifts.size(); ++s) lam[s] = {shifts[s].lambda.real(), shifts[s].lambda.imag()};
+    pdmg_batch_desc d{fine.n, S_, lam.data(), cfg.c(), PDMG_PREC_C128, device};
+    check(pdmg_create(&d, &ctx_));
+  }
+  ~BatchedMultigridHierarchy() { pdmg_destroy(ctx_); }
+  BatchedMultigridHierarchy(const BatchedMultigridHierarchy&) = delete;
+  BatchedMultigridHierarchy& operator=(const BatchedMultigridHierarchy&) = delete;
+
+  int num_levels() const { return pdmg_num_levels(ctx_); }
+  Grid2D level_grid(int ell) const { return Grid2D(pdmg_level_n(ctx_, ell)); }
+  int num_shifts() const { return S_; }
+
+  // MultigridHierarchy::solve for every shift (multigrid.cpp:85-110); u is overwritten.
+  std::vector<SolveReport> solve(std::vector<cplx>& u, const std::vector<cplx>& b) const {
+    const size_t N = static_cast<size_t>(S_) * grid_.size();
+    if (b.size() != N) throw ConfigError("MultigridHierarchy::solve: grid mismatch");
+    u.resize(N);
+    const int H = cfg_.max_iter + 1;
+    std::vector<int32_t> it(S_);
+    std::vector<uint8_t> cv(S_);
+    std::vector<double> hist(static_cast<size_t>(S_) * H), rate(S_);
+    pdmg_solve_report rep{it.data(), cv.data(), hist.data(), rate.data(), 0.0};
+    check(pdmg_solve(ctx_, reinterpret_cast<const pdmg_c128*>(b.data()), reinterpret_cast<pdmg_c128*>(u.data()),
+                     &rep));
+    std::vector<SolveReport> out(S_);
+    for (int s = 0; s < S_; ++s) {
+      out[s].converged = cv[s] != 0;
+      out[s].iterations = it[s];
+      out[s].residual_history.assign(hist.begin() + static_cast<long>(s) * H,
+                                     hist.begin() + static_cast<long>(s) * H + it[s] + 1);
+      out[s].rate = rate[s];
+      out[s].seconds = rep.seconds;
+    }
+    return out;
+  }
+
+  // MultigridHierarchy::cycle (multigrid.cpp:79-83), in place for every shift.
+  void cycle(std::vector<cplx>& u, const std::vector<cplx>& b) const {
+    check(pdmg_cycle(ctx_, reinterpret_cast<pdmg_c128*>(u.data()), reinterpret_cast<const pdmg_c128*>(b.data())));
+  }
+
+  pdmg_ctx* handle() const { return ctx_; }
+
+ private:
+  Grid2D grid_;
+  MultigridConfig cfg_;
+  int S_;
+  pdmg_ctx* ctx_ = nullptr;
+};
+
+// multigrid.cpp:112-118 convenience driver for one shift.
+inline std::pair<std::vector<cplx>, SolveReport> multigrid_solve(const std::vector<cplx>& b, Grid2D g,
+                                                                  const Shift& shift, const MultigridConfig& cfg,
+                                                                  int device = 0) {
+  BatchedMultigridHierarchy mg(g, {shift}, cfg, device);
+  std::vector<cplx> u;
+  auto reps = mg.solve(u, b);
+  return {std::move(u), reps[0]};
+}
+
+// tools/pdmg.cpp:137-147
+inline std::vector<cplx> random_rhs(Grid2D g, unsigned seed) {
+  std::vector<cplx> b(static_cast<size_t>(g.size()));
+  pdmg_random_rhs(seed, -1.0, 1.0, g.size(), reinterpret_cast<pdmg_c128*>(b.data()));
+  return b;
+}
+
+}  // namespace pdmg_b200
