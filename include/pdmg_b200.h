@@ -119,14 +119,35 @@ int pdmg_prolong_bilinear(pdmg_ctx* ctx, int level, const pdmg_c128* coarse,
 int pdmg_norm(pdmg_ctx* ctx, int level, const pdmg_c128* v, double* norms); /* grid.cpp:7-11    */
 int pdmg_coarse_solve(pdmg_ctx* ctx, const pdmg_c128* b, pdmg_c128* u);      /* dense.cpp:90-100 */
 
-/* ParaDIAG step with the alpha-circulant backward-Euler time matrix C_alpha = (1/dt)(I - Sigma_alpha)
- * (restated; the reference's three-step driver is paradiag.cpp:185-248):
- *   g = ifft_t(alpha^(t/nt) f);  (A + lambda_k I) w_k = g_k, lambda_k = (1 - alpha^(1/nt) e^(2 pi i k/nt))/dt;
- *   u = alpha^(-t/nt) fft_k(w);  relres = ||f - (C_alpha (x) I + I (x) A) u|| / ||f||.
- * f, u: host [nt][(n-1)^2].  cfg as for pdmg_create.  report arrays are per time slot k. */
+/* ParaDIAG with the alpha-circulant backward-Euler time matrix C_alpha = (1/dt)(I - Sigma_alpha), Sigma_alpha the
+ * down-shift with corner alpha (restated; the reference's three-step driver is paradiag.cpp:185-248 and its
+ * closed-form alpha-circulant diagonalization, for alpha < 0 only, paradiag.cpp:84-108):
+ *   step 1  g = ifft_t(alpha^(t/nt) f)                                  (kron_time_solve, paradiag.cpp:135-139)
+ *   step 2  (A + lambda_k I) w_k = g_k, lambda_k = (1 - alpha^(1/nt) e^(2 pi i k/nt))/dt  (paradiag.cpp:207-236)
+ *   step 3  u = alpha^(-t/nt) fft_k(w)                                  (kron_time_apply, paradiag.cpp:129-133)
+ *   relres  = ||f - (C_alpha (x) I + I (x) A) u|| / ||f||               (paradiag.cpp:243-245)
+ * f, u: [nt][(n-1)^2] time slices in the reference layout.  report arrays are per time slot k. */
+typedef struct pdmg_paradiag pdmg_paradiag;
+int pdmg_paradiag_create(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t device,
+                         pdmg_paradiag** out);
+void pdmg_paradiag_destroy(pdmg_paradiag* p);
+pdmg_ctx* pdmg_paradiag_solver(pdmg_paradiag* p); /* the inner batched solver (stats, levels) */
+int pdmg_paradiag_run(pdmg_paradiag* p, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* report,
+                      double* relres);
+int pdmg_paradiag_run_device(pdmg_paradiag* p, const void* d_f, void* d_u, pdmg_solve_report* report,
+                             double* relres);
+/* One-shot convenience (paradiag_solve, paradiag.hpp:112-113). */
 int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg,
                             int32_t device, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* report,
                             double* relres);
+/* Building blocks of the multi-GPU driver (time slices sharded over ranks, NCCL all-to-all between):
+ * alpha-scaled DFT over the full time axis of npts points laid out [nt][npts] (step 1 or 3 above), and
+ * the all-at-once residual of local slices [t0, t0+ntl) given the slice before t0 (u_{nt-1} if t0 == 0):
+ * sums = {||r||^2, ||f||^2} over the local slices.  stream: a cudaStream_t (NULL = default stream). */
+int pdmg_time_dft(int32_t device, int32_t nt, int64_t npts, double alpha, int32_t step, const void* d_in,
+                  void* d_out, void* stream);
+int pdmg_aao_residual(int32_t device, int32_t n, int32_t ntl, int32_t t0, double alpha, double dt, const void* d_u,
+                      const void* d_u_prev, const void* d_f, double* sums, void* stream);
 
 /* Host helpers (no GPU needed). */
 /* tools/pdmg.cpp:137-147 random_rhs: std::mt19937(seed), uniform_real_distribution<double>(lo,hi),

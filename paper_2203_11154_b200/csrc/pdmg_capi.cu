@@ -873,6 +873,138 @@ struct Engine {
   }
 };
 
+
+// ---------------------------------------------------------------------------------------------
+// ParaDIAG time direction (alpha-circulant backward Euler), restated: paradiag.cpp:185-248 three-step
+// driver with B = C_alpha = (1/dt)(I - Sigma_alpha), diagonalized by an alpha-scaled DFT over time.
+// ---------------------------------------------------------------------------------------------
+struct DftTables {
+  double2* tw = nullptr;  // e^{dir 2 pi i q/nt}
+  double* pre = nullptr;
+  double* post = nullptr;
+  int nt = 0, log2nt = -1;
+  ~DftTables() {
+    cudaFree(tw);
+    cudaFree(pre);
+    cudaFree(post);
+  }
+};
+
+// step 1: pre = alpha^(t/nt), dir +1, post = 1/nt;  step 3: pre = 1, dir -1, post = alpha^(-t/nt)
+std::unique_ptr<DftTables> make_dft_tables(int nt, double alpha, int step, cudaStream_t st) {
+  if (nt < 1) throw ConfigError("time DFT: nt must be >= 1");
+  auto T = std::make_unique<DftTables>();
+  T->nt = nt;
+  T->log2nt = ((nt & (nt - 1)) == 0) ? __builtin_ctz((unsigned)nt) : -1;
+  std::vector<double2> tw(nt);
+  std::vector<double> pre(nt), post(nt);
+  const double dir = step == 1 ? 1.0 : -1.0;
+  for (int q = 0; q < nt; ++q) {
+    const cplx z = std::polar(1.0, dir * 2.0 * M_PI * (double)q / (double)nt);
+    tw[q] = make_double2(z.real(), z.imag());
+    const double sc = std::pow(alpha, (double)q / (double)nt);
+    pre[q] = step == 1 ? sc : 1.0;
+    post[q] = step == 1 ? 1.0 / nt : 1.0 / sc;
+  }
+  CK(cudaMalloc(&T->tw, sizeof(double2) * nt));
+  CK(cudaMalloc(&T->pre, sizeof(double) * nt));
+  CK(cudaMalloc(&T->post, sizeof(double) * nt));
+  CK(cudaMemcpyAsync(T->tw, tw.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(T->pre, pre.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(T->post, post.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return T;
+}
+
+int dft_points_per_cta(int nt) { return std::max(1, std::min(64, 4096 / nt)); }
+
+void launch_time_dft(const DftTables& T, const double2* in, double2* out, int64_t npts, cudaStream_t st) {
+  const int P = dft_points_per_cta(T.nt);
+  const size_t smem = (size_t)T.nt * P * sizeof(double2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_time_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr_set = true;
+  }
+  const int64_t blocks = (npts + P - 1) / P;
+  if (blocks > 0)
+    k_time_dft<<<(unsigned)blocks, DFT_THREADS, smem, st>>>(in, out, T.nt, T.log2nt, (int)npts, P, T.tw, T.pre, T.post);
+  CK(cudaGetLastError());
+}
+
+struct Paradiag {
+  int n = 0, nt = 0;
+  double alpha = 0, dt = 0;
+  int device = 0;
+  std::unique_ptr<Engine<double>> eng;
+  std::unique_ptr<DftTables> t1, t3;
+  double2 *d_f = nullptr, *d_g = nullptr, *d_w = nullptr, *d_u = nullptr;
+  double* d_partial = nullptr;
+  int res_blocks = 0;
+  int64_t npts = 0;
+
+  ~Paradiag() {
+    if (eng) cudaSetDevice(device);
+    cudaFree(d_f);
+    cudaFree(d_g);
+    cudaFree(d_w);
+    cudaFree(d_u);
+    cudaFree(d_partial);
+  }
+
+  void setup(int n_, int nt_, double alpha_, double dt_, const pdmg_mg_config& cfg, int dev) {
+    if (nt_ < 2) throw ConfigError("TimeDiscretization: need n >= 2 time steps");
+    if (!(dt_ > 0.0)) throw ConfigError("TimeDiscretization: tau must be positive");
+    if (!(alpha_ > 0.0)) throw ConfigError("alpha-circulant: alpha must be positive");
+    n = n_, nt = nt_, alpha = alpha_, dt = dt_, device = dev;
+    std::vector<pdmg_c128> lam(nt);
+    pdmg_circulant_shifts(alpha, nt, dt, 0, nt, lam.data());
+    pdmg_batch_desc d{n, nt, lam.data(), cfg, PDMG_PREC_C128, dev};
+    eng = std::make_unique<Engine<double>>();
+    eng->device = -1;
+    eng->setup_host(d);
+    eng->setup_device(dev);
+    npts = (int64_t)(n - 1) * (n - 1);
+    const size_t bytes = sizeof(double2) * (size_t)nt * npts;
+    for (double2** p : {&d_f, &d_g, &d_w, &d_u}) CK(cudaMalloc(p, bytes));
+    t1 = make_dft_tables(nt, alpha, 1, eng->stream);
+    t3 = make_dft_tables(nt, alpha, 3, eng->stream);
+    res_blocks = 148 * 8;
+    CK(cudaMalloc(&d_partial, sizeof(double) * 2 * res_blocks));
+  }
+
+  // f, u: device [nt][npts]; returns relres = ||f - K u|| / ||f|| (paradiag.cpp:243-245)
+  void run_device(const double2* f, double2* u, pdmg_solve_report* rep, double* relres) {
+    CK(cudaSetDevice(device));
+    cudaStream_t st = eng->stream;
+    eng->timed("time_dft", 2.0 * sizeof(double2) * nt * npts, [&] { launch_time_dft(*t1, f, d_g, npts, st); });
+    eng->solve_device(d_g, d_w, rep);  // step 2: the nt shifted solves (paradiag.cpp:207-236)
+    eng->timed("time_dft", 2.0 * sizeof(double2) * nt * npts, [&] { launch_time_dft(*t3, d_w, u, npts, st); });
+    if (relres) {
+      eng->timed("aao_residual", 3.0 * sizeof(double2) * nt * npts, [&] {
+        k_aao_residual<<<res_blocks, 256, 0, st>>>(u, u + (int64_t)(nt - 1) * npts, f, n, nt, 0, alpha, dt, d_partial);
+      });
+      std::vector<double> part(2 * res_blocks);
+      CK(cudaMemcpyAsync(part.data(), d_partial, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      double rr = 0.0, ff = 0.0;
+      for (int b = 0; b < res_blocks; ++b) rr += part[2 * b], ff += part[2 * b + 1];
+      *relres = ff > 0.0 ? std::sqrt(rr) / std::sqrt(ff) : std::sqrt(rr);
+    }
+    CK(cudaStreamSynchronize(st));
+    eng->drain_stats();
+  }
+
+  void run_host(const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* rep, double* relres) {
+    CK(cudaSetDevice(device));
+    const size_t bytes = sizeof(double2) * (size_t)nt * npts;
+    CK(cudaMemcpyAsync(d_f, f, bytes, cudaMemcpyHostToDevice, eng->stream));
+    run_device(d_f, d_u, rep, relres);
+    CK(cudaMemcpyAsync(u, d_u, bytes, cudaMemcpyDeviceToHost, eng->stream));
+    CK(cudaStreamSynchronize(eng->stream));
+  }
+};
+
 }  // namespace pdmg_b200
 
 using namespace pdmg_b200;
@@ -1043,10 +1175,91 @@ int pdmg_kernel_stats(const pdmg_ctx* c, int i, char* name, size_t name_len, int
 }
 double pdmg_last_updates(const pdmg_ctx* c) { return c ? c->e->last_updates : 0.0; }
 
-int pdmg_paradiag_circulant(int32_t, int32_t, double, double, const pdmg_mg_config*, int32_t, const pdmg_c128*,
-                            pdmg_c128*, pdmg_solve_report*, double*) {
-  g_last_error = "pdmg_paradiag_circulant: not implemented yet";
-  return PDMG_ERR_RUNTIME;
+struct pdmg_paradiag {
+  Paradiag p;
+  pdmg_ctx* solver = nullptr;  // non-owning view of p.eng for the stats API
+};
+
+int pdmg_paradiag_create(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t device,
+                         pdmg_paradiag** out) {
+  return guarded([&] {
+    if (!cfg || !out) throw ConfigError("pdmg_paradiag_create: NULL argument");
+    *out = nullptr;
+    auto* P = new pdmg_paradiag;
+    try {
+      P->p.setup(n, nt, alpha, dt, *cfg, device);
+    } catch (...) {
+      delete P;
+      throw;
+    }
+    P->solver = new pdmg_ctx;
+    P->solver->e.reset(P->p.eng.get());
+    *out = P;
+  });
+}
+void pdmg_paradiag_destroy(pdmg_paradiag* P) {
+  if (!P) return;
+  if (P->solver) {
+    P->solver->e.release();
+    delete P->solver;
+  }
+  delete P;
+}
+pdmg_ctx* pdmg_paradiag_solver(pdmg_paradiag* P) { return P ? P->solver : nullptr; }
+int pdmg_paradiag_run(pdmg_paradiag* P, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* rep, double* relres) {
+  return guarded([&] {
+    if (!P || !f || !u) throw ConfigError("pdmg_paradiag_run: NULL argument");
+    P->p.run_host(f, u, rep, relres);
+  });
+}
+int pdmg_paradiag_run_device(pdmg_paradiag* P, const void* d_f, void* d_u, pdmg_solve_report* rep, double* relres) {
+  return guarded([&] {
+    if (!P || !d_f || !d_u) throw ConfigError("pdmg_paradiag_run_device: NULL argument");
+    P->p.run_device(static_cast<const double2*>(d_f), static_cast<double2*>(d_u), rep, relres);
+  });
+}
+
+int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t device,
+                            const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* rep, double* relres) {
+  pdmg_paradiag* P = nullptr;
+  int st = pdmg_paradiag_create(n, nt, alpha, dt, cfg, device, &P);
+  if (st) return st;
+  st = pdmg_paradiag_run(P, f, u, rep, relres);
+  pdmg_paradiag_destroy(P);
+  return st;
+}
+
+int pdmg_time_dft(int32_t device, int32_t nt, int64_t npts, double alpha, int32_t step, const void* d_in, void* d_out,
+                  void* stream) {
+  return guarded([&] {
+    if (step != 1 && step != 3) throw ConfigError("pdmg_time_dft: step must be 1 (forward transform) or 3 (back)");
+    if (!(alpha > 0.0)) throw ConfigError("alpha-circulant: alpha must be positive");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto T = make_dft_tables(nt, alpha, step, st);
+    launch_time_dft(*T, static_cast<const double2*>(d_in), static_cast<double2*>(d_out), npts, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int pdmg_aao_residual(int32_t device, int32_t n, int32_t ntl, int32_t t0, double alpha, double dt, const void* d_u,
+                      const void* d_u_prev, const void* d_f, double* sums, void* stream) {
+  return guarded([&] {
+    if (!sums) throw ConfigError("pdmg_aao_residual: NULL sums");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int blocks = 148 * 8;
+    double* part = nullptr;
+    CK(cudaMalloc(&part, sizeof(double) * 2 * blocks));
+    k_aao_residual<<<blocks, 256, 0, st>>>(static_cast<const double2*>(d_u), static_cast<const double2*>(d_u_prev),
+                                           static_cast<const double2*>(d_f), n, ntl, t0, alpha, dt, part);
+    std::vector<double> h(2 * blocks);
+    CK(cudaMemcpyAsync(h.data(), part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(part);
+    sums[0] = sums[1] = 0.0;
+    for (int b = 0; b < blocks; ++b) sums[0] += h[2 * b], sums[1] += h[2 * b + 1];
+  });
 }
 
 }  // extern "C"

@@ -639,3 +639,132 @@ __global__ void k_pack(const typename vec2<T>::type* __restrict__ buf0, const ty
 }
 
 }  // namespace pdmg_b200
+
+// ===================================================================================================
+// ParaDIAG time direction (alpha-circulant backward Euler; restated, see DESIGN.md section 1 row P3).
+//   step 1:  g_k = (1/nt) sum_t alpha^(t/nt) f_t e^{+2 pi i t k / nt}      (dir = +1, pre-scale, 1/nt)
+//   step 3:  u_t = alpha^(-t/nt) sum_k w_k e^{-2 pi i t k / nt}           (dir = -1, post-scale)
+// Layout: [nt][npts] compact (time slices of the reference layout).  A CTA transforms DFT_P spatial
+// points: loads rows t (DFT_P contiguous complex each), runs an in-place radix-2 DIT FFT in shared
+// memory when nt is a power of two (direct O(nt^2) DFT otherwise), writes rows k.
+// ===================================================================================================
+namespace pdmg_b200 {
+
+constexpr int DFT_THREADS = 256;
+
+// tw[q] = e^{dir 2 pi i q / nt}; pre[t] multiplies the input, post[k] the output (fp64 host tables).
+__global__ void k_time_dft(const double2* __restrict__ in, double2* __restrict__ out, int nt, int log2nt, int npts,
+                           int P, const double2* __restrict__ tw, const double* __restrict__ pre,
+                           const double* __restrict__ post) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // [nt][P]
+  const int p0 = blockIdx.x * P;
+  const int np = min(P, npts - p0);
+  const int tid = threadIdx.x;
+  // load (bit-reversed time order for the radix-2 path), with the pre-scaling
+  for (int q = tid; q < nt * P; q += blockDim.x) {
+    const int t = q / P, pl = q - t * P;
+    double2 v = make_double2(0.0, 0.0);
+    if (pl < np) {
+      v = in[(int64_t)t * npts + p0 + pl];
+      const double s = pre[t];
+      v.x *= s;
+      v.y *= s;
+    }
+    const int dst = log2nt >= 0 ? (int)(__brev((unsigned)t) >> (32 - log2nt)) : t;
+    buf[dst * P + pl] = v;
+  }
+  __syncthreads();
+  if (log2nt >= 0) {
+    for (int len = 2; len <= nt; len <<= 1) {
+      const int half = len >> 1, tstep = nt / len;
+      for (int q = tid; q < (nt >> 1) * P; q += blockDim.x) {
+        const int bf = q / P, pl = q - bf * P;
+        const int grp = bf / half, j = bf - grp * half;
+        const int i0 = grp * len + j, i1 = i0 + half;
+        const double2 w = tw[j * tstep];
+        const double2 a = buf[i0 * P + pl], b = buf[i1 * P + pl];
+        const double2 wb = make_double2(w.x * b.x - w.y * b.y, w.x * b.y + w.y * b.x);
+        buf[i0 * P + pl] = make_double2(a.x + wb.x, a.y + wb.y);
+        buf[i1 * P + pl] = make_double2(a.x - wb.x, a.y - wb.y);
+      }
+      __syncthreads();
+    }
+    for (int q = tid; q < nt * P; q += blockDim.x) {
+      const int k = q / P, pl = q - k * P;
+      if (pl < np) {
+        double2 v = buf[k * P + pl];
+        const double s = post[k];
+        out[(int64_t)k * npts + p0 + pl] = make_double2(v.x * s, v.y * s);
+      }
+    }
+  } else {
+    for (int q = tid; q < nt * P; q += blockDim.x) {
+      const int k = q / P, pl = q - k * P;
+      if (pl >= np) continue;
+      double2 acc = make_double2(0.0, 0.0);
+      int idx = 0;  // (t * k) mod nt
+      for (int t = 0; t < nt; ++t) {
+        const double2 w = tw[idx], v = buf[t * P + pl];
+        acc.x += w.x * v.x - w.y * v.y;
+        acc.y += w.x * v.y + w.y * v.x;
+        idx += k;
+        if (idx >= nt) idx -= nt;
+      }
+      const double s = post[k];
+      out[(int64_t)k * npts + p0 + pl] = make_double2(acc.x * s, acc.y * s);
+    }
+  }
+}
+
+// All-at-once residual r_t = f_t - ((C_alpha (x) I + I (x) A) u)_t over the local time slices
+// [t0, t0+ntl) of a global nt (paradiag.cpp:141-183 with B = C_alpha): C_alpha row t couples u_t and
+// u_{t-1} (-1/dt, 1/dt), row 0 couples u_0 and alpha u_{nt-1}.  u_prev is the slice before t0 (u_{nt-1}
+// when t0 == 0).  Per-block partial sums of |r|^2 and |f|^2 (fixed-order, deterministic).
+__global__ void k_aao_residual(const double2* __restrict__ u, const double2* __restrict__ u_prev,
+                               const double2* __restrict__ f, int n, int ntl, int t0, double alpha, double dt,
+                               double* __restrict__ partial) {
+  const int m = n - 1, npts = m * m;
+  const double h = 1.0 / n, inv_h2 = 1.0 / (h * h), idt = 1.0 / dt;
+  double rr = 0.0, ff = 0.0;
+  const int64_t total = (int64_t)ntl * npts;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int tl = (int)(q / npts), p = (int)(q - (int64_t)tl * npts);
+    const int j = p / m, i = p - j * m;  // 0-based interior coords
+    const double2* ut = u + (int64_t)tl * npts;
+    const double2 c = ut[p];
+    double ax = 4.0 * c.x, ay = 4.0 * c.y;  // A u (unshifted 5-point, grid.cpp:69-90)
+    if (i > 0) ax -= ut[p - 1].x, ay -= ut[p - 1].y;
+    if (i < m - 1) ax -= ut[p + 1].x, ay -= ut[p + 1].y;
+    if (j > 0) ax -= ut[p - m].x, ay -= ut[p - m].y;
+    if (j < m - 1) ax -= ut[p + m].x, ay -= ut[p + m].y;
+    ax *= inv_h2, ay *= inv_h2;
+    const double2 pv = tl > 0 ? u[(int64_t)(tl - 1) * npts + p] : u_prev[p];
+    const double wp = (t0 + tl == 0) ? -alpha * idt : -idt;
+    ax += idt * c.x + wp * pv.x;
+    ay += idt * c.y + wp * pv.y;
+    const double2 fv = f[(int64_t)tl * npts + p];
+    const double rx = fv.x - ax, ry = fv.y - ay;
+    rr += rx * rx + ry * ry;
+    ff += fv.x * fv.x + fv.y * fv.y;
+  }
+  __shared__ double red[2][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    ff += __shfl_xor_sync(0xffffffffu, ff, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[0][w] = rr, red[1][w] = ff;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    double a = l < nw ? red[0][l] : 0.0, b = l < nw ? red[1][l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (l == 0) partial[2 * blockIdx.x] = a, partial[2 * blockIdx.x + 1] = b;
+  }
+}
+
+}  // namespace pdmg_b200
