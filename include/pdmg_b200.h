@@ -162,6 +162,9 @@ void pdmg_host_free(void* p);
 /* Instrumentation.  When profiling is on, every kernel launch is bracketed by CUDA events on ctx's
  * stream and attributed to a kernel class; stats accumulate until reset. */
 void* pdmg_stream(pdmg_ctx* ctx); /* the cudaStream_t all of ctx's work runs on */
+/* Solve strategy: 0 auto (default), 1 batched level passes (one launch per fused operator and level,
+ * over all shifts), 2 one CTA per shift running the whole solve loop in one launch (small grids). */
+int pdmg_set_solve_path(pdmg_ctx* ctx, int path);
 int pdmg_set_profiling(pdmg_ctx* ctx, int on);
 void pdmg_reset_stats(pdmg_ctx* ctx);
 int64_t pdmg_launch_count(const pdmg_ctx* ctx); /* kernels launched since the last reset */

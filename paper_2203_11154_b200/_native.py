@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         "pdmg_host_free": (None, [vp]),
         "pdmg_stream": (vp, [vp]),
         "pdmg_set_profiling": (C.c_int, [vp, C.c_int]),
+        "pdmg_set_solve_path": (C.c_int, [vp, C.c_int]),
         "pdmg_reset_stats": (None, [vp]),
         "pdmg_launch_count": (i64, [vp]),
         "pdmg_kernel_stats": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(i64), C.POINTER(f64),

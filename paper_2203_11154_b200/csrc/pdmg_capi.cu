@@ -330,6 +330,13 @@ struct Engine {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   double last_updates = 0.0;
+  int solve_path = 0;  // 0 auto, 1 batched level passes, 2 one CTA per shift (small grids)
+
+  bool use_small_path() const {
+    if (solve_path == 1) return false;
+    if (solve_path == 2) return true;
+    return lv[0].n <= 128 && lv.size() <= MAX_LEVELS;  // BASELINE configs 1-2: launch/sync latency bound
+  }
 
   static const KernelTable<T>& kernels() {
     static KernelTable<T> t;
@@ -651,6 +658,40 @@ struct Engine {
     CK(cudaMemsetAsync(d_iters, 0, sizeof(int) * S, stream));
     CK(cudaMemsetAsync(d_conv, 0, sizeof(int) * S, stream));
     CK(cudaMemsetAsync(d_hist, 0, sizeof(double) * S * (size_t)H, stream));
+    if (use_small_path()) {
+      if (any_singular) {
+        // the reference throws at the first coarse solve, i.e. only for shifts that run a cycle
+        std::vector<double> nb(S);
+        level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
+                   nullptr, S);
+        finalize(0, F.ntiles);
+        std::vector<int> act(S);
+        CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
+        for (int s = 0; s < S; ++s)
+          if (act[s] && coarse_singular[s])
+            throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " +
+                                        std::to_string(lv.back().n));
+      }
+      SmallArgs<T> sa{};
+      for (size_t l = 0; l < lv.size(); ++l)
+        sa.lv[l] = SmallLevel<T>{lv[l].u[0], lv[l].u[1], lv[l].b, lv[l].coef, lv[l].n, lv[l].ss};
+      sa.L = (int)lv.size();
+      sa.nu1 = cfg.nu1, sa.nu2 = cfg.nu2, sa.gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+      sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
+      sa.ainv = d_ainv, sa.coarse_N = coarse_N;
+      sa.iterations = d_iters, sa.converged = d_conv, sa.r0 = d_r0, sa.hist = d_hist, sa.n_active = d_nactive;
+      const double per_shift_bytes = 0.0;
+      (void)per_shift_bytes;
+      timed("small_solve", 0.0, [&] {
+        k_small_solve<T><<<S, SMALL_THREADS, coarse_N * sizeof(V), stream>>>(sa);
+      });
+      CK(cudaGetLastError());
+      std::vector<int> parity(H, 0);
+      CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
+      pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+      finish_report(rep, t0, H);
+      return;
+    }
     // r0 = ||b|| (multigrid.cpp:91): residual of the zero guess
     level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
                nullptr, S);
@@ -663,7 +704,6 @@ struct Engine {
         if (act[s] && coarse_singular[s])
           throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
     }
-    double cycles_done = 0.0;  // sum over shifts of cycles run
     for (int k = 1; k <= cfg.max_iter && n_active_host > 0; ++k) {
       const int n_act = n_active_host;
       const bool normed = cycle_level(0, k == 1, d_active, n_act, true);
@@ -671,18 +711,15 @@ struct Engine {
         level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr, nullptr,
                    d_active, n_act);
       parity[k] = F.cur;
-      cycles_done += n_act;
       finalize(k, F.ntiles);
     }
     CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
     pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
-    // updates per cycle per shift: (nu1+nu2) * sum_l m_l^2 * gamma^l over non-coarsest levels
-    double per_cycle = 0.0, visits = 1.0;
-    for (size_t l = 0; l + 1 < lv.size(); ++l) {
-      per_cycle += (cfg.nu1 + cfg.nu2) * (double)lv[l].m * lv[l].m * visits;
-      if (cfg.cycle == PDMG_CYCLE_W) visits *= 2;
-    }
-    last_updates = per_cycle * cycles_done;
+    finish_report(rep, t0, H);
+  }
+
+  // Copy the per-shift report back; counts the smoother updates performed (sum over shifts of cycles).
+  void finish_report(pdmg_solve_report* rep, std::chrono::steady_clock::time_point t0, int H) {
     std::vector<int> it(S), cv(S);
     std::vector<double> hist;
     CK(cudaMemcpyAsync(it.data(), d_iters, sizeof(int) * S, cudaMemcpyDeviceToHost, stream));
@@ -695,6 +732,15 @@ struct Engine {
     CK(cudaStreamSynchronize(stream));
     CK(cudaGetLastError());
     drain_stats();
+    // updates per cycle per shift: (nu1+nu2) * sum_l m_l^2 * gamma^l over non-coarsest levels
+    double per_cycle = 0.0, visits = 1.0;
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+      per_cycle += (cfg.nu1 + cfg.nu2) * (double)lv[l].m * lv[l].m * visits;
+      if (cfg.cycle == PDMG_CYCLE_W) visits *= 2;
+    }
+    double cycles_done = 0.0;
+    for (int s = 0; s < S; ++s) cycles_done += it[s];
+    last_updates = per_cycle * cycles_done;
     if (rep) {
       for (int s = 0; s < S; ++s) {
         if (rep->iterations) rep->iterations[s] = it[s];
@@ -1148,6 +1194,11 @@ void pdmg_host_free(void* p) {
 }
 
 void* pdmg_stream(pdmg_ctx* c) { return c ? (void*)c->e->stream : nullptr; }
+int pdmg_set_solve_path(pdmg_ctx* c, int path) {
+  if (!c || path < 0 || path > 2) return PDMG_ERR_CONFIG;
+  c->e->solve_path = path;
+  return PDMG_OK;
+}
 int pdmg_set_profiling(pdmg_ctx* c, int on) {
   if (!c) return PDMG_ERR_CONFIG;
   c->e->profiling = on != 0;

@@ -768,3 +768,264 @@ __global__ void k_aao_residual(const double2* __restrict__ u, const double2* __r
 }
 
 }  // namespace pdmg_b200
+
+// ===================================================================================================
+// Small-grid path: one CTA runs the WHOLE solve of one shift (multigrid.cpp:85-110 loop, V or W cycles,
+// convergence test) in a single launch.  For grids whose per-level passes are far too small to fill the
+// GPU (BASELINE configs 1-2: one 63x63 system, 32 127x127 systems) the batched path is launch- and
+// sync-latency bound; here every operator is a block-wide pass over the (L2/L1-resident) level arrays
+// separated by __syncthreads, and the host is not involved until the solve ends.
+// Level arrays use the same ghosted layout; u lives in u[0] (updated in place), u[1] holds r.
+// ===================================================================================================
+namespace pdmg_b200 {
+
+constexpr int SMALL_THREADS = 1024;
+constexpr int MAX_LEVELS = 16;
+
+template <class T>
+struct SmallLevel {
+  using V = typename vec2<T>::type;
+  V* u;   // u (level 0: the iterate; coarser: the correction e)
+  V* r;   // residual scratch
+  V* b;   // rhs (level 0: user rhs; coarser: restricted residual)
+  const LevelCoef<T>* coef;
+  int n;
+  int64_t ss;
+};
+
+template <class T>
+struct SmallArgs {
+  SmallLevel<T> lv[MAX_LEVELS];
+  int L;
+  int nu1, nu2, gamma, jacobi, max_iter;
+  double tol;
+  const typename vec2<T>::type* ainv;  // [S][N][N] coarsest inverse
+  int coarse_N;
+  int* iterations;
+  int* converged;
+  double* r0;
+  double* hist;
+  int* n_active;
+};
+
+template <class T>
+struct SmallSolver {
+  using V = typename vec2<T>::type;
+  const SmallArgs<T>& a;
+  int s;
+  double* red;  // [32] block reduction scratch (shared)
+  V* cb;        // coarsest rhs staging (shared, coarse_N)
+
+  __device__ __forceinline__ V* ptr(V* base, int l) const { return base + (int64_t)s * a.lv[l].ss; }
+  __device__ __forceinline__ LevelCoef<T> coef(int l) const { return a.lv[l].coef[s]; }
+
+  // r = b - (A + lambda I) u on level l (grid.cpp:69-100); returns the block-reduced ||r||^2 if wanted
+  __device__ double residual(int l, bool zero_u, bool want_norm) const {
+    const SmallLevel<T>& L = a.lv[l];
+    const int n = L.n, m = n - 1;
+    const LevelCoef<T> cf = coef(l);
+    const V* u = ptr(L.u, l);
+    const V* b = ptr(L.b, l);
+    V* r = ptr(L.r, l);
+    double acc2 = 0.0;
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+      const int j = q / m + 1, i = q - (j - 1) * m + 1;
+      const int64_t p = (int64_t)j * n + i;
+      V rv = b[p];
+      if (!zero_u) {
+        V acc = cmul(cf.d, u[p]);
+        acc = csub(acc, u[p - 1]);
+        acc = csub(acc, u[p + 1]);
+        acc = csub(acc, u[p - n]);
+        acc = csub(acc, u[p + n]);
+        rv = csub(rv, cscale(cf.inv_h2, acc));
+      }
+      r[p] = rv;
+      if (want_norm) acc2 += (double)rv.x * (double)rv.x + (double)rv.y * (double)rv.y;
+    }
+    __syncthreads();
+    if (!want_norm) return 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc2;
+    __syncthreads();
+    double tot = 0.0;
+    if (threadIdx.x < 32) {
+      tot = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if (threadIdx.x == 0) red[32] = tot;
+    }
+    __syncthreads();
+    tot = red[32];
+    __syncthreads();
+    return tot;
+  }
+
+  // u += omega M r (Vanka 9-point or Jacobi), in place; u := omega M r when zero_u (smoother.cpp:49-67)
+  __device__ void correct(int l, bool zero_u) const {
+    const SmallLevel<T>& L = a.lv[l];
+    const int n = L.n, m = n - 1;
+    const LevelCoef<T> cf = coef(l);
+    V* u = ptr(L.u, l);
+    const V* r = ptr(L.r, l);
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
+      const int j = q / m + 1, i = q - (j - 1) * m + 1;
+      const int64_t p = (int64_t)j * n + i;
+      V dl;
+      if (a.jacobi) {
+        dl = cmul(cf.k0, r[p]);
+      } else {
+        const V e1 = cadd(cadd(cadd(r[p - n], r[p - 1]), r[p + 1]), r[p + n]);
+        const V e2 = cadd(cadd(cadd(r[p - n - 1], r[p - n + 1]), r[p + n - 1]), r[p + n + 1]);
+        dl = cadd(cadd(cmul(cf.k0, r[p]), cmul(cf.k1, e1)), cmul(cf.k2, e2));
+      }
+      u[p] = zero_u ? dl : cadd(u[p], dl);
+    }
+    __syncthreads();
+  }
+
+  // b_{l+1} = R r_l (grid.cpp:102-121) and e_{l+1} = 0
+  __device__ void restrict_to(int l) const {
+    const SmallLevel<T>& F = a.lv[l];
+    const SmallLevel<T>& Cc = a.lv[l + 1];
+    const int nf = F.n, nc = Cc.n, mc = nc - 1;
+    const V* r = ptr(F.r, l);
+    V* bc = ptr(Cc.b, l + 1);
+    for (int q = threadIdx.x; q < mc * mc; q += blockDim.x) {
+      const int J = q / mc + 1, I = q - (J - 1) * mc + 1;
+      const int64_t c = (int64_t)(2 * J) * nf + 2 * I;
+      V sum = r[c - nf - 1];
+      sum = cadd(sum, cscale((T)2, r[c - nf]));
+      sum = cadd(sum, r[c - nf + 1]);
+      sum = cadd(sum, cscale((T)2, r[c - 1]));
+      sum = cadd(sum, cscale((T)4, r[c]));
+      sum = cadd(sum, cscale((T)2, r[c + 1]));
+      sum = cadd(sum, r[c + nf - 1]);
+      sum = cadd(sum, cscale((T)2, r[c + nf]));
+      sum = cadd(sum, r[c + nf + 1]);
+      bc[(int64_t)J * nc + I] = cscale((T)(1.0 / 16.0), sum);
+    }
+    __syncthreads();
+  }
+
+  // u_l += P e_{l+1} (grid.cpp:123-153); u_l := P e when zero_u
+  __device__ void prolong_add(int l, bool zero_u) const {
+    const SmallLevel<T>& F = a.lv[l];
+    const SmallLevel<T>& Cc = a.lv[l + 1];
+    const int nf = F.n, mf = nf - 1, nc = Cc.n;
+    V* u = ptr(F.u, l);
+    const V* e = ptr(Cc.u, l + 1);
+    for (int q = threadIdx.x; q < mf * mf; q += blockDim.x) {
+      const int j = q / mf + 1, i = q - (j - 1) * mf + 1;
+      const V* e0 = e + (int64_t)(j >> 1) * nc + (i >> 1);
+      V pv;
+      if (!(i & 1) && !(j & 1)) pv = e0[0];
+      else if ((i & 1) && !(j & 1)) pv = cscale((T)0.5, cadd(e0[0], e0[1]));
+      else if (!(i & 1) && (j & 1)) pv = cscale((T)0.5, cadd(e0[0], e0[nc]));
+      else pv = cscale((T)0.25, cadd(cadd(cadd(e0[0], e0[1]), e0[nc]), e0[nc + 1]));
+      const int64_t p = (int64_t)j * nf + i;
+      u[p] = zero_u ? pv : cadd(u[p], pv);
+    }
+    __syncthreads();
+  }
+
+  __device__ void coarse_solve(int l) const {
+    const SmallLevel<T>& L = a.lv[l];
+    const int n = L.n, m = n - 1, N = a.coarse_N;
+    const V* b = ptr(L.b, l);
+    V* u = ptr(L.u, l);
+    for (int q = threadIdx.x; q < N; q += blockDim.x) cb[q] = b[(int64_t)(q / m + 1) * n + (q % m + 1)];
+    __syncthreads();
+    const V* A = a.ainv + (int64_t)s * N * N;
+    for (int rr = threadIdx.x; rr < N; rr += blockDim.x) {
+      V acc = cz<V>();
+      for (int c = 0; c < N; ++c) acc = cadd(acc, cmul(A[(int64_t)rr * N + c], cb[c]));
+      u[(int64_t)(rr / m + 1) * n + (rr % m + 1)] = acc;
+    }
+    __syncthreads();
+  }
+
+  // cycle_on_level (multigrid.cpp:63-77) as an explicit state machine (no device recursion): st[l] counts
+  // the gamma sub-cycles started from level l; z[l] says u_l is still the zero guess.
+  __device__ void cycle(bool zero0) const {
+    int st[MAX_LEVELS];
+    bool z[MAX_LEVELS];
+    int l = 0;
+    st[0] = 0;
+    z[0] = zero0;
+    while (l >= 0) {
+      if (l + 1 == a.L) {  // coarsest: u = A^{-1} b (multigrid.cpp:64-68)
+        coarse_solve(l);
+        --l;
+        continue;
+      }
+      if (st[l] == 0) {
+        for (int k = 0; k < a.nu1; ++k) {
+          residual(l, z[l], false);
+          correct(l, z[l]);
+          z[l] = false;
+        }
+        residual(l, z[l], false);
+        restrict_to(l);  // rc = R(b - L u); ec = 0 (multigrid.cpp:71-72)
+        st[l] = 1;
+        st[l + 1] = 0;
+        z[l + 1] = true;
+        ++l;
+        continue;
+      }
+      if (st[l] < a.gamma) {  // W-cycle: second recursion from the current ec (multigrid.cpp:73-74)
+        ++st[l];
+        st[l + 1] = 0;
+        z[l + 1] = false;
+        ++l;
+        continue;
+      }
+      prolong_add(l, z[l]);  // u += P ec (multigrid.cpp:75)
+      z[l] = false;
+      for (int k = 0; k < a.nu2; ++k) {
+        residual(l, false, false);
+        correct(l, false);
+      }
+      --l;
+    }
+  }
+};
+
+template <class T>
+__global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a) {
+  using V = typename vec2<T>::type;
+  __shared__ double red[33];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmallSolver<T> S{a, (int)blockIdx.x, red, reinterpret_cast<V*>(smem_raw)};
+  const int s = blockIdx.x;
+  const int H = a.max_iter + 1;
+  // u = 0 (multigrid.cpp:90), r0 = ||b|| (:91)
+  const double r0 = sqrt(S.residual(0, true, true));
+  if (threadIdx.x == 0) {
+    a.r0[s] = r0;
+    a.hist[(int64_t)s * H] = r0;
+    a.iterations[s] = 0;
+    a.converged[s] = (r0 == 0.0 || a.tol >= 1.0) ? 1 : 0;
+  }
+  {
+    const SmallLevel<T>& L0 = a.lv[0];
+    V* u = S.ptr(L0.u, 0);
+    const int n = L0.n, m = n - 1;
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) u[(int64_t)(q / m + 1) * n + (q % m + 1)] = cz<V>();
+    __syncthreads();
+  }
+  if (r0 == 0.0 || a.tol >= 1.0) return;
+  for (int k = 1; k <= a.max_iter; ++k) {
+    S.cycle(k == 1);
+    const double rk = sqrt(S.residual(0, false, true));
+    if (threadIdx.x == 0) {
+      a.hist[(int64_t)s * H + k] = rk;
+      a.iterations[s] = k;
+    }
+    if (rk <= a.tol * r0) {
+      if (threadIdx.x == 0) a.converged[s] = 1;
+      break;
+    }
+  }
+}
+
+}  // namespace pdmg_b200

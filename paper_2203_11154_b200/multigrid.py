@@ -317,6 +317,10 @@ class BatchedMultigridHierarchy:
         return out
 
     # -- instrumentation ---------------------------------------------------------------------
+    def set_solve_path(self, path: str) -> None:
+        """'auto', 'batched' (level passes over all shifts) or 'small' (one CTA per shift, one launch)."""
+        _check(N.lib().pdmg_set_solve_path(self._h, {"auto": 0, "batched": 1, "small": 2}[path]))
+
     def set_profiling(self, on: bool) -> None:
         _check(N.lib().pdmg_set_profiling(self._h, 1 if on else 0))
 

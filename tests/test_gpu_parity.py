@@ -88,8 +88,9 @@ def test_one_cycle_parity(oracle, cyc):
         assert rel(out[s], oracle.cycle(n, lam, cyc, u[s], b[s])) < 1e-12
 
 
-def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10):
+def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10, path="auto"):
     with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, mgcfg(cfg)) as H:
+        H.set_solve_path(path)
         u, reps = H.solve(b)
     ref = oracle.solve_batch(n, np.asarray(lams, np.complex128), cfg, b, threads=8)
     for s in range(len(lams)):
@@ -104,28 +105,43 @@ def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10):
     return u, reps, ref
 
 
-def test_config1_single_shift(oracle):
+PATHS = ["batched", "small"]
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_config1_single_shift(oracle, path):
     """BASELINE config 1: h=1/64, lambda_3 of the n=32 circulant family, seed 0, V(1,1), tol 1e-10."""
     lam = oracle.circulant_shifts(0.01, 32, 1 / 32, 3, 1)
     b = oracle.random_complex(0, 63 * 63).reshape(1, 63, 63)
-    u, reps, ref = _check_solve(oracle, 64, lam, b, Cfg())
+    u, reps, ref = _check_solve(oracle, 64, lam, b, Cfg(), path=path)
     assert reps[0].iterations == 11
 
 
-def test_config2_batch32(oracle):
+@pytest.mark.parametrize("path", PATHS)
+def test_config2_batch32(oracle, path):
     """BASELINE config 2: h=1/128, 32 shifts, seed 1 shift-major, V(1,1): 11-12 cycles per shift."""
     lams = oracle.circulant_shifts(0.01, 32, 1 / 32)
     b = oracle.random_complex(1, 32 * 127 * 127).reshape(32, 127, 127)
-    u, reps, ref = _check_solve(oracle, 128, lams, b, Cfg())
+    u, reps, ref = _check_solve(oracle, 128, lams, b, Cfg(), path=path)
     assert set(r.iterations for r in reps) <= {11, 12}
 
 
-def test_readme_w10_rates(oracle):
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("cyc", [Cfg(nu1=0, nu2=2), Cfg(nu1=2, nu2=0), Cfg(nu1=2, nu2=1, cycle="W"),
+                                 Cfg(smoother="jacobi", omega=0.8, tol=1e-8)])
+def test_cycle_variants_solve(oracle, path, cyc):
+    lams = oracle.circulant_shifts(0.01, 32, 1 / 32)[:3]
+    b = oracle.random_complex(8, 3 * 63 * 63).reshape(3, 63, 63)
+    _check_solve(oracle, 64, lams, b, cyc, path=path)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_readme_w10_rates(oracle, path):
     """proj/README.md:37-41: W(1,0) at h=1/64, lambda=0: Vanka 14 cycles (0.273), Jacobi 32 (0.590)."""
     b = oracle.random_complex(123, 63 * 63).reshape(1, 63, 63)
-    _, rv, _ = _check_solve(oracle, 64, [0.0], b, Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8))
+    _, rv, _ = _check_solve(oracle, 64, [0.0], b, Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8), path=path)
     _, rj, _ = _check_solve(oracle, 64, [0.0], b, Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8,
-                                                       smoother="jacobi", omega=0.8))
+                                                       smoother="jacobi", omega=0.8), path=path)
     assert rv[0].iterations == 14 and abs(rv[0].rate - 0.273) < 0.001
     assert rj[0].iterations == 32 and abs(rj[0].rate - 0.590) < 0.001
 
@@ -138,7 +154,8 @@ def test_config3_subset(oracle):
     _check_solve(oracle, n, lams, b, Cfg(nu1=2, nu2=2))
 
 
-def test_edge_cases(oracle):
+@pytest.mark.parametrize("path", PATHS)
+def test_edge_cases(oracle, path):
     """multigrid test 'report edge cases' (test_multigrid.cpp:128-163) on the GPU path."""
     n = 16
     m = n - 1
@@ -148,6 +165,7 @@ def test_edge_cases(oracle):
     # shift 0: b = 0 converges at 0 iterations; others run
     cfg = Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8)
     with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0, 0.0, 0.0], mgcfg(cfg)) as H:
+        H.set_solve_path(path)
         u, reps = H.solve(b)
     assert reps[0].converged and reps[0].iterations == 0 and reps[0].rate == 0.0
     assert np.all(u[0] == 0)
@@ -155,6 +173,7 @@ def test_edge_cases(oracle):
     # max_iter exhaustion reports non-convergence
     cfg2 = Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-14, max_iter=1)
     with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0], mgcfg(cfg2)) as H:
+        H.set_solve_path(path)
         u, reps = H.solve(b[2:3])
     assert not reps[0].converged and reps[0].iterations == 1
     h = reps[0].residual_history
@@ -162,17 +181,20 @@ def test_edge_cases(oracle):
     # tol >= 1 converges with zero iterations
     cfg3 = Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1.0)
     with P.BatchedMultigridHierarchy(P.Grid2D(n), [0.0], mgcfg(cfg3)) as H:
+        H.set_solve_path(path)
         u, reps = H.solve(b[1:2])
     assert reps[0].converged and reps[0].iterations == 0
 
 
-def test_singular_coarse_detected():
+@pytest.mark.parametrize("path", PATHS)
+def test_singular_coarse_detected(path):
     """test_multigrid.cpp:174-185: lambda = -mu_11 of the coarsest grid raises at solve."""
     cg = 8
     h = 1 / cg
     mu = (4 - 2 * np.cos(np.pi * h) - 2 * np.cos(np.pi * h)) / (h * h)
     cfg = P.MultigridConfig()
     with P.BatchedMultigridHierarchy(P.Grid2D(16), [-mu], cfg) as H:
+        H.set_solve_path(path)
         assert H.coarse_singular(0)
         with pytest.raises(P.SingularOperatorError, match="singular on grid n = 8"):
             H.solve(P.random_rhs(16, 3).reshape(1, 15, 15))
