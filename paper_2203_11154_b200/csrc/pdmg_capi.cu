@@ -280,12 +280,38 @@ struct Stat {
   double ms = 0.0, bytes = 0.0;
 };
 
-struct CtxBase {
-  virtual ~CtxBase() = default;
+// Precision-independent part of an engine (what the C ABI needs without knowing the storage type).
+struct EngineBase {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int S = 0;
+  pdmg_mg_config cfg{};
+  std::vector<int> ln;
+  std::vector<cplx> lambdas;
+  std::vector<uint8_t> coarse_singular;
+  bool any_singular = false;
+  bool profiling = false;
+  int64_t launches = 0;
+  std::map<std::string, Stat> stats;
+  double last_updates = 0.0;
+  int solve_path = 0;  // 0 auto, 1 batched level passes, 2 one CTA per shift (small grids)
+
+  virtual ~EngineBase() = default;
+  virtual void setup_host(const pdmg_batch_desc& d) = 0;
+  virtual void setup_device(int dev) = 0;
+  virtual void solve_host(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) = 0;
+  virtual void solve_device(const double2* d_b, double2* d_u, pdmg_solve_report* rep) = 0;
+  virtual void cycle_host(pdmg_c128* u, const pdmg_c128* b) = 0;
+  virtual void op_smooth(int l, const pdmg_c128* u, const pdmg_c128* b, pdmg_c128* out) = 0;
+  virtual void op_residual(int l, const pdmg_c128* b, const pdmg_c128* u, pdmg_c128* r) = 0;
+  virtual void op_restrict(int l, const pdmg_c128* fine, pdmg_c128* coarse) = 0;
+  virtual void op_prolong(int l, const pdmg_c128* coarse, pdmg_c128* fine) = 0;
+  virtual void op_norm(int l, const pdmg_c128* v, double* norms) = 0;
+  virtual void op_coarse_solve(const pdmg_c128* b, pdmg_c128* u) = 0;
 };
 
 template <class T>
-struct Engine {
+struct Engine : EngineBase {
   using V = typename vec2<T>::type;
   struct Level {
     int n = 0, m = 0;
@@ -294,34 +320,23 @@ struct Engine {
     V* u[2] = {nullptr, nullptr};
     V* b = nullptr;
     int ntx = 0, nty = 0, ntiles = 0, H = 0;
-    LevelCoef<T>* coef = nullptr;
+    LevelCoef* coef = nullptr;
     int cur = 0;
     bool uzero = false;
   };
 
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int S = 0;
-  pdmg_mg_config cfg{};
-  std::vector<int> ln;
-  std::vector<cplx> lambdas;
   std::vector<Level> lv;
-  std::vector<uint8_t> coarse_singular;
-  bool any_singular = false;
-  V* d_ainv = nullptr;
+  double2* d_ainv = nullptr;
   int coarse_N = 0;
   int *d_active = nullptr, *d_iters = nullptr, *d_conv = nullptr, *d_nactive = nullptr, *d_parity = nullptr;
   int* d_ones = nullptr;
   double *d_r0 = nullptr, *d_hist = nullptr, *d_partial = nullptr, *d_norms = nullptr;
-  V* d_stage = nullptr;
+  double2* d_stage = nullptr;  // compact complex128 host-I/O staging
   size_t stage_elems = 0;
   int* h_nactive = nullptr;
   int n_active_host = 0;
   const KernelTable<T>* table = nullptr;
   // instrumentation
-  bool profiling = false;
-  int64_t launches = 0;
-  std::map<std::string, Stat> stats;
   struct Pending {
     std::string cls;
     cudaEvent_t e0, e1;
@@ -329,9 +344,6 @@ struct Engine {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
-  double last_updates = 0.0;
-  int solve_path = 0;  // 0 auto, 1 batched level passes, 2 one CTA per shift (small grids)
-
   bool use_small_path() const {
     if (solve_path == 1) return false;
     if (solve_path == 2) return true;
@@ -373,7 +385,7 @@ struct Engine {
   }
 
   // ---- construction: host validation first (no CUDA), then device allocation ----------------
-  void setup_host(const pdmg_batch_desc& d) {
+  void setup_host(const pdmg_batch_desc& d) override {
     if (d.n_shifts < 1) throw ConfigError("pdmg_create: n_shifts must be >= 1");
     if (d.n_shifts > 65535) throw ConfigError("pdmg_create: n_shifts must be <= 65535 per context");
     if (!d.lambdas) throw ConfigError("pdmg_create: lambdas is NULL");
@@ -398,7 +410,7 @@ struct Engine {
                         " (limit 128)");
   }
 
-  void setup_device(int dev) {
+  void setup_device(int dev) override {
     device = dev;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
@@ -423,7 +435,7 @@ struct Engine {
       Lv.nty = (Lv.n + Lv.H - 1) / Lv.H;
       Lv.ntiles = Lv.ntx * Lv.nty;
       // coefficients (multigrid.cpp:47-58 per level; smoother.cpp:31-40 stencil; grid.cpp:73 diagonal)
-      std::vector<LevelCoef<T>> hc(S);
+      std::vector<LevelCoef> hc(S);
       const double h = 1.0 / Lv.n;
       for (int s = 0; s < S; ++s) {
         const cplx eta = lambdas[s] * (h * h);
@@ -440,33 +452,32 @@ struct Engine {
             k0 = cfg.omega * jacobi_weight(eta, h);
           }
         }
-        LevelCoef<T>& c = hc[s];
-        c.d.x = (T)dd.real(), c.d.y = (T)dd.imag();
-        c.k0.x = (T)k0.real(), c.k0.y = (T)k0.imag();
-        c.k1.x = (T)k1.real(), c.k1.y = (T)k1.imag();
-        c.k2.x = (T)k2.real(), c.k2.y = (T)k2.imag();
-        c.inv_h2 = (T)(1.0 / (h * h));
+        LevelCoef& c = hc[s];
+        c.d = make_double2(dd.real(), dd.imag());
+        c.k0 = make_double2(k0.real(), k0.imag());
+        c.k1 = make_double2(k1.real(), k1.imag());
+        c.k2 = make_double2(k2.real(), k2.imag());
+        c.inv_h2 = 1.0 / (h * h);
         c.pad_ = 0;
       }
-      CK(cudaMalloc(&Lv.coef, sizeof(LevelCoef<T>) * S));
-      CK(cudaMemcpyAsync(Lv.coef, hc.data(), sizeof(LevelCoef<T>) * S, cudaMemcpyHostToDevice, stream));
+      CK(cudaMalloc(&Lv.coef, sizeof(LevelCoef) * S));
+      CK(cudaMemcpyAsync(Lv.coef, hc.data(), sizeof(LevelCoef) * S, cudaMemcpyHostToDevice, stream));
     }
     // coarsest factorizations (dense.cpp:82-88), one per shift
     const int nc = ln.back(), mc = nc - 1;
     coarse_N = mc * mc;
     coarse_singular.assign(S, 0);
-    std::vector<V> hinv((size_t)S * coarse_N * coarse_N);
+    std::vector<double2> hinv((size_t)S * coarse_N * coarse_N);
     for (int s = 0; s < S; ++s) {
       CoarseFactor cf = factor_coarse(nc, lambdas[s]);
       coarse_singular[s] = cf.singular;
       any_singular |= cf.singular;
       for (size_t q = 0; q < cf.inv.size(); ++q) {
-        hinv[(size_t)s * coarse_N * coarse_N + q].x = (T)cf.inv[q].real();
-        hinv[(size_t)s * coarse_N * coarse_N + q].y = (T)cf.inv[q].imag();
+        hinv[(size_t)s * coarse_N * coarse_N + q] = make_double2(cf.inv[q].real(), cf.inv[q].imag());
       }
     }
-    CK(cudaMalloc(&d_ainv, sizeof(V) * hinv.size()));
-    CK(cudaMemcpyAsync(d_ainv, hinv.data(), sizeof(V) * hinv.size(), cudaMemcpyHostToDevice, stream));
+    CK(cudaMalloc(&d_ainv, sizeof(double2) * hinv.size()));
+    CK(cudaMemcpyAsync(d_ainv, hinv.data(), sizeof(double2) * hinv.size(), cudaMemcpyHostToDevice, stream));
     // solve state
     int maxtiles = 1;
     for (auto& Lv : lv) maxtiles = std::max(maxtiles, Lv.ntiles);
@@ -566,7 +577,7 @@ struct Engine {
     const int thr = std::min(1024, std::max(32, ((coarse_N + 31) / 32) * 32));
     const double bytes = (double)S * coarse_N * (coarse_N + 2) * sizeof(V);
     timed("coarse_solve", bytes, [&] {
-      k_coarse_solve<T><<<S, thr, coarse_N * sizeof(V), stream>>>(b, u, d_ainv, active, Lv.n, Lv.ss);
+      k_coarse_solve<T><<<S, thr, coarse_N * sizeof(double2), stream>>>(b, u, d_ainv, active, Lv.n, Lv.ss);
     });
   }
 
@@ -630,14 +641,14 @@ struct Engine {
     n_active_host = *h_nactive;
   }
 
-  void unpack(const V* src, V* dst, int l) {
+  void unpack(const double2* src, V* dst, int l) {
     const Level& Lv = lv[l];
     const int64_t total = (int64_t)S * Lv.m * Lv.m;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     timed("unpack", (double)total * 2 * sizeof(V),
           [&] { k_unpack<T><<<blocks, 256, 0, stream>>>(src, dst, Lv.n, Lv.ss, total); });
   }
-  void pack(const V* b0, const V* b1, const int* iters, const int* parity, V* dst, int l) {
+  void pack(const V* b0, const V* b1, const int* iters, const int* parity, double2* dst, int l) {
     const Level& Lv = lv[l];
     const int64_t total = (int64_t)S * Lv.m * Lv.m;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
@@ -646,7 +657,7 @@ struct Engine {
   }
 
   // ---- MultigridHierarchy::solve for all shifts (multigrid.cpp:85-110) -----------------------
-  void solve_device(const V* d_b, V* d_u, pdmg_solve_report* rep) {
+  void solve_device(const double2* d_b, double2* d_u, pdmg_solve_report* rep) override {
     const auto t0 = std::chrono::steady_clock::now();
     CK(cudaSetDevice(device));
     Level& F = lv[0];
@@ -683,7 +694,7 @@ struct Engine {
       const double per_shift_bytes = 0.0;
       (void)per_shift_bytes;
       timed("small_solve", 0.0, [&] {
-        k_small_solve<T><<<S, SMALL_THREADS, coarse_N * sizeof(V), stream>>>(sa);
+        k_small_solve<T><<<S, SMALL_THREADS, coarse_N * sizeof(double2), stream>>>(sa);
       });
       CK(cudaGetLastError());
       std::vector<int> parity(H, 0);
@@ -767,22 +778,21 @@ struct Engine {
   }
 
   // ---- host I/O staging --------------------------------------------------------------------
-  V* stage(size_t elems) {
+  double2* stage(size_t elems) {
     if (elems > stage_elems) {
       cudaFree(d_stage);
       d_stage = nullptr;
-      CK(cudaMalloc(&d_stage, elems * sizeof(V)));
+      CK(cudaMalloc(&d_stage, elems * sizeof(double2)));
       stage_elems = elems;
     }
     return d_stage;
   }
   size_t compact_elems(int l) const { return (size_t)S * lv[l].m * lv[l].m; }
-  void h2d(const pdmg_c128* src, V* dst, size_t elems) {
-    static_assert(sizeof(V) == sizeof(pdmg_c128), "c128 host I/O only for c128 engines");
-    CK(cudaMemcpyAsync(dst, src, elems * sizeof(V), cudaMemcpyHostToDevice, stream));
+  void h2d(const pdmg_c128* src, double2* dst, size_t elems) {
+    CK(cudaMemcpyAsync(dst, src, elems * sizeof(double2), cudaMemcpyHostToDevice, stream));
   }
-  void d2h(const V* src, pdmg_c128* dst, size_t elems) {
-    CK(cudaMemcpyAsync(dst, src, elems * sizeof(V), cudaMemcpyDeviceToHost, stream));
+  void d2h(const double2* src, pdmg_c128* dst, size_t elems) {
+    CK(cudaMemcpyAsync(dst, src, elems * sizeof(double2), cudaMemcpyDeviceToHost, stream));
   }
   void check_level(int l, int need_coarser) const {
     if (l < 0 || l + need_coarser >= (int)lv.size())
@@ -790,23 +800,23 @@ struct Engine {
                         "-level hierarchy");
   }
 
-  void solve_host(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) {
+  void solve_host(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) override {
     CK(cudaSetDevice(device));
     const size_t N = compact_elems(0);
-    V* st = stage(2 * N);
+    double2* st = stage(2 * N);
     h2d(b, st, N);
     solve_device(st, st + N, rep);
     d2h(st + N, u, N);
     CK(cudaStreamSynchronize(stream));
   }
 
-  void cycle_host(pdmg_c128* u, const pdmg_c128* b) {
+  void cycle_host(pdmg_c128* u, const pdmg_c128* b) override {
     CK(cudaSetDevice(device));
     if (any_singular)
       throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
     Level& F = lv[0];
     const size_t N = compact_elems(0);
-    V* st = stage(2 * N);
+    double2* st = stage(2 * N);
     h2d(b, st, N);
     h2d(u, st + N, N);
     unpack(st, F.b, 0);
@@ -821,12 +831,12 @@ struct Engine {
   }
 
   // level operators ----------------------------------------------------------------------------
-  void op_smooth(int l, const pdmg_c128* u, const pdmg_c128* b, pdmg_c128* out) {
+  void op_smooth(int l, const pdmg_c128* u, const pdmg_c128* b, pdmg_c128* out) override {
     check_level(l, 1);
     CK(cudaSetDevice(device));
     Level& Lv = lv[l];
     const size_t N = compact_elems(l);
-    V* st = stage(2 * N);
+    double2* st = stage(2 * N);
     h2d(u, st, N);
     h2d(b, st + N, N);
     unpack(st, Lv.u[0], l);
@@ -837,12 +847,12 @@ struct Engine {
     d2h(st, out, N);
     finish();
   }
-  void op_residual(int l, const pdmg_c128* b, const pdmg_c128* u, pdmg_c128* r) {
+  void op_residual(int l, const pdmg_c128* b, const pdmg_c128* u, pdmg_c128* r) override {
     check_level(l, 0);
     CK(cudaSetDevice(device));
     Level& Lv = lv[l];
     const size_t N = compact_elems(l);
-    V* st = stage(2 * N);
+    double2* st = stage(2 * N);
     h2d(u, st, N);
     h2d(b, st + N, N);
     unpack(st, Lv.u[0], l);
@@ -853,12 +863,12 @@ struct Engine {
     d2h(st, r, N);
     finish();
   }
-  void op_restrict(int l, const pdmg_c128* fine, pdmg_c128* coarse) {
+  void op_restrict(int l, const pdmg_c128* fine, pdmg_c128* coarse) override {
     check_level(l, 1);
     CK(cudaSetDevice(device));
     Level &Lv = lv[l], &Lc = lv[l + 1];
     const size_t N = compact_elems(l), Nc = compact_elems(l + 1);
-    V* st = stage(N + Nc);
+    double2* st = stage(N + Nc);
     h2d(fine, st, N);
     unpack(st, Lv.b, l);
     level_pass(l, Variant{false, false, false, POST_RESTRICT, false, false}, nullptr, nullptr, Lv.b, nullptr, Lc.b,
@@ -867,12 +877,12 @@ struct Engine {
     d2h(st + N, coarse, Nc);
     finish();
   }
-  void op_prolong(int l, const pdmg_c128* coarse, pdmg_c128* fine) {
+  void op_prolong(int l, const pdmg_c128* coarse, pdmg_c128* fine) override {
     check_level(l, 1);
     CK(cudaSetDevice(device));
     Level &Lv = lv[l], &Lc = lv[l + 1];
     const size_t N = compact_elems(l), Nc = compact_elems(l + 1);
-    V* st = stage(N + Nc);
+    double2* st = stage(N + Nc);
     h2d(coarse, st + N, Nc);
     unpack(st + N, Lc.u[0], l + 1);
     level_pass(l, Variant{false, true, false, POST_NONE, true, false}, nullptr, Lv.u[1], Lv.b, Lc.u[0], nullptr,
@@ -881,12 +891,12 @@ struct Engine {
     d2h(st, fine, N);
     finish();
   }
-  void op_norm(int l, const pdmg_c128* v, double* norms) {
+  void op_norm(int l, const pdmg_c128* v, double* norms) override {
     check_level(l, 0);
     CK(cudaSetDevice(device));
     Level& Lv = lv[l];
     const size_t N = compact_elems(l);
-    V* st = stage(N);
+    double2* st = stage(N);
     h2d(v, st, N);
     unpack(st, Lv.b, l);
     level_pass(l, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, Lv.b, nullptr, nullptr,
@@ -897,14 +907,14 @@ struct Engine {
     CK(cudaMemcpyAsync(norms, d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, stream));
     finish();
   }
-  void op_coarse_solve(const pdmg_c128* b, pdmg_c128* u) {
+  void op_coarse_solve(const pdmg_c128* b, pdmg_c128* u) override {
     CK(cudaSetDevice(device));
     if (any_singular)
       throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
     const int l = (int)lv.size() - 1;
     Level& Lv = lv[l];
     const size_t N = compact_elems(l);
-    V* st = stage(2 * N);
+    double2* st = stage(2 * N);
     h2d(b, st, N);
     unpack(st, Lv.b, l);
     coarse_solve(Lv.b, Lv.u[0], nullptr);
@@ -1056,7 +1066,7 @@ struct Paradiag {
 using namespace pdmg_b200;
 
 struct pdmg_ctx {
-  std::unique_ptr<Engine<double>> e;
+  std::unique_ptr<EngineBase> e;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -1082,9 +1092,13 @@ int pdmg_create(const pdmg_batch_desc* d, pdmg_ctx** out) {
   return guarded([&] {
     if (!d || !out) throw ConfigError("pdmg_create: NULL argument");
     *out = nullptr;
-    if (d->precision != PDMG_PREC_C128)
-      throw ConfigError("pdmg_create: precision " + std::to_string(d->precision) + " not supported (use PDMG_PREC_C128)");
-    auto e = std::make_unique<Engine<double>>();
+    std::unique_ptr<EngineBase> e;
+    if (d->precision == PDMG_PREC_C128)
+      e = std::make_unique<Engine<double>>();
+    else if (d->precision == PDMG_PREC_C64)
+      e = std::make_unique<Engine<float>>();
+    else
+      throw ConfigError("pdmg_create: unknown precision " + std::to_string(d->precision));
     e->device = -1;
     e->setup_host(*d);  // all ConfigError / SingularOperatorError paths run before any CUDA call
     e->setup_device(d->device);
@@ -1095,9 +1109,9 @@ int pdmg_create(const pdmg_batch_desc* d, pdmg_ctx** out) {
 }
 
 void pdmg_destroy(pdmg_ctx* c) { delete c; }
-int pdmg_num_levels(const pdmg_ctx* c) { return c ? (int)c->e->lv.size() : 0; }
+int pdmg_num_levels(const pdmg_ctx* c) { return c ? (int)c->e->ln.size() : 0; }
 int pdmg_level_n(const pdmg_ctx* c, int l) {
-  return (c && l >= 0 && l < (int)c->e->lv.size()) ? c->e->lv[l].n : -1;
+  return (c && l >= 0 && l < (int)c->e->ln.size()) ? c->e->ln[l] : -1;
 }
 int pdmg_num_shifts(const pdmg_ctx* c) { return c ? c->e->S : 0; }
 int pdmg_coarse_singular(const pdmg_ctx* c, int s) {

@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace pdmg_b200 {
 
 template <class T>
@@ -66,15 +68,30 @@ __device__ __forceinline__ V cscale(S s, V a) {
   return a;
 }
 
+// Storage type T (double: complex128, float: complex64); all arithmetic is fp64.  For complex64 the
+// fp32 values are widened on load, so the residual b - (A + lambda I) u of the *stored* iterate is
+// formed exactly (an fp32-arithmetic residual floors at 1.2e-5 > the 1e-5 target).
+__device__ __forceinline__ double2 ld2(double2 v) { return v; }
+__device__ __forceinline__ double2 ld2(float2 v) { return make_double2((double)v.x, (double)v.y); }
+template <class V>
+__device__ __forceinline__ V st2(double2 v);
+template <>
+__device__ __forceinline__ double2 st2<double2>(double2 v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ float2 st2<float2>(double2 v) {
+  return make_float2((float)v.x, (float)v.y);
+}
+
 // Per (level, shift) operator coefficients, precomputed on the host in fp64 (multigrid.cpp:47-58).
-template <class T>
 struct LevelCoef {
-  typename vec2<T>::type d;  // 4 + eta, eta = lambda h^2              (grid.cpp:73)
-  typename vec2<T>::type k0; // Vanka: omega*(h^2/4)*4a ; Jacobi: omega*h^2/(4+eta)
-  typename vec2<T>::type k1; // Vanka: omega*(h^2/4)*2b
-  typename vec2<T>::type k2; // Vanka: omega*(h^2/4)*c
-  T inv_h2;                  // 1/h^2
-  T pad_;
+  double2 d;      // 4 + eta, eta = lambda h^2              (grid.cpp:73)
+  double2 k0;     // Vanka: omega*(h^2/4)*4a ; Jacobi: omega*h^2/(4+eta)
+  double2 k1;     // Vanka: omega*(h^2/4)*2b
+  double2 k2;     // Vanka: omega*(h^2/4)*c
+  double inv_h2;  // 1/h^2
+  double pad_;
 };
 
 enum : int { POST_NONE = 0, POST_NORM = 1, POST_RESTRICT = 2, POST_RESID = 3 };
@@ -99,7 +116,7 @@ struct LevelArgs {
   const V* ec;               // coarse correction (PROLONG), coarse layout
   V* bc;                     // coarse rhs output (POST_RESTRICT), coarse layout
   double* partial;           // [shift][tile] partial sums of |r2|^2 (POST_NORM)
-  const LevelCoef<T>* coef;  // [shift] at this level
+  const LevelCoef* coef;     // [shift] at this level
   const int* active;         // [shift] convergence mask, or nullptr
   int n, nc;                 // fine / coarse subdivisions
   int64_t ss, ssc;           // shift strides (elements)
@@ -134,20 +151,28 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, un
       : "memory");
 }
 
-// Halo widths and shared-memory footprint of a k_level instantiation.
+// Halo widths and shared-memory footprint of a k_level instantiation.  Rings fed by TMA (u_in, b, e_c)
+// hold the storage type; r, delta and the restriction sums hold fp64.  With 8-byte elements the TMA-fed
+// buffers start at an even column (16-byte aligned segments), so their halos are rounded up to even.
 template <class T, bool USE_A, bool SWEEP, int POST, bool PROLONG>
 struct LevelShape {
+  using V = typename vec2<T>::type;
   static constexpr bool HASD = POST != POST_NONE;
   static constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
   static constexpr int hC = HASD ? hD + 1 : 0;
   static constexpr int hA = SWEEP ? hC + 2 : hC;
   static constexpr int hB = hA - 1;
-  static constexpr int WA = TILE_W + 2 * hA, WB = TILE_W + 2 * hB, WC = TILE_W + 2 * hC;
+  static constexpr bool EVEN = sizeof(V) == 8;
+  static constexpr int hAs = EVEN ? (hA + 1) / 2 * 2 : hA;  // storage halo of the u ring
+  static constexpr int hBs = EVEN ? (hB + 1) / 2 * 2 : hB;  // storage halo of the b buffer
+  static constexpr int WA = TILE_W + 2 * hAs, WBb = TILE_W + 2 * hBs;
+  static constexpr int WB = TILE_W + 2 * hB, WC = TILE_W + 2 * hC;
   static constexpr int RR = POST == POST_RESTRICT ? RING_R : RING;  // rows of the r / delta rings
-  static constexpr size_t elems = (size_t)(USE_A ? ARING * WA : 0) + (SWEEP ? (CHUNK + RR) * WB : 0) +
-                                  (SWEEP && HASD ? RR * WC : 0) + (PROLONG ? CB_ROWS * CB_COLS : 0) +
-                                  (POST == POST_RESTRICT ? 2 * RGROUPS * VX_W : 0);
-  static constexpr size_t bytes = 32 + elems * sizeof(typename vec2<T>::type) + 16 * sizeof(double);
+  static constexpr size_t bytes_v = sizeof(V) * ((size_t)(USE_A ? ARING * WA : 0) + (SWEEP ? CHUNK * WBb : 0) +
+                                                 (PROLONG ? CB_ROWS * CB_COLS : 0));
+  static constexpr size_t bytes_d = sizeof(double2) * ((size_t)(SWEEP ? RR * WB : 0) + (SWEEP && HASD ? RR * WC : 0) +
+                                                       (POST == POST_RESTRICT ? 2 * RGROUPS * VX_W : 0));
+  static constexpr size_t bytes = 32 + bytes_v + bytes_d + 16 * sizeof(double);
   // CTAs per SM the shared memory allows (227 KB usable); used as the register budget hint
   static constexpr int min_blocks = bytes <= 75 * 1024 ? 3 : 2;
   static_assert(!SWEEP || WB * RGROUPS <= NTHREADS, "stage-B tasks exceed the CTA");
@@ -167,10 +192,12 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
   constexpr bool USE_A = LOADU || PROLONG;  // otherwise u_in == 0
   using SH = LevelShape<T, USE_A, SWEEP, POST, PROLONG>;
   constexpr bool HASD = SH::HASD;
-  constexpr int hA = SH::hA, hB = SH::hB, hC = SH::hC, hD = SH::hD;
-  constexpr int WA = SH::WA, WB = SH::WB, WC = SH::WC, RR = SH::RR;
+  using D2 = double2;
+  constexpr int hA = SH::hA, hB = SH::hB, hC = SH::hC, hD = SH::hD, hAs = SH::hAs, hBs = SH::hBs;
+  constexpr int WA = SH::WA, WB = SH::WB, WBb = SH::WBb, WC = SH::WC, RR = SH::RR;
   constexpr int xD = SWEEP ? 3 : 1;  // stage index of D
   constexpr int VB = (int)sizeof(V);
+  constexpr int ALN = SH::EVEN ? 2 : 1;  // TMA segment alignment in elements
 
   const int shift = blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;  // converged shifts are frozen
@@ -183,22 +210,23 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [2] chunk barriers
-  V* sm = reinterpret_cast<V*>(smem_raw + 32);
-  V* RA = sm;  // u_in (+ P e_c): ARING x WA, local col 0 = storage col c0 - hA
+  D2* dm_ = reinterpret_cast<D2*>(smem_raw + 32);  // fp64 buffers first (16-B aligned)
+  D2* RB = dm_;  // r = b - L u_in: RR x WB
+  if constexpr (SWEEP) dm_ += RR * WB;
+  D2* RC = dm_;  // delta = omega M r: RR x WC
+  if constexpr (SWEEP && HASD) dm_ += RR * WC;
+  D2* VX = dm_;  // vertical 1-2-1 sums exchanged for the restriction: [2*RGROUPS][VX_W]
+  if constexpr (POST == POST_RESTRICT) dm_ += 2 * RGROUPS * VX_W;
+  double* red = reinterpret_cast<double*>(dm_);
+  V* sm = reinterpret_cast<V*>(red + 16);
+  V* RA = sm;  // u_in (+ P e_c): ARING x WA, local col 0 = storage col c0 - hAs
   if constexpr (USE_A) sm += ARING * WA;
-  V* Bb = sm;  // b rows of the current B step: CHUNK x WB
-  if constexpr (SWEEP) sm += CHUNK * WB;
-  V* RB = sm;  // r = b - L u_in: RR x WB
-  if constexpr (SWEEP) sm += RR * WB;
-  V* RC = sm;  // delta = omega M r: RR x WC
-  if constexpr (SWEEP && HASD) sm += RR * WC;
+  V* Bb = sm;  // b rows of the current B step: CHUNK x WBb, local col 0 = storage col c0 - hBs
+  if constexpr (SWEEP) sm += CHUNK * WBb;
   V* CB = sm;  // coarse block for the prolongation
   if constexpr (PROLONG) sm += CB_ROWS * CB_COLS;
-  V* VX = sm;  // vertical 1-2-1 sums exchanged for the restriction: [2*RGROUPS][VX_W]
-  if constexpr (POST == POST_RESTRICT) sm += 2 * RGROUPS * VX_W;
-  double* red = reinterpret_cast<double*>(sm);
 
-  const LevelCoef<T> cf = a.coef[shift];
+  const LevelCoef cf = a.coef[shift];
   const V* __restrict__ uin = a.u_in + sbase;
   const V* __restrict__ bb = a.b + sbase;
   V* __restrict__ uout = a.u_out + sbase;
@@ -219,13 +247,13 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
     // u rows of step t: storage rows [k0, k0+CHUNK) clipped to [0, n], cols [c0-hA, c0+W+hA) clipped to [0, n]
     const int k0 = base + CHUNK * t;
     const int ar_lo = max(k0, 0), ar_hi = min(min(k0 + CHUNK, r0 + H + hA), n + 1);
-    const int ac_lo = max(c0 - hA, 0), ac_hi = min(c0 + TILE_W + hA, n + 1);
+    const int ac_lo = max(c0 - hA, 0) / ALN * ALN, ac_hi = (min(c0 + TILE_W + hA, n + 1) + ALN - 1) / ALN * ALN;
     const int kb0 = base - 1 + CHUNK * t;
     const int br_lo = max(max(kb0, r0 - hB), 1), br_hi = min(min(kb0 + CHUNK, r0 + H + hB), m + 1);
-    const int bc_lo = max(c0 - hB, 1), bc_hi = min(c0 + TILE_W + hB, m + 1);
-    const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA);
+    const int bc_lo = max(c0 - hB, 1) / ALN * ALN, bc_hi = (min(c0 + TILE_W + hB, m + 1) + ALN - 1) / ALN * ALN;
+    const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA) / ALN * ALN;
     const int er_lo = max(J0, 0), er_hi = min(J0 + CB_ROWS, nc + 1);
-    const int ec_lo = max(I0, 0), ec_hi = min(I0 + CB_COLS, nc + 1);
+    const int ec_lo = max(I0, 0), ec_hi = (min(I0 + CB_COLS, nc + 1) + ALN - 1) / ALN * ALN;
     // One arrival per step and barrier phase, carrying the byte count of ALL of the step's copies (the
     // b rows of a sweep are issued later, after stage B has consumed the previous ones).
     const bool arrive = USE_A ? do_a : do_b;
@@ -240,7 +268,7 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
       if constexpr (LOADU) {
         if (ac_hi > ac_lo)
           for (int row = ar_lo + lane; row < ar_hi; row += 32)
-            tma_load_1d(RA + slot(row, ARING) * WA + (ac_lo - (c0 - hA)), uin + (int64_t)row * n + ac_lo,
+            tma_load_1d(RA + slot(row, ARING) * WA + (ac_lo - (c0 - hAs)), uin + (int64_t)row * n + ac_lo,
                         (unsigned)((ac_hi - ac_lo) * VB), &bar[t & 1]);
       }
       if constexpr (PROLONG) {
@@ -253,7 +281,7 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
     if (do_b && SWEEP) {
       if (bc_hi > bc_lo)
         for (int row = br_lo + lane; row < br_hi; row += 32)
-          tma_load_1d(Bb + (row - kb0) * WB + (bc_lo - (c0 - hB)), bb + (int64_t)row * n + bc_lo,
+          tma_load_1d(Bb + (row - kb0) * WBb + (bc_lo - (c0 - hBs)), bb + (int64_t)row * n + bc_lo,
                       (unsigned)((bc_hi - bc_lo) * VB), &bar[t & 1]);
     }
   };
@@ -266,8 +294,8 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
   __syncthreads();
 
   // b - (A + lambda I) u at an interior node (grid.cpp:69-100 order: d*u_c - W - E - S - N)
-  auto apply_res = [&](V bv, V uc, V uw, V ue, V us, V un) {
-    V acc = cmul(cf.d, uc);
+  auto apply_res = [&](D2 bv, D2 uc, D2 uw, D2 ue, D2 us, D2 un) {
+    D2 acc = cmul(cf.d, uc);
     acc = csub(acc, uw);
     acc = csub(acc, ue);
     acc = csub(acc, us);
@@ -288,34 +316,35 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
     // ---------------- stage A: u_in = [u] + P e_c (in place on the landed rows) -----------------
     if constexpr (PROLONG) {  // u += prolong_bilinear(e_c) (grid.cpp:123-153, multigrid.cpp:75)
       const int k0 = base + CHUNK * t;
-      const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA);
+      const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA) / ALN * ALN;
       const int rhi = min(k0 + CHUNK, r0 + H + hA);
       for (int q = tid; q < CHUNK * WA; q += NTHREADS) {
         const int lr = q / WA, lc = q - lr * WA;
-        const int row = k0 + lr, col = c0 - hA + lc;
+        const int row = k0 + lr, col = c0 - hAs + lc;
         if (row >= rhi) break;
         V* slotp = RA + slot(row, ARING) * WA + lc;
-        V v = cz<V>();
+        D2 v = cz<D2>();
         if (row_in(row) && (unsigned)(col - 1) < (unsigned)m) {
           const V* e0 = CB + (floordiv2(row) - J0) * CB_COLS + (floordiv2(col) - I0);
-          V p;
+          D2 p;
           if (!(col & 1) && !(row & 1)) {
-            p = e0[0];
+            p = ld2(e0[0]);
           } else if ((col & 1) && !(row & 1)) {
-            p = cscale((T)0.5, cadd(e0[0], e0[1]));
+            p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[1])));
           } else if (!(col & 1) && (row & 1)) {
-            p = cscale((T)0.5, cadd(e0[0], e0[CB_COLS]));
+            p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[CB_COLS])));
           } else {
-            p = cscale((T)0.25, cadd(cadd(cadd(e0[0], e0[1]), e0[CB_COLS]), e0[CB_COLS + 1]));
+            p = cscale(0.25, cadd(cadd(cadd(ld2(e0[0]), ld2(e0[1])), ld2(e0[CB_COLS])), ld2(e0[CB_COLS + 1])));
           }
           v = p;
-          if constexpr (LOADU) v = cadd(*slotp, p);
+          if constexpr (LOADU) v = cadd(ld2(*slotp), p);
         }
-        *slotp = v;  // non-interior nodes become exact zeros (the ghost ring the stencil reads)
+        const V vs = st2<V>(v);
+        *slotp = vs;  // non-interior nodes become exact zeros (the ghost ring the stencil reads)
         if constexpr (!SWEEP && STORE) {
           if (row >= r0 && row < r0 + H && row_in(row) && col >= c0 && col < c0 + TILE_W &&
               (unsigned)(col - 1) < (unsigned)m)
-            uout[(int64_t)row * n + col] = v;
+            uout[(int64_t)row * n + col] = vs;
         }
       }
       __syncthreads();
@@ -328,25 +357,26 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
         const int kb = base - 1 + CHUNK * t + RPT * g, col = c0 - hB + ci;
         const bool cin = (unsigned)(col - 1) < (unsigned)m;
         int sa = slot(kb - 1, ARING), sb = slot(kb, RR);
-        const V* ap = RA + ci + 1;  // local col of `col` in the A ring
-        V* bp = RB + ci;
-        V am, ac, an;
+        const V* ap = RA + ci + (hAs - hB);  // local col of `col` in the A ring
+        const V* bbp = Bb + ci + (hBs - hB);  // ... and in the b buffer
+        D2* bp = RB + ci;
+        D2 am, ac, an;
         if constexpr (USE_A) {
-          am = ap[sa * WA];
+          am = ld2(ap[sa * WA]);
           sa = sa + 1 == ARING ? 0 : sa + 1;
-          ac = ap[sa * WA];
+          ac = ld2(ap[sa * WA]);
         }
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           const int row = kb + i;
           const int sn = sa + 1 == ARING ? 0 : sa + 1;
-          if constexpr (USE_A) an = ap[sn * WA];
+          if constexpr (USE_A) an = ld2(ap[sn * WA]);
           if (row >= r0 - hB && row < r0 + H + hB) {
-            V r = cz<V>();
+            D2 r = cz<D2>();
             if (cin && row_in(row)) {
-              const V bv = Bb[(RPT * g + i) * WB + ci];
+              const D2 bv = ld2(bbp[(RPT * g + i) * WBb]);
               if constexpr (USE_A) {
-                r = apply_res(bv, ac, ap[sa * WA - 1], ap[sa * WA + 1], am, an);
+                r = apply_res(bv, ac, ld2(ap[sa * WA - 1]), ld2(ap[sa * WA + 1]), am, an);
               } else {
                 r = bv;  // zero initial guess: r = b
               }
@@ -366,10 +396,10 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
         const int kc = base - 2 + CHUNK * t + RPT * g, col = c0 - hC + ci;
         const bool cin = (unsigned)(col - 1) < (unsigned)m;
         const bool cout = cin && col >= c0 && col < c0 + TILE_W;
-        const V* rpc = RB + (ci + (hB - hC));  // local col of `col` in the r ring
+        const D2* rpc = RB + (ci + (hB - hC));  // local col of `col` in the r ring
         int s = slot(kc - 1, RR);
         // rolling 3-row window over the column: r and the horizontal pair sum r(col-1)+r(col+1)
-        V rm, rc, rn, sm_, sc, sn_;
+        D2 rm, rc, rn, sm_, sc, sn_;
         rm = rpc[s * WB];
         if constexpr (!JACOBI) sm_ = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
         s = s + 1 == RR ? 0 : s + 1;
@@ -384,24 +414,28 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
           rn = rpc[s * WB];
           if constexpr (!JACOBI) sn_ = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
           if (row >= r0 - hC && row < r0 + H + hC) {
-            V dl = cz<V>();
+            D2 dl = cz<D2>();
             if (cin && row_in(row)) {
               if constexpr (JACOBI) {
                 dl = cmul(cf.k0, rc);
               } else {  // (h^2/4)[c,2b,c;2b,4a,2b;c,2b,c] r with omega folded in (smoother.cpp:31-40)
-                const V e1 = cadd(cadd(sc, rm), rn);
-                const V e2 = cadd(sm_, sn_);
+                const D2 e1 = cadd(cadd(sc, rm), rn);
+                const D2 e2 = cadd(sm_, sn_);
                 dl = cadd(cadd(cmul(cf.k0, rc), cmul(cf.k1, e1)), cmul(cf.k2, e2));
               }
             }
-            if constexpr (HASD) RC[sd * WC + ci] = dl;
             if constexpr (STORE) {
-              if (cout && row >= r0 && row < r0 + H && row_in(row)) {
-                V uo = dl;
-                if constexpr (USE_A) uo = cadd(RA[sa * WA + ci + (hA - hC)], dl);
-                *outp = uo;
+              D2 ui = cz<D2>();
+              if constexpr (USE_A) ui = ld2(RA[sa * WA + ci + (hAs - hC)]);
+              const V us = st2<V>(cadd(ui, dl));
+              if (cout && row >= r0 && row < r0 + H && row_in(row)) *outp = us;
+              // with fp32 storage, continue with the correction the stored iterate actually received, so
+              // the residual formed next is that of the stored u (exact: a difference of two floats)
+              if constexpr (SH::EVEN) {
+                if (cin && row_in(row)) dl = csub(ld2(us), ui);
               }
             }
+            if constexpr (HASD) RC[sd * WC + ci] = dl;
           }
           rm = rc, sm_ = sc, rc = rn, sc = sn_;
           sa = sa + 1 == ARING ? 0 : sa + 1;
@@ -417,20 +451,23 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
     if constexpr (POST == POST_NORM || POST == POST_RESID || POST == POST_RESTRICT) {
       constexpr int WU = SWEEP ? WC : WA;  // width of the ring holding u_out (or delta)
       constexpr int NRU = SWEEP ? RR : ARING;
-      const V* U = SWEEP ? RC : RA;
-      constexpr int hU = SWEEP ? hC : hA;
+      using UT = typename std::conditional<SWEEP, D2, V>::type;
+      const UT* U;
+      if constexpr (SWEEP) U = RC;
+      else U = RA;
+      constexpr int hU = SWEEP ? hC : hAs;
       // r2 down one column over rows [k, k+nr): rolls a 3-row window of U
       auto r2_column = [&](int k, int col, int nr, auto&& consume) {
         const int lc = col - (c0 - hU);
-        const V* up = U + lc;
+        const UT* up = U + lc;
         int s = slot(k - 1, NRU);
         int srb = slot(k, RR);
         const bool cin = (unsigned)(col - 1) < (unsigned)m;
-        V um = cz<V>(), uc = cz<V>(), un = cz<V>();
+        D2 um = cz<D2>(), uc = cz<D2>(), un = cz<D2>();
         if constexpr (USE_A || SWEEP) {
-          um = up[s * WU];
+          um = ld2(up[s * WU]);
           s = s + 1 == NRU ? 0 : s + 1;
-          uc = up[s * WU];
+          uc = ld2(up[s * WU]);
         }
         const V* bg = bb + (int64_t)k * n + col;
 #pragma unroll
@@ -438,13 +475,13 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
           if (i >= nr) break;
           const int row = k + i;
           const int sn = s + 1 == NRU ? 0 : s + 1;
-          if constexpr (USE_A || SWEEP) un = up[sn * WU];
-          V r2 = cz<V>();
+          if constexpr (USE_A || SWEEP) un = ld2(up[sn * WU]);
+          D2 r2 = cz<D2>();
           if (cin && row_in(row)) {
-            V rb;
+            D2 rb;
             if constexpr (SWEEP) rb = RB[srb * WB + (col - (c0 - hB))];
-            else rb = bg[0];
-            if constexpr (USE_A || SWEEP) r2 = apply_res(rb, uc, up[s * WU - 1], up[s * WU + 1], um, un);
+            else rb = ld2(bg[0]);
+            if constexpr (USE_A || SWEEP) r2 = apply_res(rb, uc, ld2(up[s * WU - 1]), ld2(up[s * WU + 1]), um, un);
             else r2 = rb;
           }
           consume(i, row, r2);
@@ -459,10 +496,10 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
           const int g = tid / TILE_W, ci = tid - g * TILE_W;
           const int kd = base - xD + CHUNK * t + RPT * g, col = c0 + ci;
           if (col <= m) {
-            r2_column(kd, col, RPT, [&](int, int row, V r2) {
+            r2_column(kd, col, RPT, [&](int, int row, D2 r2) {
               if (row >= r0 && row < r0 + H && row_in(row) && col >= 1) {
-                if constexpr (POST == POST_NORM) nacc += (double)r2.x * (double)r2.x + (double)r2.y * (double)r2.y;
-                if constexpr (POST == POST_RESID) uout[(int64_t)row * n + col] = r2;
+                if constexpr (POST == POST_NORM) nacc += r2.x * r2.x + r2.y * r2.y;
+                if constexpr (POST == POST_RESID) uout[(int64_t)row * n + col] = st2<V>(r2);
               }
             });
           }
@@ -484,10 +521,10 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
           if (2 * g < nj) {
             const int col = c0 - 1 + f;
             const int nr = 2 * g + 1 < nj ? 5 : 3;
-            V acc_a = cz<V>(), acc_b = cz<V>();
-            r2_column(2 * Ja - 1, col, nr, [&](int i, int, V r2) {
-              if (i <= 2) acc_a = cadd(acc_a, i == 1 ? cscale((T)2, r2) : r2);
-              if (i >= 2) acc_b = cadd(acc_b, i == 3 ? cscale((T)2, r2) : r2);
+            D2 acc_a = cz<D2>(), acc_b = cz<D2>();
+            r2_column(2 * Ja - 1, col, nr, [&](int i, int, D2 r2) {
+              if (i <= 2) acc_a = cadd(acc_a, i == 1 ? cscale(2.0, r2) : r2);
+              if (i >= 2) acc_b = cadd(acc_b, i == 3 ? cscale(2.0, r2) : r2);
             });
             VX[(2 * g) * VX_W + f] = acc_a;
             VX[(2 * g + 1) * VX_W + f] = acc_b;
@@ -500,9 +537,9 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
           const int jr = tid / (TILE_W / 2), il = tid - jr * (TILE_W / 2);
           const int I = (c0 >> 1) + il, J = jlo + jr;
           if (I >= 1 && I <= mc) {
-            const V* v = VX + jr * VX_W + 2 * il;  // fine col 2I - 1 is local f = 2*il
-            const V s = cadd(cadd(v[0], cscale((T)2, v[1])), v[2]);
-            bco[(int64_t)J * nc + I] = cscale((T)(1.0 / 16.0), s);
+            const D2* v = VX + jr * VX_W + 2 * il;  // fine col 2I - 1 is local f = 2*il
+            const D2 s = cadd(cadd(v[0], cscale(2.0, v[1])), v[2]);
+            bco[(int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, s));
           }
         }
       }
@@ -589,44 +626,42 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int ntiles, i
 // dense.cpp:90-100): one CTA per shift, one thread per unknown, A^{-1} precomputed in fp64 on the host.
 template <class T>
 __global__ void k_coarse_solve(const typename vec2<T>::type* __restrict__ b, typename vec2<T>::type* __restrict__ u,
-                               const typename vec2<T>::type* __restrict__ ainv, const int* __restrict__ active,
-                               int n, int64_t ss) {
-  using V = typename vec2<T>::type;
+                               const double2* __restrict__ ainv, const int* __restrict__ active, int n, int64_t ss) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* sb = reinterpret_cast<V*>(smem_raw);
+  double2* sb = reinterpret_cast<double2*>(smem_raw);
   const int s = blockIdx.x;
   if (active != nullptr && active[s] == 0) return;
   const int m = n - 1, N = m * m;
-  const V* bs = b + (int64_t)s * ss;
-  for (int q = threadIdx.x; q < N; q += blockDim.x) sb[q] = bs[(int64_t)(q / m + 1) * n + (q % m + 1)];
+  const typename vec2<T>::type* bs = b + (int64_t)s * ss;
+  for (int q = threadIdx.x; q < N; q += blockDim.x) sb[q] = ld2(bs[(int64_t)(q / m + 1) * n + (q % m + 1)]);
   __syncthreads();
-  const V* A = ainv + (int64_t)s * N * N;
-  V* us = u + (int64_t)s * ss;
+  const double2* A = ainv + (int64_t)s * N * N;
+  typename vec2<T>::type* us = u + (int64_t)s * ss;
   for (int r = threadIdx.x; r < N; r += blockDim.x) {
-    V acc = cz<V>();
+    double2 acc = cz<double2>();
     for (int c = 0; c < N; ++c) acc = cadd(acc, cmul(A[(int64_t)r * N + c], sb[c]));
-    us[(int64_t)(r / m + 1) * n + (r % m + 1)] = acc;
+    us[(int64_t)(r / m + 1) * n + (r % m + 1)] = st2<typename vec2<T>::type>(acc);
   }
 }
 
-// Compact (reference layout, [S][m][m]) <-> ghosted level storage.
+// Compact complex128 (reference layout, [S][m][m]) <-> ghosted level storage of type T.
 template <class T>
-__global__ void k_unpack(const typename vec2<T>::type* __restrict__ src, typename vec2<T>::type* __restrict__ dst,
-                         int n, int64_t ss, int64_t total) {
+__global__ void k_unpack(const double2* __restrict__ src, typename vec2<T>::type* __restrict__ dst, int n, int64_t ss,
+                         int64_t total) {
   const int m = n - 1;
   const int64_t N = (int64_t)m * m;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = q / N, p = q % N;
     const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
-    dst[s * ss + (int64_t)j * n + i] = src[q];
+    dst[s * ss + (int64_t)j * n + i] = st2<typename vec2<T>::type>(src[q]);
   }
 }
 
 // Gather u out of the double buffer each shift finished in: sel = parity[iterations[s]].
 template <class T>
 __global__ void k_pack(const typename vec2<T>::type* __restrict__ buf0, const typename vec2<T>::type* __restrict__ buf1,
-                       const int* __restrict__ iters, const int* __restrict__ parity, typename vec2<T>::type* __restrict__ dst,
-                       int n, int64_t ss, int64_t total) {
+                       const int* __restrict__ iters, const int* __restrict__ parity, double2* __restrict__ dst, int n,
+                       int64_t ss, int64_t total) {
   const int m = n - 1;
   const int64_t N = (int64_t)m * m;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
@@ -634,7 +669,7 @@ __global__ void k_pack(const typename vec2<T>::type* __restrict__ buf0, const ty
     const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
     const int sel = (iters == nullptr) ? 0 : parity[iters[s]];
     const typename vec2<T>::type* src = sel ? buf1 : buf0;
-    dst[q] = src[s * ss + (int64_t)j * n + i];
+    dst[q] = ld2(src[s * ss + (int64_t)j * n + i]);
   }
 }
 
@@ -788,7 +823,7 @@ struct SmallLevel {
   V* u;   // u (level 0: the iterate; coarser: the correction e)
   V* r;   // residual scratch
   V* b;   // rhs (level 0: user rhs; coarser: restricted residual)
-  const LevelCoef<T>* coef;
+  const LevelCoef* coef;
   int n;
   int64_t ss;
 };
@@ -799,7 +834,7 @@ struct SmallArgs {
   int L;
   int nu1, nu2, gamma, jacobi, max_iter;
   double tol;
-  const typename vec2<T>::type* ainv;  // [S][N][N] coarsest inverse
+  const double2* ainv;  // [S][N][N] coarsest inverse (fp64)
   int coarse_N;
   int* iterations;
   int* converged;
@@ -813,17 +848,17 @@ struct SmallSolver {
   using V = typename vec2<T>::type;
   const SmallArgs<T>& a;
   int s;
-  double* red;  // [32] block reduction scratch (shared)
-  V* cb;        // coarsest rhs staging (shared, coarse_N)
+  double* red;  // [33] block reduction scratch (shared)
+  double2* cb;  // coarsest rhs staging (shared, coarse_N)
 
   __device__ __forceinline__ V* ptr(V* base, int l) const { return base + (int64_t)s * a.lv[l].ss; }
-  __device__ __forceinline__ LevelCoef<T> coef(int l) const { return a.lv[l].coef[s]; }
+  __device__ __forceinline__ LevelCoef coef(int l) const { return a.lv[l].coef[s]; }
 
   // r = b - (A + lambda I) u on level l (grid.cpp:69-100); returns the block-reduced ||r||^2 if wanted
   __device__ double residual(int l, bool zero_u, bool want_norm) const {
     const SmallLevel<T>& L = a.lv[l];
     const int n = L.n, m = n - 1;
-    const LevelCoef<T> cf = coef(l);
+    const LevelCoef cf = coef(l);
     const V* u = ptr(L.u, l);
     const V* b = ptr(L.b, l);
     V* r = ptr(L.r, l);
@@ -831,17 +866,17 @@ struct SmallSolver {
     for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
       const int j = q / m + 1, i = q - (j - 1) * m + 1;
       const int64_t p = (int64_t)j * n + i;
-      V rv = b[p];
+      double2 rv = ld2(b[p]);
       if (!zero_u) {
-        V acc = cmul(cf.d, u[p]);
-        acc = csub(acc, u[p - 1]);
-        acc = csub(acc, u[p + 1]);
-        acc = csub(acc, u[p - n]);
-        acc = csub(acc, u[p + n]);
+        double2 acc = cmul(cf.d, ld2(u[p]));
+        acc = csub(acc, ld2(u[p - 1]));
+        acc = csub(acc, ld2(u[p + 1]));
+        acc = csub(acc, ld2(u[p - n]));
+        acc = csub(acc, ld2(u[p + n]));
         rv = csub(rv, cscale(cf.inv_h2, acc));
       }
-      r[p] = rv;
-      if (want_norm) acc2 += (double)rv.x * (double)rv.x + (double)rv.y * (double)rv.y;
+      r[p] = st2<V>(rv);
+      if (want_norm) acc2 += rv.x * rv.x + rv.y * rv.y;
     }
     __syncthreads();
     if (!want_norm) return 0.0;
@@ -864,21 +899,22 @@ struct SmallSolver {
   __device__ void correct(int l, bool zero_u) const {
     const SmallLevel<T>& L = a.lv[l];
     const int n = L.n, m = n - 1;
-    const LevelCoef<T> cf = coef(l);
+    const LevelCoef cf = coef(l);
     V* u = ptr(L.u, l);
     const V* r = ptr(L.r, l);
     for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
       const int j = q / m + 1, i = q - (j - 1) * m + 1;
       const int64_t p = (int64_t)j * n + i;
-      V dl;
+      double2 dl;
       if (a.jacobi) {
-        dl = cmul(cf.k0, r[p]);
+        dl = cmul(cf.k0, ld2(r[p]));
       } else {
-        const V e1 = cadd(cadd(cadd(r[p - n], r[p - 1]), r[p + 1]), r[p + n]);
-        const V e2 = cadd(cadd(cadd(r[p - n - 1], r[p - n + 1]), r[p + n - 1]), r[p + n + 1]);
-        dl = cadd(cadd(cmul(cf.k0, r[p]), cmul(cf.k1, e1)), cmul(cf.k2, e2));
+        const double2 e1 = cadd(cadd(cadd(ld2(r[p - n]), ld2(r[p - 1])), ld2(r[p + 1])), ld2(r[p + n]));
+        const double2 e2 =
+            cadd(cadd(cadd(ld2(r[p - n - 1]), ld2(r[p - n + 1])), ld2(r[p + n - 1])), ld2(r[p + n + 1]));
+        dl = cadd(cadd(cmul(cf.k0, ld2(r[p])), cmul(cf.k1, e1)), cmul(cf.k2, e2));
       }
-      u[p] = zero_u ? dl : cadd(u[p], dl);
+      u[p] = st2<V>(zero_u ? dl : cadd(ld2(u[p]), dl));
     }
     __syncthreads();
   }
@@ -893,16 +929,16 @@ struct SmallSolver {
     for (int q = threadIdx.x; q < mc * mc; q += blockDim.x) {
       const int J = q / mc + 1, I = q - (J - 1) * mc + 1;
       const int64_t c = (int64_t)(2 * J) * nf + 2 * I;
-      V sum = r[c - nf - 1];
-      sum = cadd(sum, cscale((T)2, r[c - nf]));
-      sum = cadd(sum, r[c - nf + 1]);
-      sum = cadd(sum, cscale((T)2, r[c - 1]));
-      sum = cadd(sum, cscale((T)4, r[c]));
-      sum = cadd(sum, cscale((T)2, r[c + 1]));
-      sum = cadd(sum, r[c + nf - 1]);
-      sum = cadd(sum, cscale((T)2, r[c + nf]));
-      sum = cadd(sum, r[c + nf + 1]);
-      bc[(int64_t)J * nc + I] = cscale((T)(1.0 / 16.0), sum);
+      double2 sum = ld2(r[c - nf - 1]);
+      sum = cadd(sum, cscale(2.0, ld2(r[c - nf])));
+      sum = cadd(sum, ld2(r[c - nf + 1]));
+      sum = cadd(sum, cscale(2.0, ld2(r[c - 1])));
+      sum = cadd(sum, cscale(4.0, ld2(r[c])));
+      sum = cadd(sum, cscale(2.0, ld2(r[c + 1])));
+      sum = cadd(sum, ld2(r[c + nf - 1]));
+      sum = cadd(sum, cscale(2.0, ld2(r[c + nf])));
+      sum = cadd(sum, ld2(r[c + nf + 1]));
+      bc[(int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, sum));
     }
     __syncthreads();
   }
@@ -917,13 +953,13 @@ struct SmallSolver {
     for (int q = threadIdx.x; q < mf * mf; q += blockDim.x) {
       const int j = q / mf + 1, i = q - (j - 1) * mf + 1;
       const V* e0 = e + (int64_t)(j >> 1) * nc + (i >> 1);
-      V pv;
-      if (!(i & 1) && !(j & 1)) pv = e0[0];
-      else if ((i & 1) && !(j & 1)) pv = cscale((T)0.5, cadd(e0[0], e0[1]));
-      else if (!(i & 1) && (j & 1)) pv = cscale((T)0.5, cadd(e0[0], e0[nc]));
-      else pv = cscale((T)0.25, cadd(cadd(cadd(e0[0], e0[1]), e0[nc]), e0[nc + 1]));
+      double2 pv;
+      if (!(i & 1) && !(j & 1)) pv = ld2(e0[0]);
+      else if ((i & 1) && !(j & 1)) pv = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[1])));
+      else if (!(i & 1) && (j & 1)) pv = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[nc])));
+      else pv = cscale(0.25, cadd(cadd(cadd(ld2(e0[0]), ld2(e0[1])), ld2(e0[nc])), ld2(e0[nc + 1])));
       const int64_t p = (int64_t)j * nf + i;
-      u[p] = zero_u ? pv : cadd(u[p], pv);
+      u[p] = st2<V>(zero_u ? pv : cadd(ld2(u[p]), pv));
     }
     __syncthreads();
   }
@@ -933,13 +969,13 @@ struct SmallSolver {
     const int n = L.n, m = n - 1, N = a.coarse_N;
     const V* b = ptr(L.b, l);
     V* u = ptr(L.u, l);
-    for (int q = threadIdx.x; q < N; q += blockDim.x) cb[q] = b[(int64_t)(q / m + 1) * n + (q % m + 1)];
+    for (int q = threadIdx.x; q < N; q += blockDim.x) cb[q] = ld2(b[(int64_t)(q / m + 1) * n + (q % m + 1)]);
     __syncthreads();
-    const V* A = a.ainv + (int64_t)s * N * N;
+    const double2* A = a.ainv + (int64_t)s * N * N;
     for (int rr = threadIdx.x; rr < N; rr += blockDim.x) {
-      V acc = cz<V>();
+      double2 acc = cz<double2>();
       for (int c = 0; c < N; ++c) acc = cadd(acc, cmul(A[(int64_t)rr * N + c], cb[c]));
-      u[(int64_t)(rr / m + 1) * n + (rr % m + 1)] = acc;
+      u[(int64_t)(rr / m + 1) * n + (rr % m + 1)] = st2<V>(acc);
     }
     __syncthreads();
   }
@@ -995,7 +1031,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
   using V = typename vec2<T>::type;
   __shared__ double red[33];
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SmallSolver<T> S{a, (int)blockIdx.x, red, reinterpret_cast<V*>(smem_raw)};
+  SmallSolver<T> S{a, (int)blockIdx.x, red, reinterpret_cast<double2*>(smem_raw)};
   const int s = blockIdx.x;
   const int H = a.max_iter + 1;
   // u = 0 (multigrid.cpp:90), r0 = ||b|| (:91)
@@ -1010,7 +1046,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
     const SmallLevel<T>& L0 = a.lv[0];
     V* u = S.ptr(L0.u, 0);
     const int n = L0.n, m = n - 1;
-    for (int q = threadIdx.x; q < m * m; q += blockDim.x) u[(int64_t)(q / m + 1) * n + (q % m + 1)] = cz<V>();
+    for (int q = threadIdx.x; q < m * m; q += blockDim.x) u[(int64_t)(q / m + 1) * n + (q % m + 1)] = st2<V>(cz<double2>());
     __syncthreads();
   }
   if (r0 == 0.0 || a.tol >= 1.0) return;

@@ -174,16 +174,22 @@ class BatchedMultigridHierarchy:
     (multigrid.cpp:24-61) for every shift, before touching the device.
     """
 
-    def __init__(self, fine: Grid2D, shifts: Sequence[Shift | complex], cfg: MultigridConfig, device: int = 0):
+    def __init__(self, fine: Grid2D, shifts: Sequence[Shift | complex], cfg: MultigridConfig, device: int = 0,
+                 precision: str = "c128"):
+        """precision: "c128" (the reference's std::complex<double>) or "c64" (fp32 storage, fp64 arithmetic;
+        host arrays stay complex128)."""
         if isinstance(fine, int):
             fine = Grid2D(fine)
+        if precision not in ("c128", "c64"):
+            raise ConfigError(f"unknown precision {precision!r}")
+        self.precision = precision
         self.grid = fine
         self.cfg = cfg
         self.shifts = [s if isinstance(s, Shift) else Shift(complex(s), i) for i, s in enumerate(shifts)]
         self.device = device
         lam = np.array([complex(s.lam) for s in self.shifts], dtype=np.complex128)
         self._lam = lam
-        desc = N.BatchDesc(fine.n, len(lam), lam.ctypes.data, cfg._c(), 0, device)
+        desc = N.BatchDesc(fine.n, len(lam), lam.ctypes.data, cfg._c(), 0 if precision == "c128" else 1, device)
         h = C.c_void_p()
         _check(N.lib().pdmg_create(C.byref(desc), C.byref(h)))
         self._h = h
