@@ -37,6 +37,8 @@ CONFIGS = {
            "C3: n=512 (511x511), 256 shifts (alpha=1e-3, dt=1/256), V(2,2), seed 2"),
     "c4a": (1024, 1024, 0.01, 1024, 1 / 1024, 3, 1, 1,
             "C4 set A: n=1024 (1023x1023), 1024 shifts (alpha=0.01, dt=1/1024), V(1,1), seed 3"),
+    "c4b": (1024, 1024, 0.01, 1024, 2.0 ** -20, 3, 1, 1,
+            "C4 set B: n=1024 (1023x1023), 1024 shifts (alpha=0.01, dt=h^2), V(1,1), seed 3"),
     "c5": (256, 256, 0.01, 256, 1 / 256, 4, 1, 1,
            "C5: ParaDIAG backward-Euler heat step, n=256 (255x255), nt=256 (T=1), alpha=0.01, V(1,1), "
            "IC sin(pi x)sin(pi y)+U[-0.1,0.1] seed 4; time DFT + 256 shifted solves + inverse DFT + residual"),
@@ -54,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shifts", type=int, default=0, help="override the number of shifts (0 = config's)")
+    ap.add_argument("--precision", default="c128", choices=["c128", "c64"],
+                    help="c64: fp32 storage / fp64 arithmetic, tol 1e-5 (BASELINE config 4)")
     return ap.parse_args()
 
 
@@ -293,12 +297,13 @@ def main():
     j0 = 3 if args.config == "c1" else 0  # BASELINE config 1 is slot j = 3 of the n_t = 32 family
     lams_all = P.circulant_shifts(alpha, nt, dt, j0, S)
     lams = lams_all[b0:b1]
-    cfg = P.MultigridConfig(P.CycleKind.V, nu1, nu2, 4, 1e-10, 200, P.SmootherConfig.vanka())
+    tol = 1e-5 if args.precision == "c64" else 1e-10
+    cfg = P.MultigridConfig(P.CycleKind.V, nu1, nu2, 4, tol, 200, P.SmootherConfig.vanka())
     # inputs: one mt19937(seed) stream, shift-major; each rank keeps its shard
     b_all = P.random_rhs(n, seed, count=b1)
     b_host = np.ascontiguousarray(b_all.reshape(b1, m, m)[b0:b1])
     del b_all
-    H = P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg, device=local)
+    H = P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg, device=local, precision=args.precision)
     stream = torch.cuda.ExternalStream(H.stream)
     d_b = torch.from_numpy(b_host.view(np.float64)).to(f"cuda:{local}")
     d_u = torch.empty_like(d_b)
@@ -426,8 +431,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": desc + (f" [{S} shifts]" if args.shifts else ""), "shifts": S,
+                       "precision": args.precision + (" (fp32 storage, fp64 arithmetic), tol 1e-5"
+                                                      if args.precision == "c64" else ", tol 1e-10"),
                        "shifts_per_rank": Sr, "parallelism": f"shift-sharded x{world}",
                        "l2": "inputs larger than L2 (each fine array %.2f GB)" % (S * (n + 1) * n * 16 / 1e9)
                        if S * (n + 1) * n * 16 > 126e6 else "working set fits in L2 (latency-bound config)"},
