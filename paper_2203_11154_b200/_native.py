@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libpdmg_b200.so")
+LIB_PATH = os.environ.get("PDMG_B200_LIB") or os.path.join(PKG_DIR, "libpdmg_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "pdmg_b200.h")
 
 PDMG_OK, PDMG_ERR_CONFIG, PDMG_ERR_SINGULAR, PDMG_ERR_RUNTIME = 0, 1, 2, 3

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -272,6 +273,33 @@ struct KernelTable {
   }
 };
 
+template <class T>
+struct MarchTable {
+  void (*e[32])(MarchArgs<T>) = {};
+  static int key(bool lu, bool pr, int post, bool ja) { return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (ja ? 16 : 0); }
+  template <bool LU, bool PR, int PO, bool JA>
+  void reg() {
+    e[key(LU, PR, PO, JA)] = &k_march<T, LU, PR, PO, JA>;
+  }
+  template <int PO, bool JA>
+  void reg4() {
+    reg<false, false, PO, JA>();
+    reg<true, false, PO, JA>();
+    if constexpr (PO != POST_RESTRICT) {
+      reg<false, true, PO, JA>();
+      reg<true, true, PO, JA>();
+    }
+  }
+  MarchTable() {
+    reg4<POST_NONE, false>();
+    reg4<POST_NONE, true>();
+    reg4<POST_NORM, false>();
+    reg4<POST_NORM, true>();
+    reg4<POST_RESTRICT, false>();
+    reg4<POST_RESTRICT, true>();
+  }
+};
+
 // ---------------------------------------------------------------------------------------------
 // Engine: one batch of shifts on one device.
 // ---------------------------------------------------------------------------------------------
@@ -328,6 +356,7 @@ struct Engine : EngineBase {
   std::vector<Level> lv;
   double2* d_ainv = nullptr;
   int coarse_N = 0;
+  int last_partials = 0;  // partial sums written by the last level pass (tiles or warp tasks per shift)
   int *d_active = nullptr, *d_iters = nullptr, *d_conv = nullptr, *d_nactive = nullptr, *d_parity = nullptr;
   int* d_ones = nullptr;
   double *d_r0 = nullptr, *d_hist = nullptr, *d_partial = nullptr, *d_norms = nullptr;
@@ -344,6 +373,27 @@ struct Engine : EngineBase {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  int march_min_n = 64;  // levels with n >= this use the warp-marching sweep kernel (0 = never)
+  int march_hs = 0;       // strip height override (0 = automatic)
+
+  static const MarchTable<T>& marches() {
+    static MarchTable<T> t;
+    return t;
+  }
+  // measured on B200 (C3, C4): the marcher wins for sweep+norm (the last fine post-sweep), the ring kernel
+  // for the other variants; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher (experiments)
+  bool march_all = false;
+  bool use_march(int l, const Variant& v) const {
+    return march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store &&
+           ((v.post == POST_NORM && !v.prolong) || (march_all && v.post != POST_RESID));
+  }
+  int march_hs_for(int n) const { return march_hs > 0 ? march_hs : (n >= 512 ? 128 : 64); }
+  int march_tasks(int l, int post) const {
+    const int hA = (post == POST_RESTRICT ? 1 : post == POST_NONE ? -1 : 0) + 3;
+    const int wout = 64 - 2 * hA, n = lv[l].n, hs = march_hs_for(n);
+    return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
+  }
+
   bool use_small_path() const {
     if (solve_path == 1) return false;
     if (solve_path == 2) return true;
@@ -412,6 +462,9 @@ struct Engine : EngineBase {
 
   void setup_device(int dev) override {
     device = dev;
+    if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (dev < 0 || dev >= ndev) throw CudaError("pdmg_create: CUDA device " + std::to_string(dev) + " not available");
@@ -454,6 +507,7 @@ struct Engine : EngineBase {
         }
         LevelCoef& c = hc[s];
         c.d = make_double2(dd.real(), dd.imag());
+        c.dd = make_double2(dd.real() / (h * h), dd.imag() / (h * h));
         c.k0 = make_double2(k0.real(), k0.imag());
         c.k1 = make_double2(k1.real(), k1.imag());
         c.k2 = make_double2(k2.real(), k2.imag());
@@ -480,7 +534,10 @@ struct Engine : EngineBase {
     CK(cudaMemcpyAsync(d_ainv, hinv.data(), sizeof(double2) * hinv.size(), cudaMemcpyHostToDevice, stream));
     // solve state
     int maxtiles = 1;
-    for (auto& Lv : lv) maxtiles = std::max(maxtiles, Lv.ntiles);
+    for (size_t l = 0; l < lv.size(); ++l) {
+      maxtiles = std::max(maxtiles, lv[l].ntiles);
+      for (int post : {POST_NONE, POST_NORM, POST_RESTRICT}) maxtiles = std::max(maxtiles, march_tasks((int)l, post));
+    }
     CK(cudaMalloc(&d_active, sizeof(int) * S));
     CK(cudaMalloc(&d_iters, sizeof(int) * S));
     CK(cudaMalloc(&d_conv, sizeof(int) * S));
@@ -559,7 +616,6 @@ struct Engine : EngineBase {
     a.ntx = Lv.ntx;
     a.ntiles = Lv.ntiles;
     a.H = Lv.H;
-    const KernelEntry<T>& k = table->get(v);
     const double pts = (double)n_act * Lv.m * Lv.m, S_ = sizeof(V);
     double bpp = 0;  // algorithmic DRAM bytes per point
     if (v.loadu) bpp += S_;
@@ -568,8 +624,26 @@ struct Engine : EngineBase {
     if (v.store || v.post == POST_RESID) bpp += S_;
     if (v.post == POST_RESTRICT) bpp += S_ / 4;
     const std::string cls = "L" + std::to_string(l) + ":" + v.name();
+    if (use_march(l, v)) {
+      MarchArgs<T> ma{};
+      ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
+      ma.coef = Lv.coef, ma.active = active, ma.n = a.n, ma.nc = a.nc, ma.ss = a.ss, ma.ssc = a.ssc;
+      const int hA = (v.post == POST_RESTRICT ? 4 : v.post == POST_NORM ? 3 : 2);
+      const int wout = 64 - 2 * hA;
+      ma.Hs = march_hs_for(Lv.n);
+      ma.ntx = (Lv.n + wout - 1) / wout;
+      ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
+      auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi)];
+      if (!fn) throw std::logic_error("pdmg_b200: no march kernel for variant " + v.name());
+      dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
+      timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma); });
+      last_partials = ma.ntasks;
+      return;
+    }
+    const KernelEntry<T>& k = table->get(v);
     dim3 grid(Lv.ntiles, S);
     timed(cls, pts * bpp, [&] { k.fn<<<grid, NTHREADS, k.smem, stream>>>(a); });
+    last_partials = Lv.ntiles;
   }
 
   void coarse_solve(const V* b, V* u, const int* active) {
@@ -675,7 +749,7 @@ struct Engine : EngineBase {
         std::vector<double> nb(S);
         level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
                    nullptr, S);
-        finalize(0, F.ntiles);
+        finalize(0, last_partials);
         std::vector<int> act(S);
         CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
         for (int s = 0; s < S; ++s)
@@ -706,7 +780,7 @@ struct Engine : EngineBase {
     // r0 = ||b|| (multigrid.cpp:91): residual of the zero guess
     level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
                nullptr, S);
-    finalize(0, F.ntiles);
+    finalize(0, last_partials);
     std::vector<int> parity(H, 0);
     if (any_singular && n_active_host > 0) {
       std::vector<int> act(S);
@@ -722,7 +796,7 @@ struct Engine : EngineBase {
         level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr, nullptr,
                    d_active, n_act);
       parity[k] = F.cur;
-      finalize(k, F.ntiles);
+      finalize(k, last_partials);
     }
     CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
     pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
@@ -903,7 +977,7 @@ struct Engine : EngineBase {
                nullptr, S);
     const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
     timed("sum_partials", 0.0,
-          [&] { k_sum_partials<<<blocks, threads, 0, stream>>>(d_partial, Lv.ntiles, S, d_norms); });
+          [&] { k_sum_partials<<<blocks, threads, 0, stream>>>(d_partial, last_partials, S, d_norms); });
     CK(cudaMemcpyAsync(norms, d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, stream));
     finish();
   }

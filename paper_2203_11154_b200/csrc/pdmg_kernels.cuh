@@ -84,9 +84,39 @@ __device__ __forceinline__ float2 st2<float2>(double2 v) {
   return make_float2((float)v.x, (float)v.y);
 }
 
+__device__ __forceinline__ double2 csel(bool c, double2 a) { return c ? a : make_double2(0.0, 0.0); }
+// b - (1/h^2)((4+eta) u_c - (u_w + u_e + u_s + u_n)) with dd = (4+eta)/h^2 folded into FMAs
+__device__ __forceinline__ double2 res5(double2 b, double ih2, double2 dd, double2 uc, double2 uw, double2 ue,
+                                        double2 us, double2 un) {
+  const double sx = (uw.x + ue.x) + (us.x + un.x), sy = (uw.y + ue.y) + (us.y + un.y);
+  double rx = fma(ih2, sx, b.x), ry = fma(ih2, sy, b.y);
+  rx = fma(-dd.x, uc.x, rx);
+  rx = fma(dd.y, uc.y, rx);
+  ry = fma(-dd.x, uc.y, ry);
+  ry = fma(-dd.y, uc.x, ry);
+  return make_double2(rx, ry);
+}
+// k0 rc + k1 e1 + k2 e2 (complex), as one FMA chain per component
+__device__ __forceinline__ double2 cdot3(double2 k0, double2 rc, double2 k1, double2 e1, double2 k2, double2 e2) {
+  double x = k0.x * rc.x;
+  x = fma(-k0.y, rc.y, x);
+  x = fma(k1.x, e1.x, x);
+  x = fma(-k1.y, e1.y, x);
+  x = fma(k2.x, e2.x, x);
+  x = fma(-k2.y, e2.y, x);
+  double y = k0.x * rc.y;
+  y = fma(k0.y, rc.x, y);
+  y = fma(k1.x, e1.y, y);
+  y = fma(k1.y, e1.x, y);
+  y = fma(k2.x, e2.y, y);
+  y = fma(k2.y, e2.x, y);
+  return make_double2(x, y);
+}
+
 // Per (level, shift) operator coefficients, precomputed on the host in fp64 (multigrid.cpp:47-58).
 struct LevelCoef {
   double2 d;      // 4 + eta, eta = lambda h^2              (grid.cpp:73)
+  double2 dd;     // (4 + eta) / h^2
   double2 k0;     // Vanka: omega*(h^2/4)*4a ; Jacobi: omega*h^2/(4+eta)
   double2 k1;     // Vanka: omega*(h^2/4)*2b
   double2 k2;     // Vanka: omega*(h^2/4)*c
@@ -96,15 +126,21 @@ struct LevelCoef {
 
 enum : int { POST_NONE = 0, POST_NORM = 1, POST_RESTRICT = 2, POST_RESID = 3 };
 
-constexpr int TILE_W = 64;    // output columns per CTA
-constexpr int CHUNK = 16;     // rows each stage advances per step
-constexpr int RING = 18;      // rows of the r / delta rings (= CHUNK + 2: a stage reads its producer's rows -1..CHUNK)
-constexpr int RING_R = 20;    // ... when the restriction (which looks 2 more rows back) consumes them
-constexpr int ARING = 34;     // rows of the u_in ring: the 18 rows in use + the next chunk landing (TMA)
-constexpr int RPT = 4;        // rows per stencil task (register-blocked along the column)
+#ifndef PDMG_CHUNK
+#define PDMG_CHUNK 16
+#endif
+#ifndef PDMG_RPT
+#define PDMG_RPT 4
+#endif
+constexpr int TILE_W = 64;          // output columns per CTA
+constexpr int CHUNK = PDMG_CHUNK;   // rows each stage advances per step
+constexpr int RING = CHUNK + 2;     // rows of the r / delta rings (a stage reads its producer's rows -1..CHUNK)
+constexpr int RING_R = CHUNK + 4;   // ... when the restriction (which looks 2 more rows back) consumes them
+constexpr int ARING = 2 * CHUNK + 2;  // rows of the u_in ring: the rows in use + the next chunk landing (TMA)
+constexpr int RPT = PDMG_RPT;       // rows per stencil task (register-blocked along the column)
 constexpr int RGROUPS = CHUNK / RPT;
-constexpr int NTHREADS = 288; // 9 warps >= (TILE_W + 2*hB) * RGROUPS tasks for every variant
-constexpr int CB_ROWS = 10, CB_COLS = 40;  // coarse block for prolongation (CHUNK/2 + 2 rows, (TILE_W+8)/2 + 4 cols)
+constexpr int NTHREADS = 288;       // 9 warps >= (TILE_W + 2*hB) * RGROUPS tasks for every variant
+constexpr int CB_ROWS = CHUNK / 2 + 2, CB_COLS = 40;  // coarse block for prolongation
 constexpr int VX_W = TILE_W + 2;           // restriction exchange row width
 
 template <class T>
@@ -295,12 +331,7 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
 
   // b - (A + lambda I) u at an interior node (grid.cpp:69-100 order: d*u_c - W - E - S - N)
   auto apply_res = [&](D2 bv, D2 uc, D2 uw, D2 ue, D2 us, D2 un) {
-    D2 acc = cmul(cf.d, uc);
-    acc = csub(acc, uw);
-    acc = csub(acc, ue);
-    acc = csub(acc, us);
-    acc = csub(acc, un);
-    return csub(bv, cscale(cf.inv_h2, acc));
+    return res5(bv, cf.inv_h2, cf.dd, uc, uw, ue, us, un);
   };
 
   // fixed per-thread task geometry
@@ -353,12 +384,14 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
       if (t + 1 < n_iter) issue(t + 1, true, false);  // lands in ring rows no stage of step t touches
       // -------------- stage B: r = b - (A + lambda I) u_in  (grid.cpp:69-100) ---------------------
       if (tid < WB * RGROUPS) {
+        // rows outside the stage range are computed too (from stale ring rows) and written to ring slots no
+        // later stage reads; only the interior mask (Dirichlet zeros) must be exact
         const int g = tid / WB, ci = tid - g * WB;
         const int kb = base - 1 + CHUNK * t + RPT * g, col = c0 - hB + ci;
         const bool cin = (unsigned)(col - 1) < (unsigned)m;
         int sa = slot(kb - 1, ARING), sb = slot(kb, RR);
         const V* ap = RA + ci + (hAs - hB);  // local col of `col` in the A ring
-        const V* bbp = Bb + ci + (hBs - hB);  // ... and in the b buffer
+        const V* bbp = Bb + ci + (hBs - hB) + RPT * g * WBb;  // ... and in the b buffer
         D2* bp = RB + ci;
         D2 am, ac, an;
         if constexpr (USE_A) {
@@ -370,20 +403,17 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
         for (int i = 0; i < RPT; ++i) {
           const int row = kb + i;
           const int sn = sa + 1 == ARING ? 0 : sa + 1;
-          if constexpr (USE_A) an = ld2(ap[sn * WA]);
-          if (row >= r0 - hB && row < r0 + H + hB) {
-            D2 r = cz<D2>();
-            if (cin && row_in(row)) {
-              const D2 bv = ld2(bbp[(RPT * g + i) * WBb]);
-              if constexpr (USE_A) {
-                r = apply_res(bv, ac, ld2(ap[sa * WA - 1]), ld2(ap[sa * WA + 1]), am, an);
-              } else {
-                r = bv;  // zero initial guess: r = b
-              }
-            }
-            bp[sb * WB] = r;
+          const D2 bv = ld2(bbp[i * WBb]);
+          D2 r;
+          if constexpr (USE_A) {
+            an = ld2(ap[sn * WA]);
+            const V* arow = ap + sa * WA;
+            r = apply_res(bv, ac, ld2(arow[-1]), ld2(arow[1]), am, an);
+            am = ac, ac = an;
+          } else {
+            r = bv;  // zero initial guess: r = b
           }
-          if constexpr (USE_A) am = ac, ac = an;
+          bp[sb * WB] = csel(cin && row_in(row), r);
           sa = sn;
           sb = sb + 1 == RR ? 0 : sb + 1;
         }
@@ -400,43 +430,47 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
         int s = slot(kc - 1, RR);
         // rolling 3-row window over the column: r and the horizontal pair sum r(col-1)+r(col+1)
         D2 rm, rc, rn, sm_, sc, sn_;
-        rm = rpc[s * WB];
-        if constexpr (!JACOBI) sm_ = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
-        s = s + 1 == RR ? 0 : s + 1;
-        rc = rpc[s * WB];
-        if constexpr (!JACOBI) sc = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
+        {
+          const D2* q = rpc + s * WB;
+          rm = q[0];
+          if constexpr (!JACOBI) sm_ = cadd(q[-1], q[1]);
+          s = s + 1 == RR ? 0 : s + 1;
+          q = rpc + s * WB;
+          rc = q[0];
+          if constexpr (!JACOBI) sc = cadd(q[-1], q[1]);
+        }
         int sa = slot(kc, ARING), sd = slot(kc, RR);
         V* outp = uout + (int64_t)kc * n + col;
+        const int olo = max(r0, 1), ohi = min(r0 + H, m + 1);  // stored output rows
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           const int row = kc + i;
           s = s + 1 == RR ? 0 : s + 1;
-          rn = rpc[s * WB];
-          if constexpr (!JACOBI) sn_ = cadd(rpc[s * WB - 1], rpc[s * WB + 1]);
-          if (row >= r0 - hC && row < r0 + H + hC) {
-            D2 dl = cz<D2>();
-            if (cin && row_in(row)) {
-              if constexpr (JACOBI) {
-                dl = cmul(cf.k0, rc);
-              } else {  // (h^2/4)[c,2b,c;2b,4a,2b;c,2b,c] r with omega folded in (smoother.cpp:31-40)
-                const D2 e1 = cadd(cadd(sc, rm), rn);
-                const D2 e2 = cadd(sm_, sn_);
-                dl = cadd(cadd(cmul(cf.k0, rc), cmul(cf.k1, e1)), cmul(cf.k2, e2));
-              }
-            }
-            if constexpr (STORE) {
-              D2 ui = cz<D2>();
-              if constexpr (USE_A) ui = ld2(RA[sa * WA + ci + (hAs - hC)]);
-              const V us = st2<V>(cadd(ui, dl));
-              if (cout && row >= r0 && row < r0 + H && row_in(row)) *outp = us;
-              // with fp32 storage, continue with the correction the stored iterate actually received, so
-              // the residual formed next is that of the stored u (exact: a difference of two floats)
-              if constexpr (SH::EVEN) {
-                if (cin && row_in(row)) dl = csub(ld2(us), ui);
-              }
-            }
-            if constexpr (HASD) RC[sd * WC + ci] = dl;
+          {
+            const D2* q = rpc + s * WB;
+            rn = q[0];
+            if constexpr (!JACOBI) sn_ = cadd(q[-1], q[1]);
           }
+          const bool inn = cin && row_in(row);
+          D2 dl;
+          if constexpr (JACOBI) {
+            dl = cmul(cf.k0, rc);
+          } else {  // (h^2/4)[c,2b,c;2b,4a,2b;c,2b,c] r with omega folded in (smoother.cpp:31-40)
+            const D2 e1 = cadd(cadd(sc, rm), rn);
+            const D2 e2 = cadd(sm_, sn_);
+            dl = cdot3(cf.k0, rc, cf.k1, e1, cf.k2, e2);
+          }
+          dl = csel(inn, dl);
+          if constexpr (STORE) {
+            D2 ui = cz<D2>();
+            if constexpr (USE_A) ui = ld2(RA[sa * WA + ci + (hAs - hC)]);
+            const V us = st2<V>(cadd(ui, dl));
+            if (cout && row >= olo && row < ohi) *outp = us;
+            // with fp32 storage, continue with the correction the stored iterate actually received, so
+            // the residual formed next is that of the stored u (exact: a difference of two floats)
+            if constexpr (SH::EVEN) dl = csel(inn, csub(ld2(us), ui));
+          }
+          if constexpr (HASD) RC[sd * WC + ci] = dl;
           rm = rc, sm_ = sc, rc = rn, sc = sn_;
           sa = sa + 1 == ARING ? 0 : sa + 1;
           sd = sd + 1 == RR ? 0 : sd + 1;
@@ -476,14 +510,16 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
           const int row = k + i;
           const int sn = s + 1 == NRU ? 0 : s + 1;
           if constexpr (USE_A || SWEEP) un = ld2(up[sn * WU]);
-          D2 r2 = cz<D2>();
-          if (cin && row_in(row)) {
-            D2 rb;
-            if constexpr (SWEEP) rb = RB[srb * WB + (col - (c0 - hB))];
-            else rb = ld2(bg[0]);
-            if constexpr (USE_A || SWEEP) r2 = apply_res(rb, uc, ld2(up[s * WU - 1]), ld2(up[s * WU + 1]), um, un);
-            else r2 = rb;
+          const bool inn = cin && row_in(row);
+          D2 rb;
+          if constexpr (SWEEP) rb = RB[srb * WB + (col - (c0 - hB))];
+          else rb = inn ? ld2(bg[0]) : cz<D2>();
+          D2 r2 = rb;
+          if constexpr (USE_A || SWEEP) {
+            const UT* urow = up + s * WU;
+            r2 = apply_res(rb, uc, ld2(urow[-1]), ld2(urow[1]), um, un);
           }
+          r2 = csel(inn, r2);
           consume(i, row, r2);
           um = uc, uc = un;
           s = sn;
@@ -1061,6 +1097,243 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
       if (threadIdx.x == 0) a.converged[s] = 1;
       break;
     }
+  }
+}
+
+}  // namespace pdmg_b200
+
+// ===================================================================================================
+// k_march: warp-marching fused sweep for the large levels (the dominant kernels of every cycle).
+// Each warp owns a 64-column strip (2 columns per lane) of one shift, H_s rows tall, and marches down it
+// one row per step.  Every stage (u_in -> r -> delta/u_out -> r2 -> restriction or norm) keeps a 3-row
+// register window per column; horizontal neighbours come from warp shuffles (lane l holds columns
+// c0 + 2l, c0 + 2l + 1).  No shared memory and no CTA barriers: warps are independent, so latency is hidden
+// by the other warps and the loads prefetched one row ahead.  Each stage's valid columns shrink by one
+// per stage; a warp stores only its middle 64 - 2 hA columns (neighbouring strips overlap by 2 hA).
+// Stage lags: at step j the warp loads u row j, computes r at j-1, delta/u_out at j-2, r2 at j-3 and the
+// coarse row whose fine rows end at j-3.
+// ===================================================================================================
+namespace pdmg_b200 {
+
+constexpr int MARCH_WARPS = 4;  // warps per CTA (independent)
+
+__device__ __forceinline__ double2 shfl_up2(double2 v) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ double2 shfl_dn2(double2 v) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+template <class T>
+struct MarchArgs {
+  using V = typename vec2<T>::type;
+  const V* u_in;
+  V* u_out;
+  const V* b;
+  const V* ec;
+  V* bc;
+  double* partial;
+  const LevelCoef* coef;
+  const int* active;
+  int n, nc;
+  int64_t ss, ssc;
+  int ntx, ntasks, Hs;  // strips across, warp tasks per shift, strip height
+};
+
+template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI>
+__global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
+  using V = typename vec2<T>::type;
+  using D2 = double2;
+  constexpr bool EVEN = sizeof(V) == 8;
+  constexpr bool HASD = POST != POST_NONE;
+  constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
+  constexpr int hC = HASD ? hD + 1 : 0;
+  constexpr int hA = hC + 2;
+  constexpr int WOUT = 64 - 2 * hA;
+  const int shift = blockIdx.y;
+  if (a.active != nullptr && a.active[shift] == 0) return;
+  const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
+  if (task >= a.ntasks) return;
+  const int lane = threadIdx.x & 31;
+  const int tx = task % a.ntx, ty = task / a.ntx;
+  const int n = a.n, m = n - 1, Hs = a.Hs, nc = a.nc;
+  const int x0 = tx * WOUT, r0 = ty * Hs;
+  const int64_t sbase = (int64_t)shift * a.ss;
+  const V* __restrict__ uin = a.u_in + sbase;
+  const V* __restrict__ bb = a.b + sbase;
+  V* __restrict__ uout = a.u_out + sbase;
+  const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
+  const LevelCoef cf = a.coef[shift];
+
+  const int cA = x0 - hA + 2 * lane;  // storage column of this lane's first column
+  bool cin[2], cst[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int c = cA + k;
+    cin[k] = (unsigned)(c - 1) < (unsigned)m;
+    cst[k] = cin[k] && c >= x0 && c < x0 + WOUT;
+  }
+  const int rlo = r0 - hA, rhi = r0 + Hs + hA;  // rows loaded
+  const int olo = max(r0, 1), ohi = min(r0 + Hs, m + 1);
+  auto row_in = [&](int row) { return (unsigned)(row - 1) < (unsigned)m; };
+
+  // loads of one row (u_in incl. prolongation, b) for this lane's two columns
+  auto load_u = [&](int row, D2* out) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) out[k] = cz<D2>();
+    if (!row_in(row)) return;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (!cin[k]) continue;
+      const int c = cA + k;
+      D2 v = cz<D2>();
+      if constexpr (LOADU) v = ld2(uin[(int64_t)row * n + c]);
+      if constexpr (PROLONG) {  // u += prolong_bilinear(e_c) (grid.cpp:123-153)
+        const V* e0 = ecs + (int64_t)(row >> 1) * nc + (c >> 1);
+        D2 p;
+        if (!(c & 1) && !(row & 1)) p = ld2(e0[0]);
+        else if ((c & 1) && !(row & 1)) p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[1])));
+        else if (!(c & 1) && (row & 1)) p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[nc])));
+        else p = cscale(0.25, cadd(cadd(cadd(ld2(e0[0]), ld2(e0[1])), ld2(e0[nc])), ld2(e0[nc + 1])));
+        v = cadd(v, p);
+      }
+      out[k] = v;
+    }
+  };
+  auto load_b = [&](int row, D2* out) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      out[k] = (row_in(row) && cin[k]) ? ld2(bb[(int64_t)row * n + cA + k]) : cz<D2>();
+  };
+
+  // register windows: index 0 = oldest row
+  D2 U[3][2], R[3][2], S[3][2], Dl[3][2], R2[3][2];
+  D2 Bc[2], Un[2], Bn[2];
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) U[q][k] = R[q][k] = S[q][k] = Dl[q][k] = R2[q][k] = cz<D2>();
+  double nacc = 0.0;
+  load_u(rlo, Un);
+  load_b(rlo - 1, Bn);
+
+  for (int j = rlo; j < rhi; ++j) {
+    // ---- stage A: u row j (prefetched), prefetch row j+1 --------------------------------------------
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      U[0][k] = U[1][k];
+      U[1][k] = U[2][k];
+      U[2][k] = Un[k];
+      Bc[k] = Bn[k];
+    }
+    if (j + 1 < rhi) {
+      load_u(j + 1, Un);
+      load_b(j, Bn);
+    }
+    // ---- stage B: r at row j-1 = b - (A + lambda I) u  ---------------------------------------------
+    {
+      const int row = j - 1;
+      const D2 uw0 = shfl_up2(U[1][1]), ue1 = shfl_dn2(U[1][0]);
+      D2 rn[2];
+      rn[0] = res5(Bc[0], cf.inv_h2, cf.dd, U[1][0], uw0, U[1][1], U[0][0], U[2][0]);
+      rn[1] = res5(Bc[1], cf.inv_h2, cf.dd, U[1][1], U[1][0], ue1, U[0][1], U[2][1]);
+      const bool rin = row_in(row);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) rn[k] = csel(rin && cin[k], rn[k]);
+      D2 sn[2];
+      if constexpr (!JACOBI) {
+        const D2 rw0 = shfl_up2(rn[1]), re1 = shfl_dn2(rn[0]);
+        sn[0] = cadd(rw0, rn[1]);
+        sn[1] = cadd(rn[0], re1);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        R[0][k] = R[1][k];
+        R[1][k] = R[2][k];
+        R[2][k] = rn[k];
+        if constexpr (!JACOBI) {
+          S[0][k] = S[1][k];
+          S[1][k] = S[2][k];
+          S[2][k] = sn[k];
+        }
+      }
+    }
+    // ---- stage C: delta, u_out at row j-2 (u_in at row j-2 is U[0]) ------------------------------------
+    {
+      const int row = j - 2;
+      const bool rin = row_in(row);
+      const bool rst = row >= olo && row < ohi;
+      D2 dn[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        D2 dl;
+        if constexpr (JACOBI) {
+          dl = cmul(cf.k0, R[1][k]);
+        } else {  // (h^2/4)[c,2b,c;2b,4a,2b;c,2b,c] r with omega folded in (smoother.cpp:31-40)
+          const D2 e1 = cadd(cadd(S[1][k], R[0][k]), R[2][k]);
+          const D2 e2 = cadd(S[0][k], S[2][k]);
+          dl = cdot3(cf.k0, R[1][k], cf.k1, e1, cf.k2, e2);
+        }
+        const bool inn = rin && cin[k];
+        dl = csel(inn, dl);
+        // u_in at row j-2 is the OLDEST u row after this step's shift only if we read it before; U[0] holds
+        // row j-2 here because the window was shifted at stage A
+        const D2 ui = U[0][k];
+        const V us = st2<V>(cadd(ui, dl));
+        if (rst && cst[k]) uout[(int64_t)row * n + cA + k] = us;
+        if constexpr (EVEN) dl = csel(inn, csub(ld2(us), ui));
+        dn[k] = dl;
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        Dl[0][k] = Dl[1][k];
+        Dl[1][k] = Dl[2][k];
+        Dl[2][k] = dn[k];
+      }
+    }
+    if constexpr (HASD) {
+      // ---- stage D: r2 at row j-3 = r - (A + lambda I) delta  (r at j-3 is R[0]) -----------------------
+      const int row = j - 3;
+      const bool rin = row_in(row);
+      const D2 dw0 = shfl_up2(Dl[1][1]), de1 = shfl_dn2(Dl[1][0]);
+      D2 r2[2];
+      r2[0] = res5(R[0][0], cf.inv_h2, cf.dd, Dl[1][0], dw0, Dl[1][1], Dl[0][0], Dl[2][0]);
+      r2[1] = res5(R[0][1], cf.inv_h2, cf.dd, Dl[1][1], Dl[1][0], de1, Dl[0][1], Dl[2][1]);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) r2[k] = csel(rin && cin[k], r2[k]);
+      if constexpr (POST == POST_NORM) {
+        if (row >= olo && row < ohi) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            if (cst[k]) nacc += r2[k].x * r2[k].x + r2[k].y * r2[k].y;
+        }
+      }
+      if constexpr (POST == POST_RESTRICT) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          R2[0][k] = R2[1][k];
+          R2[1][k] = R2[2][k];
+          R2[2][k] = r2[k];
+        }
+        // ---- stage E: coarse row J with fine rows 2J-1..2J+1 = row-2..row (grid.cpp:102-121) -------------
+        if ((row & 1) && row >= r0 + 1 && row <= r0 + Hs) {
+          const int J = (row - 1) >> 1;
+          D2 v[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) v[k] = cadd(cadd(R2[0][k], cscale(2.0, R2[1][k])), R2[2][k]);
+          const D2 vw = shfl_up2(v[1]);  // column cA - 1 (cA is even: the coarse centre 2I = cA)
+          const int I = cA >> 1;
+          if (cA >= x0 && cA < x0 + WOUT && I >= 1 && I <= nc - 1 && J >= 1 && J <= nc - 1) {
+            const D2 s = cadd(cadd(vw, cscale(2.0, v[0])), v[1]);
+            a.bc[(int64_t)shift * a.ssc + (int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, s));
+          }
+        }
+      }
+    }
+  }
+  if constexpr (POST == POST_NORM) {
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+    if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
   }
 }
 
