@@ -93,8 +93,14 @@ void orc_random_real(uint32_t seed, double lo, double hi, int64_t count, double*
   for (int64_t k = 0; k < count; ++k) out[k] = uniform(&s, lo, hi);
 }
 
+/* principal value of alpha^p for real alpha != 0 (alpha < 0: |alpha|^p e^{i pi p}) */
+static orc_cplx real_pow_c(double alpha, double p) {
+  if (alpha > 0.0) return pow(alpha, p);
+  return pow(-alpha, p) * cexp(_Complex_I * (M_PI * p));
+}
+
 void orc_circulant_shifts(double alpha, int nt, double dt, int j0, int count, double* out) {
-  const double g = pow(alpha, 1.0 / nt);
+  const orc_cplx g = real_pow_c(alpha, 1.0 / nt);
   for (int q = 0; q < count; ++q) {
     const int j = j0 + q;
     const double ang = 2.0 * M_PI * (double)j / (double)nt;
@@ -694,14 +700,14 @@ int orc_paradiag_circulant(int n, int nt, double alpha, double dt, const orc_con
                            orc_cplx* u, int* iters, int* conv, double* relres, int threads) {
   if (nt < 2) return fail(ORC_CONFIG, "TimeDiscretization: need n >= 2 time steps");
   if (!(dt > 0.0)) return fail(ORC_CONFIG, "TimeDiscretization: tau must be positive");
-  if (!(alpha > 0.0)) return fail(ORC_CONFIG, "alpha-circulant: alpha must be positive");
+  if (!(alpha != 0.0) || alpha != alpha) return fail(ORC_CONFIG, "alpha-circulant: alpha must be nonzero");
   const long N = (long)(n - 1) * (n - 1);
   orc_cplx* tw = (orc_cplx*)malloc(sizeof(orc_cplx) * (size_t)nt);
   for (int q = 0; q < nt; ++q) tw[q] = cexp(_Complex_I * (2.0 * M_PI * (double)q / (double)nt));
   orc_cplx* g = (orc_cplx*)calloc((size_t)nt * N, sizeof(orc_cplx));
   orc_cplx* w = (orc_cplx*)calloc((size_t)nt * N, sizeof(orc_cplx));
-  double* sc = (double*)malloc(sizeof(double) * (size_t)nt);
-  for (int t = 0; t < nt; ++t) sc[t] = pow(alpha, (double)t / nt);
+  orc_cplx* sc = (orc_cplx*)malloc(sizeof(orc_cplx) * (size_t)nt);
+  for (int t = 0; t < nt; ++t) sc[t] = real_pow_c(alpha, (double)t / nt);
   /* step 1: g_k = (1/nt) sum_t alpha^(t/nt) f_t e^{+2 pi i t k / nt} */
   for (int k = 0; k < nt; ++k) {
     orc_cplx* gk = g + (size_t)k * N;
@@ -728,7 +734,7 @@ int orc_paradiag_circulant(int n, int nt, double alpha, double dt, const orc_con
         const orc_cplx* wk = w + (size_t)k * N;
         for (long p = 0; p < N; ++p) ut[p] += c * wk[p];
       }
-      const double s = 1.0 / sc[t];
+      const orc_cplx s = (orc_cplx)1.0 / sc[t];
       for (long p = 0; p < N; ++p) ut[p] *= s;
     }
     double fn = 0.0;

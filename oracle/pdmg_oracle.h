@@ -93,7 +93,9 @@ int orc_mg_solve_batch(int n, int count, const orc_cplx* lambdas, const orc_conf
                        int* converged, double* rates, int threads);
 
 /* ---- ParaDIAG with the alpha-circulant time matrix (restated) ----
- * C_alpha = (1/dt)(I - Sigma_alpha), Sigma_alpha = down-shift with corner alpha at (0, nt-1).
+ * C_alpha = (1/dt)(I - Sigma_alpha), Sigma_alpha = down-shift with corner alpha at (0, nt-1).  alpha > 0 is
+ * the BASELINE circulant preconditioner; alpha = -1/beta < 0 is the reference's BackwardHeatQBV matrix
+ * (paradiag.cpp:180-188), diagonalized with the principal root |alpha|^(1/nt) e^(i pi/nt) (paradiag.cpp:209-213).
  * Solves (C_alpha (x) I + I (x) A) U = F: g = ifft_t(alpha^(t/nt) f), nt shifted MG solves,
  * U = alpha^(-t/nt) fft_k(w).  f, u: nt * m*m complex (time-major). */
 int orc_paradiag_circulant(int n, int nt, double alpha, double dt, const orc_config* cfg,

@@ -275,11 +275,14 @@ struct KernelTable {
 
 template <class T>
 struct MarchTable {
-  void (*e[32])(MarchArgs<T>) = {};
-  static int key(bool lu, bool pr, int post, bool ja) { return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (ja ? 16 : 0); }
+  void (*e[64])(MarchArgs<T>) = {};
+  static int key(bool lu, bool pr, int post, bool ja, int lc) {
+    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (ja ? 16 : 0) | (lc == 2 ? 32 : 0);
+  }
   template <bool LU, bool PR, int PO, bool JA>
   void reg() {
-    e[key(LU, PR, PO, JA)] = &k_march<T, LU, PR, PO, JA>;
+    e[key(LU, PR, PO, JA, 1)] = &k_march<T, LU, PR, PO, JA, 1>;
+    e[key(LU, PR, PO, JA, 2)] = &k_march<T, LU, PR, PO, JA, 2>;
   }
   template <int PO, bool JA>
   void reg4() {
@@ -375,6 +378,7 @@ struct Engine : EngineBase {
   std::vector<cudaEvent_t> event_pool;
   int march_min_n = 64;  // levels with n >= this use the warp-marching sweep kernel (0 = never)
   int march_hs = 0;       // strip height override (0 = automatic)
+  int march_lc = 2;       // columns per lane of the marcher (1 or 2)
 
   static const MarchTable<T>& marches() {
     static MarchTable<T> t;
@@ -390,7 +394,7 @@ struct Engine : EngineBase {
   int march_hs_for(int n) const { return march_hs > 0 ? march_hs : (n >= 512 ? 128 : 64); }
   int march_tasks(int l, int post) const {
     const int hA = (post == POST_RESTRICT ? 1 : post == POST_NONE ? -1 : 0) + 3;
-    const int wout = 64 - 2 * hA, n = lv[l].n, hs = march_hs_for(n);
+    const int wout = 32 - 2 * hA, n = lv[l].n, hs = march_hs_for(n);  // LC = 1 (most tasks): sizing bound
     return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
   }
 
@@ -465,6 +469,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (dev < 0 || dev >= ndev) throw CudaError("pdmg_create: CUDA device " + std::to_string(dev) + " not available");
@@ -629,11 +634,11 @@ struct Engine : EngineBase {
       ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
       ma.coef = Lv.coef, ma.active = active, ma.n = a.n, ma.nc = a.nc, ma.ss = a.ss, ma.ssc = a.ssc;
       const int hA = (v.post == POST_RESTRICT ? 4 : v.post == POST_NORM ? 3 : 2);
-      const int wout = 64 - 2 * hA;
+      const int wout = 32 * march_lc - 2 * hA;
       ma.Hs = march_hs_for(Lv.n);
       ma.ntx = (Lv.n + wout - 1) / wout;
       ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
-      auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi)];
+      auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi, march_lc)];
       if (!fn) throw std::logic_error("pdmg_b200: no march kernel for variant " + v.name());
       dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
       timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma); });
@@ -1010,8 +1015,8 @@ struct Engine : EngineBase {
 // ---------------------------------------------------------------------------------------------
 struct DftTables {
   double2* tw = nullptr;  // e^{dir 2 pi i q/nt}
-  double* pre = nullptr;
-  double* post = nullptr;
+  double2* pre = nullptr;
+  double2* post = nullptr;
   int nt = 0, log2nt = -1;
   ~DftTables() {
     cudaFree(tw);
@@ -1020,28 +1025,35 @@ struct DftTables {
   }
 };
 
+// principal value of alpha^p for real alpha != 0 (alpha < 0: |alpha|^p e^{i pi p}, paradiag.cpp:209-213)
+cplx real_pow_c(double alpha, double p) {
+  if (alpha > 0.0) return cplx(std::pow(alpha, p), 0.0);
+  return std::polar(std::pow(-alpha, p), M_PI * p);
+}
+
 // step 1: pre = alpha^(t/nt), dir +1, post = 1/nt;  step 3: pre = 1, dir -1, post = alpha^(-t/nt)
 std::unique_ptr<DftTables> make_dft_tables(int nt, double alpha, int step, cudaStream_t st) {
   if (nt < 1) throw ConfigError("time DFT: nt must be >= 1");
   auto T = std::make_unique<DftTables>();
   T->nt = nt;
   T->log2nt = ((nt & (nt - 1)) == 0) ? __builtin_ctz((unsigned)nt) : -1;
-  std::vector<double2> tw(nt);
-  std::vector<double> pre(nt), post(nt);
+  std::vector<double2> tw(nt), pre(nt), post(nt);
   const double dir = step == 1 ? 1.0 : -1.0;
   for (int q = 0; q < nt; ++q) {
     const cplx z = std::polar(1.0, dir * 2.0 * M_PI * (double)q / (double)nt);
     tw[q] = make_double2(z.real(), z.imag());
-    const double sc = std::pow(alpha, (double)q / (double)nt);
-    pre[q] = step == 1 ? sc : 1.0;
-    post[q] = step == 1 ? 1.0 / nt : 1.0 / sc;
+    const cplx sc = real_pow_c(alpha, (double)q / (double)nt);
+    const cplx pr = step == 1 ? sc : cplx(1.0, 0.0);
+    const cplx po = step == 1 ? cplx(1.0 / nt, 0.0) : cplx(1.0, 0.0) / sc;
+    pre[q] = make_double2(pr.real(), pr.imag());
+    post[q] = make_double2(po.real(), po.imag());
   }
   CK(cudaMalloc(&T->tw, sizeof(double2) * nt));
-  CK(cudaMalloc(&T->pre, sizeof(double) * nt));
-  CK(cudaMalloc(&T->post, sizeof(double) * nt));
+  CK(cudaMalloc(&T->pre, sizeof(double2) * nt));
+  CK(cudaMalloc(&T->post, sizeof(double2) * nt));
   CK(cudaMemcpyAsync(T->tw, tw.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(T->pre, pre.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(T->post, post.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(T->pre, pre.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(T->post, post.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return T;
 }
@@ -1085,7 +1097,7 @@ struct Paradiag {
   void setup(int n_, int nt_, double alpha_, double dt_, const pdmg_mg_config& cfg, int dev) {
     if (nt_ < 2) throw ConfigError("TimeDiscretization: need n >= 2 time steps");
     if (!(dt_ > 0.0)) throw ConfigError("TimeDiscretization: tau must be positive");
-    if (!(alpha_ > 0.0)) throw ConfigError("alpha-circulant: alpha must be positive");
+    if (!(alpha_ != 0.0)) throw ConfigError("alpha-circulant: alpha must be nonzero");
     n = n_, nt = nt_, alpha = alpha_, dt = dt_, device = dev;
     std::vector<pdmg_c128> lam(nt);
     pdmg_circulant_shifts(alpha, nt, dt, 0, nt, lam.data());
@@ -1263,7 +1275,7 @@ void pdmg_random_rhs(uint32_t seed, double lo, double hi, int64_t count, pdmg_c1
 }
 
 void pdmg_circulant_shifts(double alpha, int32_t nt, double dt, int32_t j0, int32_t count, pdmg_c128* out) {
-  const double g = std::pow(alpha, 1.0 / nt);
+  const cplx g = real_pow_c(alpha, 1.0 / nt);
   for (int q = 0; q < count; ++q) {
     const double ang = 2.0 * M_PI * (double)(j0 + q) / (double)nt;
     const cplx lam = (cplx(1.0, 0.0) - g * std::exp(cplx(0.0, ang))) / dt;
@@ -1372,7 +1384,7 @@ int pdmg_time_dft(int32_t device, int32_t nt, int64_t npts, double alpha, int32_
                   void* stream) {
   return guarded([&] {
     if (step != 1 && step != 3) throw ConfigError("pdmg_time_dft: step must be 1 (forward transform) or 3 (back)");
-    if (!(alpha > 0.0)) throw ConfigError("alpha-circulant: alpha must be positive");
+    if (!(alpha != 0.0)) throw ConfigError("alpha-circulant: alpha must be nonzero");
     CK(cudaSetDevice(device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto T = make_dft_tables(nt, alpha, step, st);

@@ -723,10 +723,11 @@ namespace pdmg_b200 {
 
 constexpr int DFT_THREADS = 256;
 
-// tw[q] = e^{dir 2 pi i q / nt}; pre[t] multiplies the input, post[k] the output (fp64 host tables).
+// tw[q] = e^{dir 2 pi i q / nt}; pre[t] multiplies the input, post[k] the output (complex fp64 host tables:
+// alpha^(t/nt) is complex for the QBV scheme's alpha < 0).
 __global__ void k_time_dft(const double2* __restrict__ in, double2* __restrict__ out, int nt, int log2nt, int npts,
-                           int P, const double2* __restrict__ tw, const double* __restrict__ pre,
-                           const double* __restrict__ post) {
+                           int P, const double2* __restrict__ tw, const double2* __restrict__ pre,
+                           const double2* __restrict__ post) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [nt][P]
   const int p0 = blockIdx.x * P;
@@ -736,12 +737,7 @@ __global__ void k_time_dft(const double2* __restrict__ in, double2* __restrict__
   for (int q = tid; q < nt * P; q += blockDim.x) {
     const int t = q / P, pl = q - t * P;
     double2 v = make_double2(0.0, 0.0);
-    if (pl < np) {
-      v = in[(int64_t)t * npts + p0 + pl];
-      const double s = pre[t];
-      v.x *= s;
-      v.y *= s;
-    }
+    if (pl < np) v = cmul(pre[t], in[(int64_t)t * npts + p0 + pl]);
     const int dst = log2nt >= 0 ? (int)(__brev((unsigned)t) >> (32 - log2nt)) : t;
     buf[dst * P + pl] = v;
   }
@@ -763,11 +759,7 @@ __global__ void k_time_dft(const double2* __restrict__ in, double2* __restrict__
     }
     for (int q = tid; q < nt * P; q += blockDim.x) {
       const int k = q / P, pl = q - k * P;
-      if (pl < np) {
-        double2 v = buf[k * P + pl];
-        const double s = post[k];
-        out[(int64_t)k * npts + p0 + pl] = make_double2(v.x * s, v.y * s);
-      }
+      if (pl < np) out[(int64_t)k * npts + p0 + pl] = cmul(post[k], buf[k * P + pl]);
     }
   } else {
     for (int q = tid; q < nt * P; q += blockDim.x) {
@@ -782,8 +774,7 @@ __global__ void k_time_dft(const double2* __restrict__ in, double2* __restrict__
         idx += k;
         if (idx >= nt) idx -= nt;
       }
-      const double s = post[k];
-      out[(int64_t)k * npts + p0 + pl] = make_double2(acc.x * s, acc.y * s);
+      out[(int64_t)k * npts + p0 + pl] = cmul(post[k], acc);
     }
   }
 }
@@ -1140,7 +1131,7 @@ struct MarchArgs {
   int ntx, ntasks, Hs;  // strips across, warp tasks per shift, strip height
 };
 
-template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI>
+template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI, int LC>
 __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
   using V = typename vec2<T>::type;
   using D2 = double2;
@@ -1149,7 +1140,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
   constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
   constexpr int hC = HASD ? hD + 1 : 0;
   constexpr int hA = hC + 2;
-  constexpr int WOUT = 64 - 2 * hA;
+  constexpr int WOUT = 32 * LC - 2 * hA;  // stored columns per warp
   const int shift = blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
   const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
@@ -1165,10 +1156,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
   const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
   const LevelCoef cf = a.coef[shift];
 
-  const int cA = x0 - hA + 2 * lane;  // storage column of this lane's first column
-  bool cin[2], cst[2];
+  const int cA = x0 - hA + LC * lane;  // storage column of this lane's first column
+  bool cin[LC], cst[LC];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < LC; ++k) {
     const int c = cA + k;
     cin[k] = (unsigned)(c - 1) < (unsigned)m;
     cst[k] = cin[k] && c >= x0 && c < x0 + WOUT;
@@ -1177,13 +1168,12 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
   const int olo = max(r0, 1), ohi = min(r0 + Hs, m + 1);
   auto row_in = [&](int row) { return (unsigned)(row - 1) < (unsigned)m; };
 
-  // loads of one row (u_in incl. prolongation, b) for this lane's two columns
   auto load_u = [&](int row, D2* out) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) out[k] = cz<D2>();
+    for (int k = 0; k < LC; ++k) out[k] = cz<D2>();
     if (!row_in(row)) return;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < LC; ++k) {
       if (!cin[k]) continue;
       const int c = cA + k;
       D2 v = cz<D2>();
@@ -1202,17 +1192,22 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
   };
   auto load_b = [&](int row, D2* out) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < LC; ++k)
       out[k] = (row_in(row) && cin[k]) ? ld2(bb[(int64_t)row * n + cA + k]) : cz<D2>();
   };
+  // horizontal neighbours of a row held as x[LC]: west of column k and east of column k
+  auto west = [&](const D2* x, int k, const D2& wl) { return k == 0 ? wl : x[k - 1]; };
+  auto east = [&](const D2* x, int k, const D2& er) { return k == LC - 1 ? er : x[k + 1]; };
 
-  // register windows: index 0 = oldest row
-  D2 U[3][2], R[3][2], S[3][2], Dl[3][2], R2[3][2];
-  D2 Bc[2], Un[2], Bn[2];
+  D2 U[3][LC], R[3][LC], S[3][LC], Dl[3][LC];
+  D2 Vp[LC], R2c[LC];  // restriction: partial vertical 1-2-1 sum of the coarse row in progress, last r2
+  D2 Bc[LC], Un[LC], Bn[LC];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
-    for (int k = 0; k < 2; ++k) U[q][k] = R[q][k] = S[q][k] = Dl[q][k] = R2[q][k] = cz<D2>();
+    for (int k = 0; k < LC; ++k) U[q][k] = R[q][k] = S[q][k] = Dl[q][k] = cz<D2>();
+#pragma unroll
+  for (int k = 0; k < LC; ++k) Vp[k] = R2c[k] = cz<D2>();
   double nacc = 0.0;
   load_u(rlo, Un);
   load_b(rlo - 1, Bn);
@@ -1220,7 +1215,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
   for (int j = rlo; j < rhi; ++j) {
     // ---- stage A: u row j (prefetched), prefetch row j+1 --------------------------------------------
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < LC; ++k) {
       U[0][k] = U[1][k];
       U[1][k] = U[2][k];
       U[2][k] = Un[k];
@@ -1233,21 +1228,21 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
     // ---- stage B: r at row j-1 = b - (A + lambda I) u  ---------------------------------------------
     {
       const int row = j - 1;
-      const D2 uw0 = shfl_up2(U[1][1]), ue1 = shfl_dn2(U[1][0]);
-      D2 rn[2];
-      rn[0] = res5(Bc[0], cf.inv_h2, cf.dd, U[1][0], uw0, U[1][1], U[0][0], U[2][0]);
-      rn[1] = res5(Bc[1], cf.inv_h2, cf.dd, U[1][1], U[1][0], ue1, U[0][1], U[2][1]);
       const bool rin = row_in(row);
+      const D2 wl = shfl_up2(U[1][LC - 1]), er = shfl_dn2(U[1][0]);
+      D2 rn[LC];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) rn[k] = csel(rin && cin[k], rn[k]);
-      D2 sn[2];
+      for (int k = 0; k < LC; ++k)
+        rn[k] = csel(rin && cin[k], res5(Bc[k], cf.inv_h2, cf.dd, U[1][k], west(U[1], k, wl), east(U[1], k, er),
+                                         U[0][k], U[2][k]));
+      D2 sn[LC];
       if constexpr (!JACOBI) {
-        const D2 rw0 = shfl_up2(rn[1]), re1 = shfl_dn2(rn[0]);
-        sn[0] = cadd(rw0, rn[1]);
-        sn[1] = cadd(rn[0], re1);
+        const D2 rwl = shfl_up2(rn[LC - 1]), rer = shfl_dn2(rn[0]);
+#pragma unroll
+        for (int k = 0; k < LC; ++k) sn[k] = cadd(west(rn, k, rwl), east(rn, k, rer));
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < LC; ++k) {
         R[0][k] = R[1][k];
         R[1][k] = R[2][k];
         R[2][k] = rn[k];
@@ -1263,9 +1258,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
       const int row = j - 2;
       const bool rin = row_in(row);
       const bool rst = row >= olo && row < ohi;
-      D2 dn[2];
+      D2 dn[LC];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < LC; ++k) {
         D2 dl;
         if constexpr (JACOBI) {
           dl = cmul(cf.k0, R[1][k]);
@@ -1276,8 +1271,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
         }
         const bool inn = rin && cin[k];
         dl = csel(inn, dl);
-        // u_in at row j-2 is the OLDEST u row after this step's shift only if we read it before; U[0] holds
-        // row j-2 here because the window was shifted at stage A
         const D2 ui = U[0][k];
         const V us = st2<V>(cadd(ui, dl));
         if (rst && cst[k]) uout[(int64_t)row * n + cA + k] = us;
@@ -1285,7 +1278,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
         dn[k] = dl;
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < LC; ++k) {
         Dl[0][k] = Dl[1][k];
         Dl[1][k] = Dl[2][k];
         Dl[2][k] = dn[k];
@@ -1295,38 +1288,47 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
       // ---- stage D: r2 at row j-3 = r - (A + lambda I) delta  (r at j-3 is R[0]) -----------------------
       const int row = j - 3;
       const bool rin = row_in(row);
-      const D2 dw0 = shfl_up2(Dl[1][1]), de1 = shfl_dn2(Dl[1][0]);
-      D2 r2[2];
-      r2[0] = res5(R[0][0], cf.inv_h2, cf.dd, Dl[1][0], dw0, Dl[1][1], Dl[0][0], Dl[2][0]);
-      r2[1] = res5(R[0][1], cf.inv_h2, cf.dd, Dl[1][1], Dl[1][0], de1, Dl[0][1], Dl[2][1]);
+      const D2 wl = shfl_up2(Dl[1][LC - 1]), er = shfl_dn2(Dl[1][0]);
+      D2 r2[LC];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) r2[k] = csel(rin && cin[k], r2[k]);
+      for (int k = 0; k < LC; ++k)
+        r2[k] = csel(rin && cin[k], res5(R[0][k], cf.inv_h2, cf.dd, Dl[1][k], west(Dl[1], k, wl),
+                                         east(Dl[1], k, er), Dl[0][k], Dl[2][k]));
       if constexpr (POST == POST_NORM) {
         if (row >= olo && row < ohi) {
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
+          for (int k = 0; k < LC; ++k)
             if (cst[k]) nacc += r2[k].x * r2[k].x + r2[k].y * r2[k].y;
         }
       }
       if constexpr (POST == POST_RESTRICT) {
+        // ---- stage E: coarse row J, fine rows 2J-1, 2J, 2J+1 (grid.cpp:102-121) --------------------------
+        // vertical 1-2-1 accumulated as rows arrive: odd row 2J-1 opens J (and closes J-1), even row 2J adds 2x
+        if (row & 1) {
+          D2 v[LC];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          R2[0][k] = R2[1][k];
-          R2[1][k] = R2[2][k];
-          R2[2][k] = r2[k];
-        }
-        // ---- stage E: coarse row J with fine rows 2J-1..2J+1 = row-2..row (grid.cpp:102-121) -------------
-        if ((row & 1) && row >= r0 + 1 && row <= r0 + Hs) {
-          const int J = (row - 1) >> 1;
-          D2 v[2];
-#pragma unroll
-          for (int k = 0; k < 2; ++k) v[k] = cadd(cadd(R2[0][k], cscale(2.0, R2[1][k])), R2[2][k]);
-          const D2 vw = shfl_up2(v[1]);  // column cA - 1 (cA is even: the coarse centre 2I = cA)
-          const int I = cA >> 1;
-          if (cA >= x0 && cA < x0 + WOUT && I >= 1 && I <= nc - 1 && J >= 1 && J <= nc - 1) {
-            const D2 s = cadd(cadd(vw, cscale(2.0, v[0])), v[1]);
-            a.bc[(int64_t)shift * a.ssc + (int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, s));
+          for (int k = 0; k < LC; ++k) {
+            v[k] = cadd(Vp[k], r2[k]);  // closes coarse row (row-1)/2 = J
+            Vp[k] = r2[k];              // opens coarse row J+1 with its first fine row
           }
+          const int J = (row - 1) >> 1;
+          if (row >= r0 + 1 && row <= r0 + Hs && J >= 1 && J <= nc - 1) {
+            const D2 vwl = shfl_up2(v[LC - 1]), ver = shfl_dn2(v[0]);
+#pragma unroll
+            for (int k = 0; k < LC; ++k) {
+              const int c = cA + k;
+              if (!(c & 1) && c >= x0 && c < x0 + WOUT) {
+                const int I = c >> 1;
+                if (I >= 1 && I <= nc - 1) {
+                  const D2 s = cadd(cadd(west(v, k, vwl), cscale(2.0, v[k])), east(v, k, ver));
+                  a.bc[(int64_t)shift * a.ssc + (int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, s));
+                }
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < LC; ++k) Vp[k] = cadd(Vp[k], cscale(2.0, r2[k]));
         }
       }
     }

@@ -100,3 +100,106 @@ def _real_draws(seed: int, lo: float, hi: float, count: int) -> np.ndarray:
     buf = np.empty((count + 1) // 2, np.complex128)
     N.lib().pdmg_random_rhs(seed, lo, hi, buf.size, buf.ctypes.data)
     return buf.view(np.float64)[:count].copy()
+
+
+# ---------------------------------------------------------------------------------------------------
+# Reference-facing time discretizations (proj/include/pdmg/paradiag.hpp:13-33)
+# ---------------------------------------------------------------------------------------------------
+import enum as _enum  # noqa: E402
+from dataclasses import dataclass as _dataclass  # noqa: E402
+
+
+class TimeSchemeKind(_enum.IntEnum):
+    HeatBVM = 0          # boundary-value-method stencil (general dense eigendecomposition; not on the GPU path)
+    BackwardHeatQBV = 1  # quasi-boundary-value regularization: alpha-circulant with alpha = -1/beta
+    CirculantAlpha = 2   # BASELINE's alpha-circulant backward-Euler preconditioner, alpha > 0
+
+
+@_dataclass(frozen=True)
+class TimeDiscretization:
+    """pdmg::TimeDiscretization (paradiag.hpp:18-33); `alpha` is used by CirculantAlpha only."""
+
+    kind: TimeSchemeKind = TimeSchemeKind.BackwardHeatQBV
+    n: int = 0
+    tau: float = 0.0
+    beta: float = 0.01
+    alpha: float = 0.01
+
+    def dim(self) -> int:  # paradiag.hpp:25
+        return self.n + 1 if self.kind == TimeSchemeKind.BackwardHeatQBV else self.n
+
+    def validate(self) -> None:  # paradiag.hpp:27-32
+        if self.n < 2:
+            raise ConfigError("TimeDiscretization: need n >= 2 time steps")
+        if not self.tau > 0.0:
+            raise ConfigError("TimeDiscretization: tau must be positive")
+        if self.kind == TimeSchemeKind.BackwardHeatQBV and not self.beta > 0.0:
+            raise ConfigError("TimeDiscretization: beta must be positive")
+
+    def circulant_alpha(self) -> float:
+        if self.kind == TimeSchemeKind.BackwardHeatQBV:
+            return -1.0 / self.beta  # paradiag.cpp:209
+        if self.kind == TimeSchemeKind.CirculantAlpha:
+            return self.alpha
+        raise ConfigError("HeatBVM needs a general eigendecomposition of B (paradiag.cpp:71-82); "
+                          "only the circulant schemes run on the B200 path")
+
+
+def time_stepping_matrix(td: TimeDiscretization) -> np.ndarray:
+    """Dense B (paradiag.cpp:46-69 for HeatBVM/QBV; C_alpha for CirculantAlpha) -- host-side, for oracles."""
+    td.validate()
+    it = 1.0 / td.tau
+    if td.kind == TimeSchemeKind.HeatBVM:
+        n = td.n
+        B = np.zeros((n, n))
+        for i in range(n - 1):
+            B[i, i + 1] = 0.5 * it
+            if i > 0:
+                B[i, i - 1] = -0.5 * it
+        B[n - 1, n - 2] = -it
+        B[n - 1, n - 1] = it
+        return B
+    m = td.dim()
+    B = np.zeros((m, m))
+    for i in range(m):
+        B[i, i] = it
+        if i > 0:
+            B[i, i - 1] = -it
+    B[0, m - 1] = -td.circulant_alpha() * it
+    return B
+
+
+def paradiag_solve(f: np.ndarray, td: TimeDiscretization, cfg: MultigridConfig, device: int = 0):
+    """paradiag_solve (paradiag.cpp:185-248) for the circulant schemes: returns (u, reports, relres)."""
+    td.validate()
+    f = np.ascontiguousarray(f, np.complex128)
+    if f.shape[0] != td.dim():
+        raise ConfigError(f"paradiag_solve: expected {td.dim()} time slices, got {f.shape[0]}")
+    n = f.shape[-1] + 1
+    with ParadiagCirculant(n, td.dim(), td.circulant_alpha(), td.tau, cfg, device) as pd:
+        return pd.run(f)
+
+
+def manufactured_field(grid: Grid2D | int, slices: int, tau: float) -> np.ndarray:
+    """u*(x, y, t_i) = sin(pi x) sin(pi y) (1 + t_i), t_i = (i+1) tau (paradiag.cpp:250-267)."""
+    n = grid.n if isinstance(grid, Grid2D) else int(grid)
+    h = 1.0 / n
+    x = np.arange(1, n) * h
+    base = np.outer(np.sin(np.pi * x), np.sin(np.pi * x))
+    return np.stack([base * (1.0 + (s + 1) * tau) for s in range(slices)]).astype(np.complex128)
+
+
+def all_at_once_apply(B: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """(B (x) I + I (x) A) u, matrix-free over numpy slices (paradiag.cpp:141-161); host-side helper."""
+    n = u.shape[-1] + 1
+    h2 = 1.0 / n ** 2
+    out = np.empty_like(u)
+    for i in range(u.shape[0]):
+        z = np.pad(u[i], 1)
+        au = (4 * z[1:-1, 1:-1] - z[:-2, 1:-1] - z[2:, 1:-1] - z[1:-1, :-2] - z[1:-1, 2:]) / h2
+        y = au
+        for j in range(u.shape[0]):
+            if B[i, j] != 0.0:
+                y = y + B[i, j] * u[j]
+        out[i] = y
+    return out

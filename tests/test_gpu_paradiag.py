@@ -66,3 +66,44 @@ def test_config5_heat_step(oracle):
     # each slot is solved to 1e-10 of its transformed rhs; alpha^(-t/nt) (up to 1/alpha) re-amplifies
     # the late slices on the way back, so the all-at-once residual sits near 1e-9 -- same as the oracle's
     assert relres < 1e-8 and abs(relres - ref["relres"]) <= 1e-3 * ref["relres"]
+
+
+def test_qbv_tiny_matches_dense_kronecker(oracle):
+    """test_paradiag.cpp:214-226 on the GPU: BackwardHeatQBV (alpha = -1/beta) vs the dense all-at-once solve."""
+    td = P.TimeDiscretization(P.TimeSchemeKind.BackwardHeatQBV, 4, 0.25, 0.01)
+    n, m, nt = 4, 3, td.dim()
+    B = P.time_stepping_matrix(td)
+    K = np.kron(B, np.eye(m * m)) + np.kron(np.eye(nt), oracle.dense_operator(n, 0.0))
+    f = np.stack([oracle.random_complex(50 + i, m * m) for i in range(nt)]).reshape(nt, m, m)
+    want = np.linalg.solve(K, f.ravel())
+    cfg = P.MultigridConfig(coarsest_n=4)
+    u, reps, relres = P.paradiag_solve(f, td, cfg)
+    assert all(r.converged for r in reps)
+    assert np.linalg.norm(u.ravel() - want) <= 1e-8 * np.linalg.norm(want)
+    assert relres <= 1e-10
+
+
+def test_qbv_matches_oracle(oracle):
+    td = P.TimeDiscretization(P.TimeSchemeKind.BackwardHeatQBV, 8, 1.0 / 8, 0.01)
+    n, m, nt = 32, 31, td.dim()
+    f = oracle.random_complex(7, nt * m * m).reshape(nt, m, m)
+    cfg = P.MultigridConfig(P.CycleKind.V, 1, 1, 4, 1e-10, 200, P.SmootherConfig.vanka())
+    u, reps, relres = P.paradiag_solve(f, td, cfg)
+    ref = oracle.paradiag(n, nt, td.circulant_alpha(), td.tau, Cfg(), f, threads=8)
+    assert [r.iterations for r in reps] == ref["iterations"].tolist()
+    assert rel(u, ref["u"]) < 1e-10
+    assert abs(relres - ref["relres"]) <= 1e-3 * ref["relres"] + 1e-14
+
+
+def test_qbv_manufactured_run():
+    """'manufactured space-time run converges with a small residual' (test_paradiag.cpp:230-250), QBV scheme,
+    reference W(1,0) preset: relres <= 1e-6 and the manufactured field is recovered to 1e-5."""
+    n = 16
+    td = P.TimeDiscretization(P.TimeSchemeKind.BackwardHeatQBV, n, 1.0 / n, 0.01)
+    ustar = P.manufactured_field(n, td.dim(), td.tau)
+    f = P.all_at_once_apply(P.time_stepping_matrix(td), ustar)
+    u, reps, relres = P.paradiag_solve(f, td, P.MultigridConfig())
+    assert all(r.converged for r in reps)
+    assert relres <= 1e-6
+    err = max(np.linalg.norm(u[i] - ustar[i]) / np.linalg.norm(ustar[i]) for i in range(td.dim()))
+    assert err <= 1e-5

@@ -221,3 +221,26 @@ def test_paradiag_circulant_small(oracle):
     r = oracle.paradiag(n, nt, 0.01, 1 / nt, Cfg(tol=1e-12), f, threads=4)
     assert r["converged"].all()
     assert r["relres"] < 1e-10
+
+
+def test_qbv_scheme_matches_dense_kronecker(oracle):
+    """'space-time solve with the regularized backward scheme matches its oracle' (test_paradiag.cpp:214-226):
+    BackwardHeatQBV = alpha-circulant with alpha = -1/beta; tiny grid so the coarse solve is exact."""
+    import numpy as np
+
+    import paper_2203_11154_b200 as P
+
+    td = P.TimeDiscretization(P.TimeSchemeKind.BackwardHeatQBV, 4, 0.25, 0.01)
+    n, m, nt = 4, 3, td.dim()
+    B = P.time_stepping_matrix(td)
+    K = np.kron(B, np.eye(m * m)) + np.kron(np.eye(nt), oracle.dense_operator(n, 0.0))
+    f = np.stack([oracle.random_complex(50 + i, m * m) for i in range(nt)])
+    want = np.linalg.solve(K, f.ravel())
+    r = oracle.paradiag(n, nt, td.circulant_alpha(), td.tau, Cfg(coarsest_n=4), f, threads=2)
+    assert np.linalg.norm(r["u"].ravel() - want) <= 1e-8 * np.linalg.norm(want)
+    assert r["relres"] <= 1e-10
+    # the closed-form eigenvalues (paradiag.cpp:221) are the shift set, in reversed slot order
+    g = (1 / td.beta) ** (1 / nt) * np.exp(1j * np.pi / nt)
+    ref = np.array([(1 - g * np.exp(-2j * np.pi * k / nt)) / td.tau for k in range(nt)])
+    mine = oracle.circulant_shifts(td.circulant_alpha(), nt, td.tau)
+    np.testing.assert_allclose(mine, ref[(-np.arange(nt)) % nt], rtol=1e-13)
