@@ -140,6 +140,16 @@ int pdmg_paradiag_run_device(pdmg_paradiag* p, const void* d_f, void* d_u, pdmg_
 int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg,
                             int32_t device, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* report,
                             double* relres);
+/* General diagonalizable time matrix (the reference's HeatBVM path: diagonalize_time_matrix, paradiag.cpp:71-82,
+ * then paradiag_solve, paradiag.cpp:185-248): the caller supplies B = V diag(lambdas) V^{-1} (host, nt x nt
+ * row-major; B real).  g = (V^{-1} (x) I) f and u = (V (x) I) w run as dense complex GEMMs over the time index
+ * on the GPU; relres = ||f - (B (x) I + I (x) A) u|| / ||f||. */
+int pdmg_paradiag_general(int32_t n, int32_t nt, const pdmg_c128* lambdas, const pdmg_c128* V, const pdmg_c128* Vinv,
+                          const double* B, const pdmg_mg_config* cfg, int32_t device, const pdmg_c128* f,
+                          pdmg_c128* u, pdmg_solve_report* report, double* relres);
+/* Y = (M (x) I) X for device arrays [nt][npts] (kron_time_apply, paradiag.cpp:129-133); M host nt x nt. */
+int pdmg_time_transform(int32_t device, int32_t nt, int64_t npts, const pdmg_c128* M, const void* d_in, void* d_out,
+                        void* stream);
 /* Building blocks of the multi-GPU driver (time slices sharded over ranks, NCCL all-to-all between):
  * alpha-scaled DFT over the full time axis of npts points laid out [nt][npts] (step 1 or 3 above), and
  * the all-at-once residual of local slices [t0, t0+ntl) given the slice before t0 (u_{nt-1} if t0 == 0):

@@ -75,6 +75,9 @@ def lib() -> C.CDLL:
         "pdmg_paradiag_run": (C.c_int, [vp, vp, vp, C.POINTER(SolveReport), C.POINTER(f64)]),
         "pdmg_paradiag_run_device": (C.c_int, [vp, vp, vp, C.POINTER(SolveReport), C.POINTER(f64)]),
         "pdmg_time_dft": (C.c_int, [i32, i32, i64, f64, i32, vp, vp, vp]),
+        "pdmg_paradiag_general": (C.c_int, [i32, i32, vp, vp, vp, vp, C.POINTER(MgConfig), i32, vp, vp,
+                                            C.POINTER(SolveReport), C.POINTER(f64)]),
+        "pdmg_time_transform": (C.c_int, [i32, i32, i64, vp, vp, vp, vp]),
         "pdmg_aao_residual": (C.c_int, [i32, i32, i32, i32, f64, f64, vp, vp, vp, C.POINTER(f64), vp]),
         "pdmg_random_rhs": (None, [C.c_uint32, f64, f64, i64, vp]),
         "pdmg_circulant_shifts": (None, [f64, i32, f64, i32, i32, vp]),

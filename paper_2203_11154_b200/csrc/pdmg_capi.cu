@@ -6,6 +6,7 @@
 // cycle is a short sequence of batched k_level launches (pdmg_kernels.cuh) over all still-active
 // shifts; convergence is decided on the device per shift (k_finalize) exactly as in
 // MultigridHierarchy::solve, so per-shift cycle counts match the reference.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1151,6 +1152,89 @@ struct Paradiag {
 
 using namespace pdmg_b200;
 
+namespace pdmg_b200 {
+
+// cuBLAS handle per device (created on first use); plain library ZGEMMs for the dense time transforms
+cublasHandle_t cublas_for(int device) {
+  static std::map<int, cublasHandle_t> handles;
+  auto it = handles.find(device);
+  if (it != handles.end()) return it->second;
+  cublasHandle_t h;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
+  handles[device] = h;
+  return h;
+}
+
+// Y[nt][npts] = M[nt][nt] X[nt][npts] (row-major, time slowest): column-major Y^T = X^T M^T, i.e.
+// ZGEMM(N, N, npts, nt, nt, X, M-as-column-major(=M^T)).
+void time_gemm(int device, cudaStream_t st, int nt, int64_t npts, const double2* dM, const double2* dX, double2* dY) {
+  cublasHandle_t h = cublas_for(device);
+  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream failed");
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  const cublasStatus_t s =
+      cublasZgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)npts, nt, nt, &one, reinterpret_cast<const cuDoubleComplex*>(dX),
+                  (int)npts, reinterpret_cast<const cuDoubleComplex*>(dM), nt, &zero,
+                  reinterpret_cast<cuDoubleComplex*>(dY), (int)npts);
+  if (s != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasZgemm failed (" + std::to_string((int)s) + ")");
+}
+
+// paradiag_solve with a general diagonalization B = V diag(lambda) V^{-1} supplied by the caller
+// (diagonalize_time_matrix, paradiag.cpp:71-82): g = (V^{-1} (x) I) f, batched shifted solves,
+// u = (V (x) I) w, relres = ||f - (B (x) I + I (x) A) u|| / ||f|| (paradiag.cpp:185-248).
+void paradiag_general(int n, int nt, const pdmg_c128* lambdas, const pdmg_c128* V, const pdmg_c128* Vinv,
+                      const double* B, const pdmg_mg_config& cfg, int device, const pdmg_c128* f, pdmg_c128* u,
+                      pdmg_solve_report* rep, double* relres) {
+  pdmg_batch_desc d{n, nt, lambdas, cfg, PDMG_PREC_C128, device};
+  Engine<double> eng;
+  eng.device = -1;
+  eng.setup_host(d);
+  eng.setup_device(device);
+  cudaStream_t st = eng.stream;
+  const int64_t npts = (int64_t)(n - 1) * (n - 1);
+  const size_t bytes = sizeof(double2) * (size_t)nt * npts;
+  double2 *d_f = nullptr, *d_g = nullptr, *d_w = nullptr, *d_u = nullptr, *d_V = nullptr, *d_Vi = nullptr,
+          *d_B = nullptr;
+  double* d_part = nullptr;
+  const int blocks = 148 * 8;
+  auto cleanup = [&] {
+    cudaFree(d_f), cudaFree(d_g), cudaFree(d_w), cudaFree(d_u), cudaFree(d_V), cudaFree(d_Vi), cudaFree(d_B);
+    cudaFree(d_part);
+  };
+  try {
+    for (double2** p : {&d_f, &d_g, &d_w, &d_u}) CK(cudaMalloc(p, bytes));
+    for (double2** p : {&d_V, &d_Vi, &d_B}) CK(cudaMalloc(p, sizeof(double2) * nt * nt));
+    CK(cudaMalloc(&d_part, sizeof(double) * 2 * blocks));
+    std::vector<double2> Bc((size_t)nt * nt);
+    for (size_t q = 0; q < Bc.size(); ++q) Bc[q] = make_double2(B[q], 0.0);
+    CK(cudaMemcpyAsync(d_V, V, sizeof(double2) * nt * nt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_Vi, Vinv, sizeof(double2) * nt * nt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_B, Bc.data(), sizeof(double2) * nt * nt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_f, f, bytes, cudaMemcpyHostToDevice, st));
+    time_gemm(device, st, nt, npts, d_Vi, d_f, d_g);  // step 1 (kron_time_solve, paradiag.cpp:135-139)
+    eng.solve_device(d_g, d_w, rep);                   // step 2 (paradiag.cpp:207-236)
+    time_gemm(device, st, nt, npts, d_V, d_w, d_u);   // step 3 (kron_time_apply, paradiag.cpp:129-133)
+    if (relres) {
+      time_gemm(device, st, nt, npts, d_B, d_u, d_g);  // (B (x) I) u
+      k_aao_residual_dense<<<blocks, 256, 0, st>>>(d_u, d_g, d_f, n, nt, d_part);
+      CK(cudaGetLastError());
+      std::vector<double> part(2 * blocks);
+      CK(cudaMemcpyAsync(part.data(), d_part, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      double rr = 0.0, ff = 0.0;
+      for (int b = 0; b < blocks; ++b) rr += part[2 * b], ff += part[2 * b + 1];
+      *relres = ff > 0.0 ? std::sqrt(rr) / std::sqrt(ff) : std::sqrt(rr);
+    }
+    CK(cudaMemcpyAsync(u, d_u, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+}  // namespace pdmg_b200
+
 struct pdmg_ctx {
   std::unique_ptr<EngineBase> e;
 };
@@ -1378,6 +1462,36 @@ int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, cons
   st = pdmg_paradiag_run(P, f, u, rep, relres);
   pdmg_paradiag_destroy(P);
   return st;
+}
+
+int pdmg_paradiag_general(int32_t n, int32_t nt, const pdmg_c128* lambdas, const pdmg_c128* V, const pdmg_c128* Vinv,
+                          const double* B, const pdmg_mg_config* cfg, int32_t device, const pdmg_c128* f, pdmg_c128* u,
+                          pdmg_solve_report* report, double* relres) {
+  return guarded([&] {
+    if (!lambdas || !V || !Vinv || !B || !cfg || !f || !u) throw ConfigError("pdmg_paradiag_general: NULL argument");
+    if (nt < 1) throw ConfigError("paradiag_solve: empty right-hand side");
+    paradiag_general(n, nt, lambdas, V, Vinv, B, *cfg, device, f, u, report, relres);
+  });
+}
+
+int pdmg_time_transform(int32_t device, int32_t nt, int64_t npts, const pdmg_c128* M, const void* d_in, void* d_out,
+                        void* stream) {
+  return guarded([&] {
+    if (!M || !d_in || !d_out) throw ConfigError("pdmg_time_transform: NULL argument");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double2* dM = nullptr;
+    CK(cudaMalloc(&dM, sizeof(double2) * nt * nt));
+    CK(cudaMemcpyAsync(dM, M, sizeof(double2) * nt * nt, cudaMemcpyHostToDevice, st));
+    try {
+      time_gemm(device, st, nt, npts, dM, static_cast<const double2*>(d_in), static_cast<double2*>(d_out));
+      CK(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaFree(dM);
+      throw;
+    }
+    cudaFree(dM);
+  });
 }
 
 int pdmg_time_dft(int32_t device, int32_t nt, int64_t npts, double alpha, int32_t step, const void* d_in, void* d_out,

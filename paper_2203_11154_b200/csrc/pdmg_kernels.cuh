@@ -1340,3 +1340,52 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
 }
 
 }  // namespace pdmg_b200
+
+// ===================================================================================================
+// General (dense) time matrix B for ParaDIAG (HeatBVM, paradiag.cpp:46-82): the time transforms are dense
+// complex GEMMs over the time index (cuBLAS ZGEMM, see pdmg_capi.cu); this kernel forms the all-at-once
+// residual r = f - Y - (I (x) A) u with Y = (B (x) I) u precomputed, and its per-block partial norms.
+// ===================================================================================================
+namespace pdmg_b200 {
+
+__global__ void k_aao_residual_dense(const double2* __restrict__ u, const double2* __restrict__ y,
+                                     const double2* __restrict__ f, int n, int nt, double* __restrict__ partial) {
+  const int m = n - 1, npts = m * m;
+  const double h = 1.0 / n, inv_h2 = 1.0 / (h * h);
+  double rr = 0.0, ff = 0.0;
+  const int64_t total = (int64_t)nt * npts;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(q / npts), p = (int)(q - (int64_t)t * npts);
+    const int j = p / m, i = p - j * m;
+    const double2* ut = u + (int64_t)t * npts;
+    const double2 c = ut[p];
+    double ax = 4.0 * c.x, ay = 4.0 * c.y;  // A u (unshifted 5-point, grid.cpp:69-90)
+    if (i > 0) ax -= ut[p - 1].x, ay -= ut[p - 1].y;
+    if (i < m - 1) ax -= ut[p + 1].x, ay -= ut[p + 1].y;
+    if (j > 0) ax -= ut[p - m].x, ay -= ut[p - m].y;
+    if (j < m - 1) ax -= ut[p + m].x, ay -= ut[p + m].y;
+    const double2 yv = y[q], fv = f[q];
+    const double rx = fv.x - (inv_h2 * ax + yv.x), ry = fv.y - (inv_h2 * ay + yv.y);
+    rr += rx * rx + ry * ry;
+    ff += fv.x * fv.x + fv.y * fv.y;
+  }
+  __shared__ double red[2][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    ff += __shfl_xor_sync(0xffffffffu, ff, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[0][w] = rr, red[1][w] = ff;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    double a = l < nw ? red[0][l] : 0.0, b = l < nw ? red[1][l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (l == 0) partial[2 * blockIdx.x] = a, partial[2 * blockIdx.x + 1] = b;
+  }
+}
+
+}  // namespace pdmg_b200

@@ -110,7 +110,7 @@ from dataclasses import dataclass as _dataclass  # noqa: E402
 
 
 class TimeSchemeKind(_enum.IntEnum):
-    HeatBVM = 0          # boundary-value-method stencil (general dense eigendecomposition; not on the GPU path)
+    HeatBVM = 0          # boundary-value-method stencil (general dense eigendecomposition, GEMM time transforms)
     BackwardHeatQBV = 1  # quasi-boundary-value regularization: alpha-circulant with alpha = -1/beta
     CirculantAlpha = 2   # BASELINE's alpha-circulant backward-Euler preconditioner, alpha > 0
 
@@ -141,8 +141,7 @@ class TimeDiscretization:
             return -1.0 / self.beta  # paradiag.cpp:209
         if self.kind == TimeSchemeKind.CirculantAlpha:
             return self.alpha
-        raise ConfigError("HeatBVM needs a general eigendecomposition of B (paradiag.cpp:71-82); "
-                          "only the circulant schemes run on the B200 path")
+        raise ConfigError("HeatBVM is not circulant: use diagonalize_time_matrix (paradiag.cpp:71-82)")
 
 
 def time_stepping_matrix(td: TimeDiscretization) -> np.ndarray:
@@ -169,15 +168,68 @@ def time_stepping_matrix(td: TimeDiscretization) -> np.ndarray:
     return B
 
 
+@_dataclass
+class TimeDiagonalization:
+    """pdmg::TimeDiagonalization (paradiag.hpp:45-53): B = V diag(eigenvalues) V^{-1}."""
+
+    eigenvalues: np.ndarray
+    V: np.ndarray
+    Vinv: np.ndarray
+    cond_estimate: float
+    ill_conditioned: bool
+
+
+def diagonalize_time_matrix(B: np.ndarray) -> TimeDiagonalization:
+    """diagonalize_time_matrix (paradiag.cpp:71-82): general dense eigendecomposition (host, setup time; the
+    reference uses Eigen::EigenSolver, here LAPACK through numpy).  The eigenvalue order may differ from
+    Eigen's; the solution of the space-time system does not depend on it."""
+    if B.ndim != 2 or B.shape[0] != B.shape[1] or B.shape[0] < 1:
+        raise ConfigError("diagonalize_time_matrix: matrix must be square and nonempty")
+    lam, V = np.linalg.eig(B)
+    V = V.astype(np.complex128)
+    cond = float(np.linalg.cond(V, 1))
+    return TimeDiagonalization(lam.astype(np.complex128), V, np.linalg.inv(V), cond, not cond <= 1e12)
+
+
 def paradiag_solve(f: np.ndarray, td: TimeDiscretization, cfg: MultigridConfig, device: int = 0):
-    """paradiag_solve (paradiag.cpp:185-248) for the circulant schemes: returns (u, reports, relres)."""
+    """paradiag_solve (paradiag.cpp:185-248): returns (u, reports, relres).  The circulant schemes
+    (BackwardHeatQBV, CirculantAlpha) transform time with an alpha-scaled FFT; HeatBVM with dense GEMMs
+    against the eigenvector matrix."""
     td.validate()
     f = np.ascontiguousarray(f, np.complex128)
     if f.shape[0] != td.dim():
         raise ConfigError(f"paradiag_solve: expected {td.dim()} time slices, got {f.shape[0]}")
     n = f.shape[-1] + 1
-    with ParadiagCirculant(n, td.dim(), td.circulant_alpha(), td.tau, cfg, device) as pd:
-        return pd.run(f)
+    if td.kind != TimeSchemeKind.HeatBVM:
+        with ParadiagCirculant(n, td.dim(), td.circulant_alpha(), td.tau, cfg, device) as pd:
+            return pd.run(f)
+    B = np.ascontiguousarray(time_stepping_matrix(td), np.float64)
+    dg = diagonalize_time_matrix(B)
+    nt = td.dim()
+    u = np.empty_like(f)
+    H = cfg.max_iter + 1
+    it, cv = np.zeros(nt, np.int32), np.zeros(nt, np.uint8)
+    hist, rate = np.zeros((nt, H)), np.zeros(nt)
+    rep = N.SolveReport(it.ctypes.data, cv.ctypes.data, hist.ctypes.data, rate.ctypes.data, 0.0)
+    rr = C.c_double()
+    lam = np.ascontiguousarray(dg.eigenvalues)
+    V, Vi = np.ascontiguousarray(dg.V), np.ascontiguousarray(dg.Vinv)
+    c = cfg._c()
+    _check(N.lib().pdmg_paradiag_general(n, nt, lam.ctypes.data, V.ctypes.data, Vi.ctypes.data, B.ctypes.data,
+                                         C.byref(c), device, f.ctypes.data, u.ctypes.data, C.byref(rep),
+                                         C.byref(rr)))
+    reps = [SolveReport(bool(cv[s]), int(it[s]), hist[s, : it[s] + 1].copy(), float(rate[s]), rep.seconds)
+            for s in range(nt)]
+    return u, reps, rr.value
+
+
+def helmholtz_shifts(h: float) -> np.ndarray:
+    """lambda_j = -j^2 (1 - 0.5 i), j = 1..min(128, floor(1/(2h))) (paradiag.cpp:237-247)."""
+    if not (0.0 < h < 0.5):
+        raise ConfigError("helmholtz_shifts: need 0 < h < 1/2")
+    jmax = min(128, int(np.floor(1.0 / (2.0 * h))))
+    j = np.arange(1, jmax + 1, dtype=np.float64)
+    return (-(j * j) + 0.5j * (j * j)).astype(np.complex128)
 
 
 def manufactured_field(grid: Grid2D | int, slices: int, tau: float) -> np.ndarray:

@@ -107,3 +107,32 @@ def test_qbv_manufactured_run():
     assert relres <= 1e-6
     err = max(np.linalg.norm(u[i] - ustar[i]) / np.linalg.norm(ustar[i]) for i in range(td.dim()))
     assert err <= 1e-5
+
+
+def test_heat_bvm_tiny_matches_dense_kronecker(oracle):
+    """'space-time solve matches a dense oracle on a tiny problem' (test_paradiag.cpp:198-212): HeatBVM,
+    4 slices x 9 unknowns, general eigendecomposition + GPU GEMM time transforms."""
+    td = P.TimeDiscretization(P.TimeSchemeKind.HeatBVM, 4, 0.25, 0.01)
+    n, m, nt = 4, 3, td.dim()
+    f = np.stack([oracle.random_complex(1 + i, m * m) for i in range(nt)]).reshape(nt, m, m)
+    B = P.time_stepping_matrix(td)
+    K = np.kron(B, np.eye(m * m)) + np.kron(np.eye(nt), oracle.dense_operator(n, 0.0))
+    want = np.linalg.solve(K, f.ravel())
+    u, reps, relres = P.paradiag_solve(f, td, P.MultigridConfig(coarsest_n=4))
+    assert all(r.converged for r in reps)
+    assert np.linalg.norm(u.ravel() - want) <= 1e-8 * np.linalg.norm(want)
+    assert relres <= 1e-10
+
+
+def test_heat_bvm_manufactured_run():
+    """'manufactured space-time run converges with a small residual' (test_paradiag.cpp:230-250): HeatBVM,
+    n = 16, tau = 1/16, reference W(1,0) preset: relres <= 1e-6, manufactured error <= 1e-5."""
+    n = 16
+    td = P.TimeDiscretization(P.TimeSchemeKind.HeatBVM, n, 1.0 / n, 0.01)
+    ustar = P.manufactured_field(n, td.dim(), td.tau)
+    f = P.all_at_once_apply(P.time_stepping_matrix(td), ustar)
+    u, reps, relres = P.paradiag_solve(f, td, P.MultigridConfig())
+    assert all(r.converged for r in reps)
+    assert relres <= 1e-6
+    err = max(np.linalg.norm(u[i] - ustar[i]) / np.linalg.norm(ustar[i]) for i in range(td.dim()))
+    assert err <= 1e-5
