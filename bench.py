@@ -77,50 +77,55 @@ def updates_per_cycle(n: int, nu1: int, nu2: int, coarsest: int = 4) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks line), in-process
+    through NVML (the library nvidia-smi reads; spawning nvidia-smi every 50 ms contends for driver locks with the
+    solve's per-cycle host synchronisation).  Falls back to nvidia-smi when NVML is unavailable."""
 
-    def __init__(self, device: int):
-        self.device = device
-        self.samples = []
-        self.proc = None
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+    def __init__(self, device: int, period_s: float = 0.02):
+        self.device, self.period = device, period_s
+        self.samples = []  # (sm_mhz, max_mhz, reasons_mask)
+        self._stop = threading.Event()
+        self.src = "nvml"
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, mx, rs))
+                    except Exception:
+                        pass
+                    self._stop.wait(self.period)
+
+            self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self.thread = None
+            self.src = "unavailable"
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"clock sampling {self.src}"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({k for s in self.samples for k, bit in self.REASONS.items() if s[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": self.src}
 
 
 def cpu_reference_run(n, lams, nu1, nu2, b, threads):
@@ -232,17 +237,22 @@ def run_paradiag(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    t0 = time.perf_counter()
+    # events on the stream the library launches on (the solver's stream for one GPU, torch's for the
+    # distributed driver whose kernels run on torch's current stream)
+    from paper_2203_11154_b200 import _native as N
+
+    sh = N.lib().pdmg_stream(pd.solver_handle) if world == 1 else None
+    stream = torch.cuda.ExternalStream(sh) if sh else torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    t0 = time.perf_counter()
     with ClockSampler(local) as clk:
+        ev0.record(stream)
         for _ in range(args.steps):
             out = step()
-        ev1.record()
+        ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    ms = max(ms, wall_ms)  # steps synchronize on the host internally; take the larger clock
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -265,6 +275,7 @@ def run_paradiag(args):
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": desc, "parallelism": f"time-sharded x{world} + NCCL all-to-all"},
             "paradiag_steps_per_s": 1e3 / ms, "relres": relres, "cycles_total": iters_total,
+            "host_wall_ms_per_step": wall_ms,
             "clocks": clk.summary()}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

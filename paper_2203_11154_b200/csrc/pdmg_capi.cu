@@ -366,7 +366,8 @@ struct Engine : EngineBase {
   double *d_r0 = nullptr, *d_hist = nullptr, *d_partial = nullptr, *d_norms = nullptr;
   double2* d_stage = nullptr;  // compact complex128 host-I/O staging
   size_t stage_elems = 0;
-  int* h_nactive = nullptr;
+  int* h_nactive = nullptr;  // [2] pinned: active-shift counts of the last two cycles
+  cudaEvent_t ev_nactive[2] = {nullptr, nullptr};
   int n_active_host = 0;
   const KernelTable<T>* table = nullptr;
   // instrumentation
@@ -378,6 +379,7 @@ struct Engine : EngineBase {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   int march_min_n = 64;  // levels with n >= this use the warp-marching sweep kernel (0 = never)
+  int level_h_min_n = 512;  // levels with n >= this use 128-row strips in k_level (else 64)
   int march_hs = 0;       // strip height override (0 = automatic)
   int march_lc = 2;       // columns per lane of the marcher (1 or 2)
 
@@ -431,6 +433,8 @@ struct Engine : EngineBase {
     cudaFree(d_norms);
     cudaFree(d_stage);
     if (h_nactive) cudaFreeHost(h_nactive);
+    for (auto e : ev_nactive)
+      if (e) cudaEventDestroy(e);
     for (auto& p : pending) {
       cudaEventDestroy(p.e0);
       cudaEventDestroy(p.e1);
@@ -468,6 +472,7 @@ struct Engine : EngineBase {
   void setup_device(int dev) override {
     device = dev;
     if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_LEVEL_H_MIN_N")) level_h_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
@@ -489,7 +494,7 @@ struct Engine : EngineBase {
         CK(cudaMalloc(p, Lv.elems * sizeof(V)));
         CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
       }
-      Lv.H = std::min(Lv.n >= 512 ? 128 : 64, Lv.n + (Lv.n & 1));
+      Lv.H = std::min(Lv.n >= level_h_min_n ? 128 : 64, Lv.n + (Lv.n & 1));
       Lv.ntx = (Lv.n + TILE_W - 1) / TILE_W;
       Lv.nty = (Lv.n + Lv.H - 1) / Lv.H;
       Lv.ntiles = Lv.ntx * Lv.nty;
@@ -547,7 +552,7 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&d_active, sizeof(int) * S));
     CK(cudaMalloc(&d_iters, sizeof(int) * S));
     CK(cudaMalloc(&d_conv, sizeof(int) * S));
-    CK(cudaMalloc(&d_nactive, sizeof(int)));
+    CK(cudaMalloc(&d_nactive, 2 * sizeof(int)));
     CK(cudaMalloc(&d_parity, sizeof(int) * (cfg.max_iter + 1)));
     CK(cudaMalloc(&d_ones, sizeof(int) * S));
     CK(cudaMalloc(&d_r0, sizeof(double) * S));
@@ -556,7 +561,9 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&d_norms, sizeof(double) * S));
     std::vector<int> ones(S, 1);
     CK(cudaMemcpyAsync(d_ones, ones.data(), sizeof(int) * S, cudaMemcpyHostToDevice, stream));
-    CK(cudaMallocHost(&h_nactive, sizeof(int)));
+    CK(cudaMallocHost(&h_nactive, 2 * sizeof(int)));
+    CK(cudaEventCreateWithFlags(&ev_nactive[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_nactive[1], cudaEventDisableTiming));
     for (auto& kv : table->e)
       if (kv.fn) CK(cudaFuncSetAttribute(kv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.smem));
     CK(cudaStreamSynchronize(stream));
@@ -711,14 +718,22 @@ struct Engine : EngineBase {
     return normed;
   }
 
-  void finalize(int k, int ntiles) {
-    CK(cudaMemsetAsync(d_nactive, 0, sizeof(int), stream));
-    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive, S, cfg.max_iter, cfg.tol};
+  // Convergence bookkeeping of cycle k (k_finalize); the active count lands in pinned slot k % 2.  With
+  // wait = false the host does not block: the solve loop enqueues cycle k+1 before reading cycle k's count
+  // (converged shifts are frozen on the device, so a speculative extra cycle leaves them untouched).
+  void finalize(int k, int ntiles, bool wait = true) {
+    const int slot = k & 1;
+    CK(cudaMemsetAsync(d_nactive + slot, 0, sizeof(int), stream));
+    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol};
     const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
     timed("finalize", 0.0, [&] { k_finalize<<<blocks, threads, 0, stream>>>(d_partial, ntiles, k, st); });
-    CK(cudaMemcpyAsync(h_nactive, d_nactive, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    n_active_host = *h_nactive;
+    CK(cudaMemcpyAsync(h_nactive + slot, d_nactive + slot, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(ev_nactive[slot], stream));
+    if (wait) n_active_host = read_nactive(k);
+  }
+  int read_nactive(int k) {
+    CK(cudaEventSynchronize(ev_nactive[k & 1]));
+    return h_nactive[k & 1];
   }
 
   void unpack(const double2* src, V* dst, int l) {
@@ -770,7 +785,7 @@ struct Engine : EngineBase {
       sa.nu1 = cfg.nu1, sa.nu2 = cfg.nu2, sa.gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
       sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
       sa.ainv = d_ainv, sa.coarse_N = coarse_N;
-      sa.iterations = d_iters, sa.converged = d_conv, sa.r0 = d_r0, sa.hist = d_hist, sa.n_active = d_nactive;
+      sa.iterations = d_iters, sa.converged = d_conv, sa.r0 = d_r0, sa.hist = d_hist, sa.n_active = d_nactive;  // unused
       const double per_shift_bytes = 0.0;
       (void)per_shift_bytes;
       timed("small_solve", 0.0, [&] {
@@ -795,14 +810,17 @@ struct Engine : EngineBase {
         if (act[s] && coarse_singular[s])
           throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
     }
-    for (int k = 1; k <= cfg.max_iter && n_active_host > 0; ++k) {
-      const int n_act = n_active_host;
+    // cycles are enqueued one ahead of the host's convergence check (pipelined: the GPU never idles on it)
+    int n_act = n_active_host;
+    for (int k = 1; k <= cfg.max_iter && n_act > 0; ++k) {
       const bool normed = cycle_level(0, k == 1, d_active, n_act, true);
       if (!normed)
         level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr, nullptr,
                    d_active, n_act);
       parity[k] = F.cur;
-      finalize(k, last_partials);
+      finalize(k, last_partials, false);
+      if (k >= 2 || k == cfg.max_iter) n_act = read_nactive(k == cfg.max_iter ? k : k - 1);
+      if (k == 1 && cfg.max_iter > 1) continue;  // cycle 2 is enqueued before cycle 1's count is read
     }
     CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
     pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);

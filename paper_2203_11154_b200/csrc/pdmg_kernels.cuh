@@ -383,11 +383,14 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
     if constexpr (SWEEP) {
       if (t + 1 < n_iter) issue(t + 1, true, false);  // lands in ring rows no stage of step t touches
       // -------------- stage B: r = b - (A + lambda I) u_in  (grid.cpp:69-100) ---------------------
-      if (tid < WB * RGROUPS) {
+      const int gB = tid / WB;
+      const int kbg = base - 1 + CHUNK * t + RPT * gB;
+      if (tid < WB * RGROUPS && kbg + RPT > r0 - hB && kbg < r0 + H + hB) {
         // rows outside the stage range are computed too (from stale ring rows) and written to ring slots no
-        // later stage reads; only the interior mask (Dirichlet zeros) must be exact
-        const int g = tid / WB, ci = tid - g * WB;
-        const int kb = base - 1 + CHUNK * t + RPT * g, col = c0 - hB + ci;
+        // later stage reads; only the interior mask (Dirichlet zeros) must be exact.  Task groups entirely
+        // outside the range (first/last step of a strip) are skipped.
+        const int g = gB, ci = tid - g * WB;
+        const int kb = kbg, col = c0 - hB + ci;
         const bool cin = (unsigned)(col - 1) < (unsigned)m;
         int sa = slot(kb - 1, ARING), sb = slot(kb, RR);
         const V* ap = RA + ci + (hAs - hB);  // local col of `col` in the A ring
@@ -421,9 +424,11 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
       __syncthreads();
       if (t + 1 < n_iter) issue(t + 1, false, true);
       // -------------- stage C: delta = omega M r; u_out = u_in + delta  (smoother.cpp:49-67) -------
-      if (tid < WC * RGROUPS) {
-        const int g = tid / WC, ci = tid - g * WC;
-        const int kc = base - 2 + CHUNK * t + RPT * g, col = c0 - hC + ci;
+      const int gC = tid / WC;
+      const int kcg = base - 2 + CHUNK * t + RPT * gC;
+      if (tid < WC * RGROUPS && kcg + RPT > r0 - hC && kcg < r0 + H + hC) {
+        const int g = gC, ci = tid - g * WC;
+        const int kc = kcg, col = c0 - hC + ci;
         const bool cin = (unsigned)(col - 1) < (unsigned)m;
         const bool cout = cin && col >= c0 && col < c0 + TILE_W;
         const D2* rpc = RB + (ci + (hB - hC));  // local col of `col` in the r ring
@@ -528,9 +533,11 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
         }
       };
       if constexpr (POST == POST_NORM || POST == POST_RESID) {
-        if (tid < TILE_W * RGROUPS) {
-          const int g = tid / TILE_W, ci = tid - g * TILE_W;
-          const int kd = base - xD + CHUNK * t + RPT * g, col = c0 + ci;
+        const int gD = tid / TILE_W;
+        const int kdg = base - xD + CHUNK * t + RPT * gD;
+        if (tid < TILE_W * RGROUPS && kdg + RPT > r0 && kdg < r0 + H) {
+          const int g = gD, ci = tid - g * TILE_W;
+          const int kd = kdg, col = c0 + ci;
           if (col <= m) {
             r2_column(kd, col, RPT, [&](int, int row, D2 r2) {
               if (row >= r0 && row < r0 + H && row_in(row) && col >= 1) {
