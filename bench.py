@@ -345,12 +345,10 @@ def main():
         reps = H.solve_device(d_b.data_ptr(), d_u.data_ptr())
     # ---- timed region: device-resident inputs, CUDA events on the library's stream ----------
     H.reset_stats()
-    H.set_profiling(True)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
+        ev0.record(stream)
         upd = 0.0
         for _ in range(args.steps):
             reps = H.solve_device(d_b.data_ptr(), d_u.data_ptr())
@@ -359,6 +357,12 @@ def main():
         barrier()
     ms = ev0.elapsed_time(ev1)
     launches = H.launch_count()
+    # ---- per-kernel CUDA-event timing (separate pass: per-launch events cost ~6% of a step) ----
+    H.reset_stats()
+    H.set_profiling(True)
+    for _ in range(max(1, min(args.steps, 3))):
+        H.solve_device(d_b.data_ptr(), d_u.data_ptr(), want_reports=False)
+    torch.cuda.synchronize()
     stats = H.kernel_stats()
     H.set_profiling(False)
     ms_max = max_over_ranks(ms)
@@ -419,6 +423,7 @@ def main():
     roofline = {"bound": bound, "kernel": top_name, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
                 "kernel_share_of_step": round(top["ms"] / total_ms, 4),
+                "timing": "per-kernel CUDA events on the library stream, profiled pass right after the timed region",
                 "launch_avg_ms": round(top["ms"] / top["launches"], 4),
                 "algo_bytes_per_launch": top["bytes"] / top["launches"],
                 "all_kernels_algorithmic_GBps": round(all_bytes / (total_ms / 1e3) / 1e9, 1)}

@@ -380,6 +380,7 @@ struct Engine : EngineBase {
   std::vector<cudaEvent_t> event_pool;
   int march_min_n = 64;  // levels with n >= this use the warp-marching sweep kernel (0 = never)
   int level_h_min_n = 512;  // levels with n >= this use 128-row strips in k_level (else 64)
+  int tail_max_n = 64;      // levels with n <= this run as one per-shift CTA cycle (k_small_cycle); 0 = off
   int march_hs = 0;       // strip height override (0 = automatic)
   int march_lc = 2;       // columns per lane of the marcher (1 or 2)
 
@@ -387,12 +388,12 @@ struct Engine : EngineBase {
     static MarchTable<T> t;
     return t;
   }
-  // measured on B200 (C3, C4): the marcher wins for sweep+norm (the last fine post-sweep), the ring kernel
-  // for the other variants; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher (experiments)
+  // measured on B200 (C3, C4): the marcher wins for sweep+norm and sweep+restrict, the ring
+  // kernel for the plain and prolongating sweeps; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher
   bool march_all = false;
   bool use_march(int l, const Variant& v) const {
-    return march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store &&
-           ((v.post == POST_NORM && !v.prolong) || (march_all && v.post != POST_RESID));
+    return march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store && !v.prolong &&
+           (v.post == POST_NORM || v.post == POST_RESTRICT || march_all) && v.post != POST_RESID;
   }
   int march_hs_for(int n) const { return march_hs > 0 ? march_hs : (n >= 512 ? 128 : 64); }
   int march_tasks(int l, int post) const {
@@ -473,6 +474,7 @@ struct Engine : EngineBase {
     device = dev;
     if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_LEVEL_H_MIN_N")) level_h_min_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_TAIL_MAX_N")) tail_max_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
@@ -672,10 +674,34 @@ struct Engine : EngineBase {
   // zero: u on this level is known to be zero on entry (ec = 0 before recursing, multigrid.cpp:72;
   // u = 0 before the first fine cycle, multigrid.cpp:90).  fuse_norm: leave ||b - L u||^2 partials of
   // the updated fine iterate in d_partial (returns whether it did).
+  // first level of the coarse tail (levels with n <= tail_max_n below the finest), or -1
+  int tail_level() const {
+    if (tail_max_n <= 0 || (int)lv.size() > MAX_LEVELS) return -1;
+    for (int l = 1; l < (int)lv.size(); ++l)
+      if (lv[l].n <= tail_max_n) return l;
+    return -1;
+  }
+  void tail_cycle(int l, const int* active, bool zero) {
+    SmallArgs<T> sa{};
+    for (size_t q = l; q < lv.size(); ++q)
+      sa.lv[q - l] = SmallLevel<T>{lv[q].u[0], lv[q].u[1], lv[q].b, lv[q].coef, lv[q].n, lv[q].ss};
+    sa.L = (int)lv.size() - l;
+    sa.nu1 = cfg.nu1, sa.nu2 = cfg.nu2, sa.gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+    sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
+    sa.ainv = d_ainv, sa.coarse_N = coarse_N, sa.active = active, sa.tail_zero = zero ? 1 : 0;
+    timed("coarse_tail", 0.0,
+          [&] { k_small_cycle<T><<<S, SMALL_THREADS, coarse_N * sizeof(double2), stream>>>(sa); });
+    for (size_t q = l; q < lv.size(); ++q) lv[q].cur = 0, lv[q].uzero = false;
+  }
+
   bool cycle_level(int l, bool zero, const int* active, int n_act, bool want_norm) {
     Level& Lv = lv[l];
     const int L = (int)lv.size();
     const bool jac = cfg.smoother == PDMG_SMOOTHER_JACOBI;
+    if (l > 0 && l == tail_level()) {  // the whole coarse tail in one launch (each visit of a W-cycle)
+      tail_cycle(l, active, zero);
+      return false;
+    }
     if (l + 1 == L) {
       coarse_solve(Lv.b, Lv.u[Lv.cur], active);
       Lv.uzero = false;

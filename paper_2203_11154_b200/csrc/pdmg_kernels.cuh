@@ -875,6 +875,8 @@ struct SmallArgs {
   double* r0;
   double* hist;
   int* n_active;
+  const int* active;  // tail mode: convergence mask of the batched solve (nullptr = all)
+  int tail_zero;      // tail mode: u of the tail's top level starts at zero (first visit of the cycle)
 };
 
 template <class T>
@@ -1060,6 +1062,19 @@ struct SmallSolver {
   }
 };
 
+// Coarse tail of a batched cycle: one CTA per shift runs cycle_on_level from the first tail level down
+// (multigrid.cpp:63-77) entirely in one launch; the tail's top-level u (the correction) starts at zero and
+// is left in lv[0].u for the prolongation by the level above.
+template <class T>
+__global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_cycle(SmallArgs<T> a) {
+  using V = typename vec2<T>::type;
+  __shared__ double red[33];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.active != nullptr && a.active[blockIdx.x] == 0) return;
+  SmallSolver<T> S{a, (int)blockIdx.x, red, reinterpret_cast<double2*>(smem_raw)};
+  S.cycle(a.tail_zero != 0);
+}
+
 template <class T>
 __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a) {
   using V = typename vec2<T>::type;
@@ -1139,7 +1154,10 @@ struct MarchArgs {
 };
 
 template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI, int LC>
-__global__ void __launch_bounds__(32 * MARCH_WARPS) k_march(MarchArgs<T> a) {
+#ifndef PDMG_MARCH_MINB
+#define PDMG_MARCH_MINB 3
+#endif
+__global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(MarchArgs<T> a) {
   using V = typename vec2<T>::type;
   using D2 = double2;
   constexpr bool EVEN = sizeof(V) == 8;
