@@ -346,36 +346,42 @@ __global__ void __launch_bounds__(NTHREADS, (LevelShape<T, LOADU || PROLONG, SWE
     __syncthreads();
     // ---------------- stage A: u_in = [u] + P e_c (in place on the landed rows) -----------------
     if constexpr (PROLONG) {  // u += prolong_bilinear(e_c) (grid.cpp:123-153, multigrid.cpp:75)
+      // one thread per coarse cell (I, J): its 2x2 fine block (2I..2I+1, 2J..2J+1) needs e(I..I+1, J..J+1)
       const int k0 = base + CHUNK * t;
       const int J0 = floordiv2(k0), I0 = floordiv2(c0 - hA) / ALN * ALN;
       const int rhi = min(k0 + CHUNK, r0 + H + hA);
-      for (int q = tid; q < CHUNK * WA; q += NTHREADS) {
-        const int lr = q / WA, lc = q - lr * WA;
-        const int row = k0 + lr, col = c0 - hAs + lc;
-        if (row >= rhi) break;
-        V* slotp = RA + slot(row, ARING) * WA + lc;
-        D2 v = cz<D2>();
-        if (row_in(row) && (unsigned)(col - 1) < (unsigned)m) {
-          const V* e0 = CB + (floordiv2(row) - J0) * CB_COLS + (floordiv2(col) - I0);
-          D2 p;
-          if (!(col & 1) && !(row & 1)) {
-            p = ld2(e0[0]);
-          } else if ((col & 1) && !(row & 1)) {
-            p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[1])));
-          } else if (!(col & 1) && (row & 1)) {
-            p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[CB_COLS])));
-          } else {
-            p = cscale(0.25, cadd(cadd(cadd(ld2(e0[0]), ld2(e0[1])), ld2(e0[CB_COLS])), ld2(e0[CB_COLS + 1])));
+      const int clo = c0 - hAs, chi = clo + WA;
+      const int Jb = floordiv2(k0), Ib = floordiv2(clo);
+      const int nJ = floordiv2(rhi - 1) - Jb + 1, nI = floordiv2(chi - 1) - Ib + 1;
+      for (int q = tid; q < nJ * nI; q += NTHREADS) {
+        const int jl = q / nI, il = q - jl * nI;
+        const int J = Jb + jl, I = Ib + il;
+        const V* e0 = CB + (J - J0) * CB_COLS + (I - I0);
+        const D2 e00 = ld2(e0[0]), e10 = ld2(e0[1]), e01 = ld2(e0[CB_COLS]), e11 = ld2(e0[CB_COLS + 1]);
+        const D2 pv[2][2] = {{e00, cscale(0.5, cadd(e00, e10))},
+                             {cscale(0.5, cadd(e00, e01)), cscale(0.25, cadd(cadd(cadd(e00, e10), e01), e11))}};
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+          const int row = 2 * J + dy;
+          if (row < k0 || row >= rhi) continue;
+          V* rowp = RA + slot(row, ARING) * WA - clo;
+          const bool rin = row_in(row);
+#pragma unroll
+          for (int dx = 0; dx < 2; ++dx) {
+            const int col = 2 * I + dx;
+            if (col < clo || col >= chi) continue;
+            D2 v = cz<D2>();
+            if (rin && (unsigned)(col - 1) < (unsigned)m) {
+              v = pv[dy][dx];
+              if constexpr (LOADU) v = cadd(ld2(rowp[col]), v);
+            }
+            const V vs = st2<V>(v);
+            rowp[col] = vs;  // non-interior nodes become exact zeros (the ghost ring the stencil reads)
+            if constexpr (!SWEEP && STORE) {
+              if (row >= r0 && row < r0 + H && rin && col >= c0 && col < c0 + TILE_W && (unsigned)(col - 1) < (unsigned)m)
+                uout[(int64_t)row * n + col] = vs;
+            }
           }
-          v = p;
-          if constexpr (LOADU) v = cadd(ld2(*slotp), p);
-        }
-        const V vs = st2<V>(v);
-        *slotp = vs;  // non-interior nodes become exact zeros (the ghost ring the stencil reads)
-        if constexpr (!SWEEP && STORE) {
-          if (row >= r0 && row < r0 + H && row_in(row) && col >= c0 && col < c0 + TILE_W &&
-              (unsigned)(col - 1) < (unsigned)m)
-            uout[(int64_t)row * n + col] = vs;
         }
       }
       __syncthreads();
