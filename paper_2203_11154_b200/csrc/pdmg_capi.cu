@@ -392,8 +392,9 @@ struct Engine : EngineBase {
   // kernel for the plain and prolongating sweeps; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher
   bool march_all = false;
   bool use_march(int l, const Variant& v) const {
-    return march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store && !v.prolong &&
-           (v.post == POST_NORM || v.post == POST_RESTRICT || march_all) && v.post != POST_RESID;
+    if (!(march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store && v.post != POST_RESID)) return false;
+    if (march_all) return true;
+    return !v.prolong && (v.post == POST_NORM || v.post == POST_RESTRICT);
   }
   int march_hs_for(int n) const { return march_hs > 0 ? march_hs : (n >= 512 ? 128 : 64); }
   int march_tasks(int l, int post) const {

@@ -1199,9 +1199,35 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
   const int olo = max(r0, 1), ohi = min(r0 + Hs, m + 1);
   auto row_in = [&](int row) { return (unsigned)(row - 1) < (unsigned)m; };
 
+  // prolongation: a 2-coarse-row register window of e(Ie .. Ie+LC, J), Ie = floor(cA / 2), refilled once per
+  // coarse row (rows are loaded in increasing order), instead of 2-4 coarse loads per fine row
+  constexpr int NE = LC + 1;
+  D2 E0[NE], E1[NE];
+  int wJ = -1000;
+  const int Ie = cA >> 1;
+  auto load_crow = [&](int J, D2* out) {
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      const int I = Ie + q;
+      out[q] = ((unsigned)J <= (unsigned)nc && (unsigned)I <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + I]) : cz<D2>();
+    }
+  };
   auto load_u = [&](int row, D2* out) {
 #pragma unroll
     for (int k = 0; k < LC; ++k) out[k] = cz<D2>();
+    if constexpr (PROLONG) {
+      const int J = row >> 1;
+      if (J == wJ + 1) {
+#pragma unroll
+        for (int q = 0; q < NE; ++q) E0[q] = E1[q];
+        load_crow(J + 1, E1);
+        wJ = J;
+      } else if (J != wJ) {
+        load_crow(J, E0);
+        load_crow(J + 1, E1);
+        wJ = J;
+      }
+    }
     if (!row_in(row)) return;
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
@@ -1210,12 +1236,16 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
       D2 v = cz<D2>();
       if constexpr (LOADU) v = ld2(uin[(int64_t)row * n + c]);
       if constexpr (PROLONG) {  // u += prolong_bilinear(e_c) (grid.cpp:123-153)
-        const V* e0 = ecs + (int64_t)(row >> 1) * nc + (c >> 1);
+        const int q = (c >> 1) - Ie;  // 0 .. LC-1 (runtime for odd cA): select, no local-memory indexing
+        D2 a0 = E0[0], a1 = E0[1], b0 = E1[0], b1 = E1[1];
+#pragma unroll
+        for (int z = 1; z < LC; ++z)
+          if (q == z) a0 = E0[z], a1 = E0[z + 1], b0 = E1[z], b1 = E1[z + 1];
         D2 p;
-        if (!(c & 1) && !(row & 1)) p = ld2(e0[0]);
-        else if ((c & 1) && !(row & 1)) p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[1])));
-        else if (!(c & 1) && (row & 1)) p = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[nc])));
-        else p = cscale(0.25, cadd(cadd(cadd(ld2(e0[0]), ld2(e0[1])), ld2(e0[nc])), ld2(e0[nc + 1])));
+        if (!(c & 1) && !(row & 1)) p = a0;
+        else if ((c & 1) && !(row & 1)) p = cscale(0.5, cadd(a0, a1));
+        else if (!(c & 1) && (row & 1)) p = cscale(0.5, cadd(a0, b0));
+        else p = cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1));
         v = cadd(v, p);
       }
       out[k] = v;
