@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -366,7 +367,18 @@ struct Engine : EngineBase {
   double *d_r0 = nullptr, *d_hist = nullptr, *d_partial = nullptr, *d_norms = nullptr;
   double2* d_stage = nullptr;  // compact complex128 host-I/O staging
   size_t stage_elems = 0;
-  int* h_nactive = nullptr;  // [2] pinned: active-shift counts of the last two cycles
+  // mapped pinned results, written by k_copy_words: [hist S*H doubles][iters S][conv S][nactive 2]
+  char* h_map = nullptr;
+  char* d_map = nullptr;
+  size_t map_hist() const { return 0; }
+  size_t map_iters() const { return sizeof(double) * (size_t)S * (cfg.max_iter + 1); }
+  size_t map_conv() const { return map_iters() + sizeof(int) * S; }
+  size_t map_nact() const { return map_conv() + sizeof(int) * S; }
+  void to_host(const void* dsrc, size_t map_off, size_t bytes) {
+    const int64_t w = (int64_t)(bytes / 4);
+    const int blocks = (int)std::min<int64_t>((w + 255) / 256, 148);
+    k_copy_words<<<std::max(blocks, 1), 256, 0, stream>>>((const uint32_t*)dsrc, (uint32_t*)(d_map + map_off), w);
+  }
   cudaEvent_t ev_nactive[2] = {nullptr, nullptr};
   int n_active_host = 0;
   const KernelTable<T>* table = nullptr;
@@ -434,7 +446,7 @@ struct Engine : EngineBase {
     cudaFree(d_partial);
     cudaFree(d_norms);
     cudaFree(d_stage);
-    if (h_nactive) cudaFreeHost(h_nactive);
+    if (h_map) cudaFreeHost(h_map);
     for (auto e : ev_nactive)
       if (e) cudaEventDestroy(e);
     for (auto& p : pending) {
@@ -442,6 +454,7 @@ struct Engine : EngineBase {
       cudaEventDestroy(p.e1);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -476,6 +489,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_LEVEL_H_MIN_N")) level_h_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_TAIL_MAX_N")) tail_max_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
@@ -564,7 +578,8 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&d_norms, sizeof(double) * S));
     std::vector<int> ones(S, 1);
     CK(cudaMemcpyAsync(d_ones, ones.data(), sizeof(int) * S, cudaMemcpyHostToDevice, stream));
-    CK(cudaMallocHost(&h_nactive, 2 * sizeof(int)));
+    CK(cudaHostAlloc((void**)&h_map, map_nact() + 2 * sizeof(int), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&d_map, h_map, 0));
     CK(cudaEventCreateWithFlags(&ev_nactive[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_nactive[1], cudaEventDisableTiming));
     for (auto& kv : table->e)
@@ -748,19 +763,19 @@ struct Engine : EngineBase {
   // Convergence bookkeeping of cycle k (k_finalize); the active count lands in pinned slot k % 2.  With
   // wait = false the host does not block: the solve loop enqueues cycle k+1 before reading cycle k's count
   // (converged shifts are frozen on the device, so a speculative extra cycle leaves them untouched).
-  void finalize(int k, int ntiles, bool wait = true) {
+  void finalize(int k, int ntiles, bool wait = true, int cur = 0) {
     const int slot = k & 1;
     CK(cudaMemsetAsync(d_nactive + slot, 0, sizeof(int), stream));
-    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol};
+    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol, d_parity, cur};
     const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
     timed("finalize", 0.0, [&] { k_finalize<<<blocks, threads, 0, stream>>>(d_partial, ntiles, k, st); });
-    CK(cudaMemcpyAsync(h_nactive + slot, d_nactive + slot, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    to_host(d_nactive + slot, map_nact() + sizeof(int) * slot, sizeof(int));
     CK(cudaEventRecord(ev_nactive[slot], stream));
     if (wait) n_active_host = read_nactive(k);
   }
   int read_nactive(int k) {
     CK(cudaEventSynchronize(ev_nactive[k & 1]));
-    return h_nactive[k & 1];
+    return ((volatile int*)(h_map + map_nact()))[k & 1];
   }
 
   void unpack(const double2* src, V* dst, int l) {
@@ -801,7 +816,7 @@ struct Engine : EngineBase {
         std::vector<int> act(S);
         CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
         for (int s = 0; s < S; ++s)
-          if (act[s] && coarse_singular[s])
+          if (act[s] && coarse_singular[s_base + s])
             throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " +
                                         std::to_string(lv.back().n));
       }
@@ -819,8 +834,7 @@ struct Engine : EngineBase {
         k_small_solve<T><<<S, SMALL_THREADS, coarse_N * sizeof(double2), stream>>>(sa);
       });
       CK(cudaGetLastError());
-      std::vector<int> parity(H, 0);
-      CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
+      CK(cudaMemsetAsync(d_parity, 0, sizeof(int) * H, stream));
       pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
       finish_report(rep, t0, H);
       return;
@@ -829,12 +843,11 @@ struct Engine : EngineBase {
     level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
                nullptr, S);
     finalize(0, last_partials);
-    std::vector<int> parity(H, 0);
     if (any_singular && n_active_host > 0) {
       std::vector<int> act(S);
       CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
       for (int s = 0; s < S; ++s)
-        if (act[s] && coarse_singular[s])
+        if (act[s] && coarse_singular[s_base + s])
           throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
     }
     // cycles are enqueued one ahead of the host's convergence check (pipelined: the GPU never idles on it)
@@ -844,29 +857,25 @@ struct Engine : EngineBase {
       if (!normed)
         level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr, nullptr,
                    d_active, n_act);
-      parity[k] = F.cur;
-      finalize(k, last_partials, false);
+      finalize(k, last_partials, false, F.cur);  // records parity[k] = F.cur on the device
       if (k >= 2 || k == cfg.max_iter) n_act = read_nactive(k == cfg.max_iter ? k : k - 1);
       if (k == 1 && cfg.max_iter > 1) continue;  // cycle 2 is enqueued before cycle 1's count is read
     }
-    CK(cudaMemcpyAsync(d_parity, parity.data(), sizeof(int) * H, cudaMemcpyHostToDevice, stream));
     pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
     finish_report(rep, t0, H);
   }
 
   // Copy the per-shift report back; counts the smoother updates performed (sum over shifts of cycles).
   void finish_report(pdmg_solve_report* rep, std::chrono::steady_clock::time_point t0, int H) {
-    std::vector<int> it(S), cv(S);
-    std::vector<double> hist;
-    CK(cudaMemcpyAsync(it.data(), d_iters, sizeof(int) * S, cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(cv.data(), d_conv, sizeof(int) * S, cudaMemcpyDeviceToHost, stream));
+    to_host(d_iters, map_iters(), sizeof(int) * S);
+    to_host(d_conv, map_conv(), sizeof(int) * S);
     const bool need_hist = rep && (rep->residual_history || rep->rate);
-    if (need_hist) {
-      hist.resize((size_t)S * H);
-      CK(cudaMemcpyAsync(hist.data(), d_hist, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost, stream));
-    }
+    if (need_hist) to_host(d_hist, map_hist(), sizeof(double) * S * (size_t)H);
     CK(cudaStreamSynchronize(stream));
     CK(cudaGetLastError());
+    const int* it = (const int*)(h_map + map_iters());
+    const int* cv = (const int*)(h_map + map_conv());
+    const double* hist = (const double*)(h_map + map_hist());
     drain_stats();
     // updates per cycle per shift: (nu1+nu2) * sum_l m_l^2 * gamma^l over non-coarsest levels
     double per_cycle = 0.0, visits = 1.0;
@@ -882,8 +891,8 @@ struct Engine : EngineBase {
         if (rep->iterations) rep->iterations[s] = it[s];
         if (rep->converged) rep->converged[s] = (uint8_t)cv[s];
         if (rep->residual_history)
-          std::memcpy(rep->residual_history + (size_t)s * H, hist.data() + (size_t)s * H, sizeof(double) * H);
-        if (rep->rate) rep->rate[s] = measured_rate(hist.data() + (size_t)s * H, it[s]);
+          std::memcpy(rep->residual_history + (size_t)s * H, hist + (size_t)s * H, sizeof(double) * H);
+        if (rep->rate) rep->rate[s] = measured_rate(hist + (size_t)s * H, it[s]);
       }
       rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
@@ -925,14 +934,117 @@ struct Engine : EngineBase {
                         "-level hierarchy");
   }
 
+  // ---- shift sub-range view: the engine's per-shift arrays offset to shifts [s0, s0 + cnt) ---------------
+  int s_base = 0;  // offset of the current view into coarse_singular
+  struct RangeView {
+    Engine& e;
+    int S0;
+    std::vector<std::array<V*, 3>> saved_lv;
+    std::vector<LevelCoef*> saved_coef;
+    std::vector<size_t> saved_elems;
+    double2* ainv;
+    int *act, *it, *cv, *ones;
+    double *r0, *hist;
+    RangeView(Engine& en, int s0, int cnt) : e(en), S0(en.S) {
+      for (auto& L : e.lv) {
+        saved_lv.push_back({L.u[0], L.u[1], L.b});
+        saved_coef.push_back(L.coef);
+        saved_elems.push_back(L.elems);
+        L.u[0] += s0 * L.ss, L.u[1] += s0 * L.ss, L.b += s0 * L.ss, L.coef += s0;
+        L.elems = (size_t)L.ss * cnt + (s0 + cnt == en.S ? L.n + 2 : 0);
+      }
+      ainv = e.d_ainv, act = e.d_active, it = e.d_iters, cv = e.d_conv, ones = e.d_ones, r0 = e.d_r0, hist = e.d_hist;
+      e.d_ainv += (int64_t)s0 * e.coarse_N * e.coarse_N;
+      e.d_active += s0, e.d_iters += s0, e.d_conv += s0, e.d_ones += s0, e.d_r0 += s0;
+      e.d_hist += (int64_t)s0 * (e.cfg.max_iter + 1);
+      e.S = cnt;
+      e.s_base = s0;
+    }
+    ~RangeView() {
+      for (size_t l = 0; l < e.lv.size(); ++l) {
+        e.lv[l].u[0] = saved_lv[l][0], e.lv[l].u[1] = saved_lv[l][1], e.lv[l].b = saved_lv[l][2];
+        e.lv[l].coef = saved_coef[l], e.lv[l].elems = saved_elems[l];
+      }
+      e.d_ainv = ainv, e.d_active = act, e.d_iters = it, e.d_conv = cv, e.d_ones = ones, e.d_r0 = r0, e.d_hist = hist;
+      e.S = S0;
+      e.s_base = 0;
+    }
+  };
+
+  cudaStream_t copy_stream = nullptr;
+  int io_chunks = 0;  // 0 = automatic
+
+  // Host-buffer solve.  Large batches are pipelined over chunks of shifts: H2D of later chunks and D2H of
+  // earlier ones run on a copy stream while the current chunk solves (results are identical: every shift's
+  // solve is independent and its kernels see the same data).
   void solve_host(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) override {
     CK(cudaSetDevice(device));
     const size_t N = compact_elems(0);
+    const int64_t per = (int64_t)lv[0].m * lv[0].m;
     double2* st = stage(2 * N);
-    h2d(b, st, N);
-    solve_device(st, st + N, rep);
-    d2h(st + N, u, N);
-    CK(cudaStreamSynchronize(stream));
+    // automatic: three chunks of S/4, S/2, S/4 shifts.  Each chunk solve carries a fixed ~3 ms of
+    // coarse-level latency (C3 on B200: t(S) ~ 2.9 ms + 0.148 ms * S), so few chunks with short end
+    // chunks minimise exposed copy + overhead: 62 ms (4 equal) -> ~55 ms for C3 (serial: 78 ms).
+    const bool auto_split = io_chunks <= 0;
+    int nch = io_chunks > 0 ? io_chunks : (N * sizeof(double2) >= ((size_t)256 << 20) && S >= 8 ? 3 : 1);
+    nch = std::max(1, std::min(nch, S));
+    auto pinned = [](const void* p) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) return (cudaGetLastError(), false);
+      return a.type == cudaMemoryTypeHost;
+    };
+    if (nch > 1 && !(pinned(b) && pinned(u))) nch = 1;  // pageable copies are host-synchronous: no overlap
+    if (nch == 1) {
+      h2d(b, st, N);
+      solve_device(st, st + N, rep);
+      d2h(st + N, u, N);
+      CK(cudaStreamSynchronize(stream));
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> in(nch), done(nch);
+    for (int c = 0; c < nch; ++c) {
+      CK(cudaEventCreateWithFlags(&in[c], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming));
+    }
+    auto bound = [&](int c) {
+      if (auto_split && nch == 3) return c == 0 ? 0 : c == 1 ? S / 4 : c == 2 ? S - S / 4 : S;
+      return (int)((int64_t)S * c / nch);
+    };
+    auto range = [&](int c) { return std::make_pair(bound(c), bound(c + 1)); };
+    for (int c = 0; c < nch; ++c) {
+      const auto [s0, s1] = range(c);
+      CK(cudaMemcpyAsync(st + s0 * per, b + s0 * per, sizeof(double2) * per * (s1 - s0), cudaMemcpyHostToDevice,
+                         copy_stream));
+      CK(cudaEventRecord(in[c], copy_stream));
+    }
+    const int H = cfg.max_iter + 1;
+    double upd = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      const auto [s0, s1] = range(c);
+      CK(cudaStreamWaitEvent(stream, in[c], 0));
+      pdmg_solve_report rc{};
+      if (rep) {
+        rc.iterations = rep->iterations ? rep->iterations + s0 : nullptr;
+        rc.converged = rep->converged ? rep->converged + s0 : nullptr;
+        rc.residual_history = rep->residual_history ? rep->residual_history + (int64_t)s0 * H : nullptr;
+        rc.rate = rep->rate ? rep->rate + s0 : nullptr;
+      }
+      {
+        RangeView view(*this, s0, s1 - s0);
+        solve_device(st + s0 * per, st + N + s0 * per, rep ? &rc : nullptr);
+      }
+      upd += last_updates;
+      CK(cudaEventRecord(done[c], stream));
+      CK(cudaStreamWaitEvent(copy_stream, done[c], 0));
+      CK(cudaMemcpyAsync(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * (s1 - s0), cudaMemcpyDeviceToHost,
+                         copy_stream));
+    }
+    CK(cudaStreamSynchronize(copy_stream));
+    for (int c = 0; c < nch; ++c) cudaEventDestroy(in[c]), cudaEventDestroy(done[c]);
+    last_updates = upd;
+    if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
 
   void cycle_host(pdmg_c128* u, const pdmg_c128* b) override {

@@ -625,10 +625,13 @@ struct SolveState {
   int* n_active;     // scalar
   int S, max_iter;
   double tol;
+  int* parity;       // [max_iter+1]: which u buffer holds the iterate after cycle k (written by k_finalize)
+  int cur;
 };
 
 __global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k, SolveState st) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st.parity) st.parity[k] = st.cur;
   if (warp >= st.S) return;
   const int s = warp;
   if (st.active[s] == 0) return;
@@ -659,6 +662,13 @@ __global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k
   }
   st.active[s] = act;
   if (act) atomicAdd(st.n_active, 1);
+}
+
+// Device -> mapped pinned host words, written by SMs over PCIe: small result copies that never queue
+// behind bulk transfers on the copy engines (the chunked host solve keeps those busy).
+__global__ void k_copy_words(const uint32_t* __restrict__ src, volatile uint32_t* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // Per-shift norms (op-level pdmg_norm): sum partials -> sqrt.

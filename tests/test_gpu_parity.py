@@ -198,3 +198,40 @@ def test_singular_coarse_detected(path):
         assert H.coarse_singular(0)
         with pytest.raises(P.SingularOperatorError, match="singular on grid n = 8"):
             H.solve(P.random_rhs(16, 3).reshape(1, 15, 15))
+
+
+@pytest.mark.parametrize("path", ["small", "batched"])
+@pytest.mark.parametrize("chunks", [2, 3, 7])
+def test_chunked_host_solve_matches(oracle, monkeypatch, chunks, path):
+    """pdmg_solve on pinned host buffers pipelines the batch over chunks of shifts (copies overlap the
+    solve); every shift's result and report must be bitwise those of the one-chunk path."""
+    import ctypes
+
+    from paper_2203_11154_b200 import _native as N
+
+    n, S = 64, 7
+    lams = [8.959263353215057 - 15.395328029306036j + 3j * k for k in range(S)]
+    cfg = P.MultigridConfig(coarsest_n=4, tol=1e-10, max_iter=60)
+    b = P.random_rhs(n, 5, count=S)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        H.set_solve_path(path)
+        u_ref, reps_ref = H.solve(b)  # pageable numpy buffers: one chunk
+    monkeypatch.setenv("PDMG_IO_CHUNKS", str(chunks))
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        H.set_solve_path(path)
+        nbytes = b.nbytes
+        hb, hu = N.lib().pdmg_host_alloc(nbytes), N.lib().pdmg_host_alloc(nbytes)
+        try:
+            ctypes.memmove(hb, b.ctypes.data, nbytes)
+            rep, it, cv, hist, rate = H._report_bufs()
+            assert N.lib().pdmg_solve(H._h, hb, hu, ctypes.byref(rep)) == 0, N.lib().pdmg_last_error()
+            u = np.empty_like(b)
+            ctypes.memmove(u.ctypes.data, hu, nbytes)
+            reps = H._reports(rep, it, cv, hist, rate)
+        finally:
+            N.lib().pdmg_host_free(hb)
+            N.lib().pdmg_host_free(hu)
+    assert np.array_equal(u, u_ref)
+    for r, q in zip(reps, reps_ref):
+        assert r.iterations == q.iterations and r.converged == q.converged
+        assert list(r.residual_history) == list(q.residual_history)
