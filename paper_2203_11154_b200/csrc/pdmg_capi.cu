@@ -305,6 +305,40 @@ struct MarchTable {
   }
 };
 
+// two-sweep fused Vanka passes (k_march2): key = loadu | prolong << 1 | post << 2
+template <class T>
+struct March2Table {
+  void (*e[32])(MarchArgs<T>) = {};
+  static int key(bool lu, bool pr, int post, bool nin = false) {
+    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0);
+  }
+  size_t smem[32] = {};
+  template <bool LU, bool PR, int PO, bool NI = false>
+  void reg() {
+    e[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI>;
+    smem[key(LU, PR, PO, NI)] = march2_smem<T>(LU);
+    if (march2_smem<T>(LU) > 0)
+      CK(cudaFuncSetAttribute(&k_march2<T, LU, PR, PO, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)march2_smem<T>(LU)));
+  }
+  March2Table() {
+    reg<false, false, POST_NONE>();
+    reg<true, false, POST_NONE>();
+    reg<false, false, POST_RESTRICT>();
+    reg<true, false, POST_RESTRICT>();
+    reg<false, false, POST_NORM>();
+    reg<true, false, POST_NORM>();
+    reg<false, true, POST_NONE>();
+    reg<true, true, POST_NONE>();
+    reg<false, true, POST_NORM>();
+    reg<true, true, POST_NORM>();
+    reg<false, false, POST_RESTRICT, true>();
+    reg<true, false, POST_RESTRICT, true>();
+    reg<false, false, POST_NONE, true>();
+    reg<true, false, POST_NONE, true>();
+  }
+};
+
 // ---------------------------------------------------------------------------------------------
 // Engine: one batch of shifts on one device.
 // ---------------------------------------------------------------------------------------------
@@ -400,6 +434,48 @@ struct Engine : EngineBase {
     static MarchTable<T> t;
     return t;
   }
+  static const March2Table<T>& marches2() {
+    static March2Table<T> t;
+    return t;
+  }
+  int march2_min_n = 64;  // levels with n >= this run Vanka sweep pairs as one k_march2 pass (0 = never)
+  int march2_hs = 0;      // strip height override (0 = automatic)
+  bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
+  bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
+  int nin_k = -1;         // cycle_level: the first fine pass computes the norm of iterate nin_k (>= 0)
+  bool use_norm_next() const {
+    return norm_next && march2_pre && use_march2(0) && cfg.nu1 >= 2 && cfg.nu1 % 2 == 0;
+  }
+  bool use_march2(int l) const {
+    return march2_min_n > 0 && lv[l].n >= march2_min_n && cfg.smoother == PDMG_SMOOTHER_VANKA;
+  }
+  // two consecutive Vanka sweeps u[cur] -> u[cur^1] (+ prolongation of ec before, + restriction/norm after)
+  void level_pass2(int l, bool loadu, bool prolong, int post, const V* uin, V* uout, const V* b, const V* ec, V* bc,
+                   const int* active, int n_act, bool norm_in = false) {
+    const Level& Lv = lv[l];
+    MarchArgs<T> ma{};
+    ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
+    ma.coef = Lv.coef, ma.active = active, ma.n = Lv.n;
+    ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
+    ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
+    const int hA = (4 + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;  // = k_march2 hA
+    const int wout = 64 - 2 * hA;
+    ma.Hs = march2_hs > 0 ? march2_hs : (Lv.n >= 512 ? 128 : 64);
+    ma.ntx = (Lv.n + wout - 1) / wout;
+    ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
+    const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
+    auto fn = marches2().e[key2];
+    const size_t smem2 = marches2().smem[key2];
+    if (!fn) throw std::logic_error("pdmg_b200: no two-sweep kernel for this variant");
+    const double S_ = sizeof(V), pts = (double)n_act * Lv.m * Lv.m;
+    const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0);
+    std::string cls = "L" + std::to_string(l) + ":" + (prolong ? (loadu ? "prolong+" : "prolong0+") : (loadu ? "" : "zero+")) +
+                      "vanka2" + (post == POST_NORM ? "+norm" : post == POST_RESTRICT ? "+restrict" : "") +
+                      (norm_in ? "+norm_in" : "");
+    dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
+    timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, smem2, stream>>>(ma); });
+    last_partials = ma.ntasks;
+  }
   // measured on B200 (C3, C4): the marcher wins for sweep+norm and sweep+restrict, the ring
   // kernel for the plain and prolongating sweeps; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher
   bool march_all = false;
@@ -490,6 +566,12 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_LEVEL_H_MIN_N")) level_h_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_TAIL_MAX_N")) tail_max_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH2_MIN_N")) march2_min_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH2_HS")) march2_hs = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH2_PRE")) march2_pre = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_MARCH2_POST")) march2_post = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_NORM_NEXT")) norm_next = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
@@ -697,6 +779,14 @@ struct Engine : EngineBase {
       if (lv[l].n <= tail_max_n) return l;
     return -1;
   }
+  // Block size of the one-CTA-per-shift kernels (64 registers/thread: 1024 threads fill an SM's register
+  // file).  Smaller blocks once S exceeds the SM count keep every shift resident in a single wave.
+  int small_threads_env = 0;
+  int small_threads() const {
+    if (small_threads_env > 0) return small_threads_env;
+    int sms = 148;
+    return S <= sms ? SMALL_THREADS : S <= 2 * sms ? SMALL_THREADS / 2 : SMALL_THREADS / 4;
+  }
   void tail_cycle(int l, const int* active, bool zero) {
     SmallArgs<T> sa{};
     for (size_t q = l; q < lv.size(); ++q)
@@ -706,7 +796,7 @@ struct Engine : EngineBase {
     sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
     sa.ainv = d_ainv, sa.coarse_N = coarse_N, sa.active = active, sa.tail_zero = zero ? 1 : 0;
     timed("coarse_tail", 0.0,
-          [&] { k_small_cycle<T><<<S, SMALL_THREADS, coarse_N * sizeof(double2), stream>>>(sa); });
+          [&] { k_small_cycle<T><<<S, small_threads(), coarse_N * sizeof(double2), stream>>>(sa); });
     for (size_t q = l; q < lv.size(); ++q) lv[q].cur = 0, lv[q].uzero = false;
   }
 
@@ -725,8 +815,22 @@ struct Engine : EngineBase {
     }
     Level& Lc = lv[l + 1];
     if (zero) Lv.uzero = true;
+    const bool pair = use_march2(l) && march2_pre;
     for (int k = 0; k < cfg.nu1; ++k) {
       const bool last = k == cfg.nu1 - 1;
+      if (pair && (cfg.nu1 - k) % 2 == 0) {  // sweeps k, k+1 as one pass (the pairs end at the last sweep)
+        const bool nin = l == 0 && k == 0 && nin_k >= 0;
+        level_pass2(l, !Lv.uzero, false, k + 2 == cfg.nu1 ? POST_RESTRICT : POST_NONE, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1],
+                    Lv.b, nullptr, Lc.b, active, n_act, nin);
+        if (nin) {  // convergence bookkeeping of the previous iterate (still in u[cur]) before the rest runs
+          finalize(nin_k, last_partials, false, Lv.cur);
+          nin_k = -1;
+        }
+        Lv.cur ^= 1;
+        Lv.uzero = false;
+        ++k;
+        continue;
+      }
       Variant v{!Lv.uzero, false, true, last ? POST_RESTRICT : POST_NONE, true, jac};
       level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, nullptr, Lc.b, active, n_act);
       Lv.cur ^= 1;
@@ -743,6 +847,16 @@ struct Engine : EngineBase {
     if (cfg.nu2 > 0) {
       for (int k = 0; k < cfg.nu2; ++k) {
         const bool last = k == cfg.nu2 - 1;
+        if (use_march2(l) && march2_post && k + 1 < cfg.nu2) {  // sweeps k, k+1 as one pass (pairs from the first, prolongating, sweep)
+          const int post2 = (k + 2 == cfg.nu2 && want_norm) ? POST_NORM : POST_NONE;
+          level_pass2(l, k == 0 ? !Lv.uzero : true, k == 0, post2, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b,
+                      k == 0 ? ec : nullptr, nullptr, active, n_act);
+          Lv.cur ^= 1;
+          Lv.uzero = false;
+          normed = post2 == POST_NORM;
+          ++k;
+          continue;
+        }
         const int post = (last && want_norm) ? POST_NORM : POST_NONE;
         Variant v{k == 0 ? !Lv.uzero : true, k == 0, true, post, true, jac};
         level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, k == 0 ? ec : nullptr, nullptr, active, n_act);
@@ -831,10 +945,33 @@ struct Engine : EngineBase {
       const double per_shift_bytes = 0.0;
       (void)per_shift_bytes;
       timed("small_solve", 0.0, [&] {
-        k_small_solve<T><<<S, SMALL_THREADS, coarse_N * sizeof(double2), stream>>>(sa);
+        k_small_solve<T><<<S, small_threads(), coarse_N * sizeof(double2), stream>>>(sa);
       });
       CK(cudaGetLastError());
       CK(cudaMemsetAsync(d_parity, 0, sizeof(int) * H, stream));
+      pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+      finish_report(rep, t0, H);
+      return;
+    }
+    if (use_norm_next() && !any_singular) {
+      // The residual norm of iterate k-1 (multigrid.cpp:91, 96-105) is the first fine sweep's residual in
+      // cycle k: that pass leaves its partials, k_finalize(k-1) runs right after it (freezing converged
+      // shifts, whose iterate stays in the other buffer) and the rest of cycle k runs for the active ones.
+      // The host reads count(k-1) once cycle k is enqueued, so it enqueues cycle k+1 while the GPU is
+      // still in cycle k.  After max_iter cycles one norm pass closes the history.
+      int n_act = S, k = 1;
+      for (; k <= cfg.max_iter; ++k) {
+        nin_k = k - 1;
+        const bool normed = cycle_level(0, k == 1, d_active, n_act, false);
+        (void)normed;
+        n_act = read_nactive(k - 1);
+        if (n_act == 0) break;
+      }
+      if (k > cfg.max_iter) {
+        level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr,
+                   nullptr, d_active, n_act);
+        finalize(cfg.max_iter, last_partials, true, F.cur);
+      }
       pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
       finish_report(rep, t0, H);
       return;

@@ -113,6 +113,19 @@ __device__ __forceinline__ double2 cdot3(double2 k0, double2 rc, double2 k1, dou
   return make_double2(x, y);
 }
 
+// k0 x + k1 y (complex), one FMA chain per component
+__device__ __forceinline__ double2 cmad2(double2 k0, double2 x, double2 k1, double2 y) {
+  double re = k0.x * x.x;
+  re = fma(-k0.y, x.y, re);
+  re = fma(k1.x, y.x, re);
+  re = fma(-k1.y, y.y, re);
+  double im = k0.x * x.y;
+  im = fma(k0.y, x.x, im);
+  im = fma(k1.x, y.y, im);
+  im = fma(k1.y, y.x, im);
+  return make_double2(re, im);
+}
+
 // Per (level, shift) operator coefficients, precomputed on the host in fp64 (multigrid.cpp:47-58).
 struct LevelCoef {
   double2 d;      // 4 + eta, eta = lambda h^2              (grid.cpp:73)
@@ -1405,6 +1418,393 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
     }
   }
   if constexpr (POST == POST_NORM) {
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+    if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
+  }
+}
+
+// ===================================================================================================
+// k_march2: TWO fused Vanka sweeps per pass (temporal blocking) for the large levels.  A V(nu1, nu2) cycle
+// with nu >= 2 runs its last two pre-sweeps (+ residual + restriction) and its first two post-sweeps
+// (prolongation + sweeps [+ norm]) as one pass each, so the fine level is streamed twice per cycle instead
+// of four times.  Every point gets exactly the arithmetic of two consecutive single sweeps (the second
+// sweep's residual is b - L u1 of the first sweep's stored iterate, fp32-rounded for complex64); only the
+// halo (hA = 4 + hC columns/rows per side) is computed redundantly by neighbouring strips.
+// The Vanka correction delta_t = k0 r_t + k1 (s_t + r_{t-1} + r_{t+1}) + k2 (s_{t-1} + s_{t+1}), s = the
+// horizontal neighbour sum of r, is accumulated row by row: c_t = k1 r_t + k2 s_t, d_t = k0 r_t + k1 s_t,
+// delta_t = c_{t-1} + d_t + c_{t+1}, so a sweep keeps 2 complex per column in registers instead of 6.
+// Stage lags at step j: load u0 row j; r at j-1 -> delta1/u1 at j-2; r' at j-3 -> delta2/u2 at j-4 (stored);
+// r2 = b - L u2 at j-5 -> restriction or norm.  b rows j-3 and j-5 are re-read (L1 hits).
+// The row loop is unrolled by 3 with the 3-row windows addressed as rings (no register rotation), and
+// steps whose rows and columns are all interior run a copy without Dirichlet masking.
+// Input rows (u_in and b, 64 columns) reach shared memory by TMA bulk copies issued M2_D rows ahead into a
+// per-warp ring of M2_NS slots (one mbarrier each): M2_D rows of both arrays in flight per warp keep
+// enough bytes moving to saturate HBM at 8 warps/SM, without spending registers on prefetch.  b rows stay
+// in the ring until the second sweep (row j-3) and the post-residual (row j-5) have read them.
+// ===================================================================================================
+template <int X>
+struct IC {
+  static constexpr int value = X;
+};
+#ifndef PDMG_MARCH2_MINB
+#define PDMG_MARCH2_MINB 2
+#endif
+#ifndef PDMG_MARCH2_D
+#define PDMG_MARCH2_D 4
+#endif
+#ifndef PDMG_MARCH2_TMA
+#define PDMG_MARCH2_TMA 0
+#endif
+constexpr bool M2_TMA = PDMG_MARCH2_TMA;  // input rows via the TMA ring (1) or register prefetch (0)
+constexpr int M2_D = PDMG_MARCH2_D;  // rows in flight per warp
+constexpr int M2_NS = M2_D + 6;      // ring slots: rows j-5 .. j+D
+constexpr int M2_ROWW = 68;          // ring row width (64 columns + even-alignment slack for 8-byte elements)
+template <class T>
+constexpr size_t march2_smem(bool loadu) {
+  if (!M2_TMA) return 0;
+  return (size_t)MARCH_WARPS * M2_NS * 8 + (size_t)MARCH_WARPS * M2_NS * M2_ROWW * sizeof(typename vec2<T>::type) *
+                                               (loadu ? 2 : 1);
+}
+// NORM_IN: also leave the partial sums of ||b - L u_in||^2 (the first sweep's residual, i.e. the residual of
+// the previous cycle's iterate) in a.partial -- the fine-level convergence norm, read one pass later.
+template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false>
+__global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(MarchArgs<T> a) {
+  using V = typename vec2<T>::type;
+  using D2 = double2;
+  constexpr int LC = 2;
+  constexpr bool EVEN = sizeof(V) == 8;
+  constexpr bool HASD = POST != POST_NONE;
+  constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
+  constexpr int hC = HASD ? hD + 1 : 0;
+  constexpr int hA = (hC + 5) & ~1;  // rounded up to even: strips start at even columns
+  constexpr int WOUT = 32 * LC - 2 * hA;
+  const int shift = blockIdx.y;
+  if (a.active != nullptr && a.active[shift] == 0) return;
+  const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
+  if (task >= a.ntasks) return;
+  const int lane = threadIdx.x & 31;
+  const int tx = task % a.ntx, ty = task / a.ntx;
+  const int n = a.n, m = n - 1, Hs = a.Hs, nc = a.nc;
+  const int x0 = tx * WOUT, r0 = ty * Hs;
+  const int64_t sbase = (int64_t)shift * a.ss;
+  const int cA = x0 - hA + LC * lane;
+  V* __restrict__ uout = a.u_out + sbase + cA;  // per-lane column pointer (row 0)
+  // ---- TMA ring: slot q holds u_in row r and b row r for r = rlo + q (mod M2_NS) ----------------------
+  extern __shared__ __align__(128) unsigned char m2_smem[];
+  const int wid = threadIdx.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(m2_smem) + wid * M2_NS;
+  V* ring_b = reinterpret_cast<V*>(m2_smem + MARCH_WARPS * M2_NS * 8) + (size_t)wid * M2_NS * M2_ROWW * (LOADU ? 2 : 1);
+  V* ring_u = ring_b + M2_NS * M2_ROWW;  // LOADU only
+  const int cs = (x0 - hA) & (EVEN ? ~1 : ~0);  // first ring column (even for 8-byte elements)
+  const int lofs = (x0 - hA) - cs + LC * lane;  // this lane's first column within a ring row
+  const int c_lo = max(cs, 0), c_hi = min(cs + M2_ROWW, n);
+  const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
+  const LevelCoef cf = a.coef[shift];
+
+  bool cin[LC], cst[LC];
+#pragma unroll
+  for (int k = 0; k < LC; ++k) {
+    const int c = cA + k;
+    cin[k] = (unsigned)(c - 1) < (unsigned)m;
+    cst[k] = cin[k] && c >= x0 && c < x0 + WOUT;
+  }
+  const int rlo = r0 - hA, rhi = r0 + Hs + hA;
+  const int olo = max(r0, 1), ohi = min(r0 + Hs, m + 1);
+  auto row_in = [&](int row) __attribute__((always_inline)) { return (unsigned)(row - 1) < (unsigned)m; };
+  // rows before rlo are never loaded: they read as zero (they only reach halo rows, which are not stored)
+  auto row_ok = [&](int row) __attribute__((always_inline)) { return row_in(row) && row >= rlo; };
+  const V* __restrict__ uin = a.u_in + sbase + cA;  // register-prefetch path: per-lane column pointers
+  const V* __restrict__ bb = a.b + sbase + cA;
+  if (M2_TMA && lane == 0) {
+    for (int q = 0; q < M2_NS; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  // ring slot of row rlo + i is i mod M2_NS; qj = slot of the current row j, pj = its mbarrier phase
+  int qj = 0, pj = 0;
+  auto wrap = [&](int q) __attribute__((always_inline)) { return q >= M2_NS ? q - M2_NS : (q < 0 ? q + M2_NS : q); };
+  auto issue_q = [&](int row, int q) __attribute__((always_inline)) {  // lane 0: TMA of u_in and b row into slot q
+    if (lane != 0) return;
+    const bool ok = row_in(row) && c_hi > c_lo;
+    const unsigned bytes = ok ? (unsigned)((c_hi - c_lo) * sizeof(V)) : 0u;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_arrive_expect_tx(&bars[q], LOADU ? 2 * bytes : bytes);
+    if (ok) {
+      const int64_t g = sbase + (int64_t)row * n + c_lo;
+      tma_load_1d(ring_b + q * M2_ROWW + (c_lo - cs), a.b + g, bytes, &bars[q]);
+      if constexpr (LOADU) tma_load_1d(ring_u + q * M2_ROWW + (c_lo - cs), a.u_in + g, bytes, &bars[q]);
+    }
+  };
+  // ring element of row j - back (back = 0, 1, 3, 5: slots relative to qj)
+  auto ring_at = [&](const V* ring, int back, int k) __attribute__((always_inline)) {
+    return ld2(ring[wrap(qj - back) * M2_ROWW + lofs + k]);
+  };
+  // warp-uniform: every column of the strip (and its coarse prolongation columns) is interior
+  const bool col_int = (x0 - hA >= 1) && (x0 - hA + 32 * LC + 1 <= m - 1);
+  // steps j in [jlo_int, jhi_int] touch only interior rows (loads j-5 .. j+1, coarse rows up to (j+1)/2+1)
+  const int jlo_int = max(6, rlo + 5), jhi_int = m - 3;  // (register path: loads reach j+1 and j-4)
+
+  // prolongation window: coarse rows J, J+1 (in use) and J+2 (prefetched) at this lane's coarse column Ie;
+  // the column Ie+1 comes from the next lane (lane 31 loads it itself)
+  D2 Eo0 = cz<D2>(), Eo1 = cz<D2>(), Eo2 = cz<D2>(), Ex0 = cz<D2>(), Ex1 = cz<D2>(), Ex2 = cz<D2>();
+  int wJ = -1000;
+  const int Ie = cA >> 1;
+  const bool codd = (cA & 1) != 0;  // warp-uniform (strips start at x0 - hA, lanes step by 2)
+  auto load_crow = [&](int J, D2& o, D2& x, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+#ifdef PDMG_DBG_NOPROLOAD
+    o = make_double2((double)J, (double)Ie);
+    x = o;
+#else
+    const bool jok = (unsigned)J <= (unsigned)nc;
+    if constexpr (MASK)
+      o = (jok && (unsigned)Ie <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie]) : cz<D2>();
+    else
+      o = ld2(ecs[(int64_t)J * nc + Ie]);
+    if (lane == 31) x = (jok && (unsigned)(Ie + 1) <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie + 1]) : cz<D2>();
+#endif
+  };
+  // u_in row `row` (ring) and the prolongation of e_c onto fine row `row` (register window E0/E1, rows
+  // visited in increasing order; computed a step ahead so the coarse loads are not waited on)
+  auto read_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+#pragma unroll
+    for (int k = 0; k < LC; ++k) {
+      out[k] = cz<D2>();
+      if constexpr (LOADU) {
+        if (!MASK || (row_ok(row) && cin[k])) out[k] = ring_at(ring_u, 0, k);
+      }
+    }
+  };
+  auto gread_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+#pragma unroll
+    for (int k = 0; k < LC; ++k) {
+      out[k] = cz<D2>();
+      if constexpr (LOADU) {
+        if (!MASK || (row_ok(row) && cin[k])) out[k] = ld2(uin[(int64_t)row * n + k]);
+      }
+    }
+  };
+  auto gload_b = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+#pragma unroll
+    for (int k = 0; k < LC; ++k) {
+      if constexpr (MASK)
+        out[k] = (row_ok(row) && cin[k]) ? ld2(bb[(int64_t)row * n + k]) : cz<D2>();
+      else
+        out[k] = ld2(bb[(int64_t)row * n + k]);
+    }
+  };
+  auto prolong_row = [&](int row, D2* pout, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+    const int J = row >> 1;
+    if (J == wJ + 1) {
+      Eo0 = Eo1, Eo1 = Eo2, Ex0 = Ex1, Ex1 = Ex2;
+      load_crow(J + 2, Eo2, Ex2, MK);
+      wJ = J;
+    } else if (J != wJ) {
+      load_crow(J, Eo0, Ex0, IC<1>{});
+      load_crow(J + 1, Eo1, Ex1, IC<1>{});
+      load_crow(J + 2, Eo2, Ex2, IC<1>{});
+      wJ = J;
+    }
+    const D2 a0 = Eo0, b0 = Eo1;
+    D2 a1 = shfl_dn2(Eo0), b1 = shfl_dn2(Eo1);
+    if (lane == 31) a1 = Ex0, b1 = Ex1;
+    const bool rin = !MASK || row_ok(row);
+    // prolong_bilinear (grid.cpp:123-153): even/odd fine column and row (both warp-uniform)
+    D2 p[LC];
+    if (row & 1) {
+      const D2 q4 = cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1));
+      p[0] = codd ? q4 : cscale(0.5, cadd(a0, b0));
+      p[1] = codd ? cscale(0.5, cadd(a1, b1)) : q4;
+    } else {
+      const D2 q2 = cscale(0.5, cadd(a0, a1));
+      p[0] = codd ? q2 : a0;
+      p[1] = codd ? a1 : q2;
+    }
+#pragma unroll
+    for (int k = 0; k < LC; ++k) pout[k] = MASK ? csel(rin && cin[k], p[k]) : p[k];
+  };
+  auto west = [&](const D2* x, int k, const D2& wl) __attribute__((always_inline)) { return k == 0 ? wl : x[k - 1]; };
+  auto east = [&](const D2* x, int k, const D2& er) __attribute__((always_inline)) { return k == LC - 1 ? er : x[k + 1]; };
+  // residual b - L u at the centre row c of a window (rows above/below: lo, hi), masked to the domain
+  auto resid = [&](const D2* lo, const D2* c, const D2* hi, const D2* bw, bool inside, D2* r, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+    const D2 wl = shfl_up2(c[LC - 1]), er = shfl_dn2(c[0]);
+#pragma unroll
+    for (int k = 0; k < LC; ++k) {
+      const D2 v = res5(bw[k], cf.inv_h2, cf.dd, c[k], west(c, k, wl), east(c, k, er), lo[k], hi[k]);
+      r[k] = MASK ? csel(inside && cin[k], v) : v;
+    }
+  };
+  // one Vanka sweep's row update: r_t arrives, delta_{t-1} leaves (masked to the domain at row t-1)
+  auto vanka_row = [&](const D2* r, D2* P, D2* C, bool din, D2* dl, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+    const D2 rwl = shfl_up2(r[LC - 1]), rer = shfl_dn2(r[0]);
+#pragma unroll
+    for (int k = 0; k < LC; ++k) {
+      const D2 s = cadd(west(r, k, rwl), east(r, k, rer));
+      const D2 c = cmad2(cf.k1, r[k], cf.k2, s);
+      const D2 d = cmad2(cf.k0, r[k], cf.k1, s);
+      const D2 v = cadd(P[k], c);
+      dl[k] = MASK ? csel(din && cin[k], v) : v;
+      P[k] = cadd(C[k], d);
+      C[k] = c;
+    }
+  };
+
+  D2 U0[3][LC], U1[3][LC], U2[3][LC];
+  D2 P1[LC], C1[LC], P2[LC], C2[LC], Vp[LC];
+  D2 Pn[LC], Unx[LC], Bn[LC], B3n[LC], B5n[LC];  // (the last four: register-prefetch path only)
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int k = 0; k < LC; ++k) U0[q][k] = U1[q][k] = U2[q][k] = cz<D2>();
+#pragma unroll
+  for (int k = 0; k < LC; ++k) P1[k] = C1[k] = P2[k] = C2[k] = Vp[k] = cz<D2>();
+  double nacc = 0.0;
+  if constexpr (M2_TMA) {
+    for (int r = rlo; r < min(rlo + M2_D, rhi); ++r) issue_q(r, r - rlo);
+  } else {
+    gread_u(rlo, Unx, IC<1>{});
+    gload_b(rlo - 1, Bn, IC<1>{});
+    gload_b(rlo - 3, B3n, IC<1>{});
+    if constexpr (HASD) gload_b(rlo - 5, B5n, IC<1>{});
+  }
+  if constexpr (PROLONG) prolong_row(rlo, Pn, IC<1>{});
+
+  // one step at row j; window slot of (oldest, middle, newest) row = ((PH + 0, 1, 2) % 3)
+  auto step = [&](int j, auto PH, auto MK) __attribute__((always_inline)) {
+    constexpr int ph = decltype(PH)::value;
+    constexpr int so = ph % 3, sm = (ph + 1) % 3, sn = (ph + 2) % 3;
+    // ---- loads: u0 row j (prefetched last step), prefetch u0 row j+1 and b row j; b rows j-3, j-5 ----
+    D2 B3[LC], B5[LC], Bc[LC], Un[LC];
+    if constexpr (M2_TMA) {
+      __syncwarp();  // every lane is done with the slot row j + D - M2_NS last held (read at step j-1)
+      if (j + M2_D < rhi) issue_q(j + M2_D, wrap(qj + M2_D));
+      mbar_wait(&bars[qj], pj);
+      load_b(j, 1, Bc, MK);
+      load_b(j, 3, B3, MK);
+      if constexpr (HASD) load_b(j, 5, B5, MK);
+      read_u(j, Un, MK);
+#pragma unroll
+      for (int k = 0; k < LC; ++k)
+        if constexpr (PROLONG) Un[k] = cadd(Un[k], Pn[k]);
+      if constexpr (PROLONG) {
+        if (j + 1 < rhi) prolong_row(j + 1, Pn, MK);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < LC; ++k) {
+        Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
+        Bc[k] = Bn[k];
+        B3[k] = B3n[k];
+        if constexpr (HASD) B5[k] = B5n[k];
+      }
+      if (j + 1 < rhi) {
+        gread_u(j + 1, Unx, MK);
+        if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
+        gload_b(j, Bn, MK);
+        gload_b(j - 2, B3n, MK);
+        if constexpr (HASD) gload_b(j - 4, B5n, MK);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < LC; ++k) U0[sn][k] = Un[k];
+    // ---- sweep 1: r at j-1, delta1 / u1 at j-2 ------------------------------------------------------
+    {
+      D2 r[LC], dl[LC];
+      resid(U0[so], U0[sm], U0[sn], Bc, row_in(j - 1), r, MK);
+      if constexpr (NORM_IN) {
+        if (j - 1 >= olo && j - 1 < ohi) {
+#pragma unroll
+          for (int k = 0; k < LC; ++k)
+            if (cst[k]) nacc += r[k].x * r[k].x + r[k].y * r[k].y;
+        }
+      }
+      vanka_row(r, P1, C1, row_in(j - 2), dl, MK);
+#pragma unroll
+      for (int k = 0; k < LC; ++k) {
+        D2 u1 = cadd(U0[so][k], dl[k]);
+        if constexpr (EVEN) u1 = ld2(st2<V>(u1));  // the iterate the unfused sweep would have stored
+        U1[sn][k] = u1;
+      }
+    }
+    // ---- sweep 2: r' = b - L u1 at j-3, delta2 / u2 at j-4 (stored) ----------------------------------
+    {
+      D2 r[LC], dl[LC];
+      resid(U1[so], U1[sm], U1[sn], B3, row_in(j - 3), r, MK);
+      const int row = j - 4;
+      vanka_row(r, P2, C2, row_in(row), dl, MK);
+      const bool rst = row >= olo && row < ohi;
+#pragma unroll
+      for (int k = 0; k < LC; ++k) {
+        const V us = st2<V>(cadd(U1[so][k], dl[k]));
+        if (rst && cst[k]) uout[(int64_t)row * n + k] = us;
+        U2[sn][k] = ld2(us);
+      }
+    }
+    if constexpr (HASD) {
+      // ---- r2 = b - L u2 at j-5: norm or restriction (grid.cpp:102-121) ------------------------------
+      const int row = j - 5;
+      D2 r2[LC];
+      resid(U2[so], U2[sm], U2[sn], B5, row_in(row), r2, MK);
+      if constexpr (POST == POST_NORM) {
+        if (row >= olo && row < ohi) {
+#pragma unroll
+          for (int k = 0; k < LC; ++k)
+            if (cst[k]) nacc += r2[k].x * r2[k].x + r2[k].y * r2[k].y;
+        }
+      }
+      if constexpr (POST == POST_RESTRICT) {
+        if (row & 1) {
+          D2 v[LC];
+#pragma unroll
+          for (int k = 0; k < LC; ++k) {
+            v[k] = cadd(Vp[k], r2[k]);
+            Vp[k] = r2[k];
+          }
+          const int J = (row - 1) >> 1;
+          if (row >= r0 + 1 && row <= r0 + Hs && J >= 1 && J <= nc - 1) {
+            const D2 vwl = shfl_up2(v[LC - 1]), ver = shfl_dn2(v[0]);
+#pragma unroll
+            for (int k = 0; k < LC; ++k) {
+              const int c = cA + k;
+              if (!(c & 1) && c >= x0 && c < x0 + WOUT) {
+                const int I = c >> 1;
+                if (I >= 1 && I <= nc - 1) {
+                  const D2 s = cadd(cadd(west(v, k, vwl), cscale(2.0, v[k])), east(v, k, ver));
+                  a.bc[(int64_t)shift * a.ssc + (int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, s));
+                }
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < LC; ++k) Vp[k] = cadd(Vp[k], cscale(2.0, r2[k]));
+        }
+      }
+    }
+  };
+#ifndef PDMG_MARCH2_SPLIT
+#define PDMG_MARCH2_SPLIT 1
+#endif
+  auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
+    if (PDMG_MARCH2_SPLIT && col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
+    else step(j, PH, IC<1>{});
+    if (++qj == M2_NS) qj = 0, pj ^= 1;
+  };
+  int j = rlo;
+  for (; j + 2 < rhi; j += 3) {
+    step_any(j, IC<0>{});
+    step_any(j + 1, IC<1>{});
+    step_any(j + 2, IC<2>{});
+  }
+  if (j < rhi) step_any(j, IC<0>{});
+  if (j + 1 < rhi) step_any(j + 1, IC<1>{});
+  if constexpr (POST == POST_NORM || NORM_IN) {
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
     if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
   }

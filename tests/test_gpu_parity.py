@@ -74,8 +74,8 @@ def test_coarse_solve_parity(oracle):
 
 
 @pytest.mark.parametrize("cyc", [Cfg(), Cfg(cycle="W", nu1=1, nu2=0, coarsest_n=8, tol=1e-8),
-                                 Cfg(nu1=2, nu2=2), Cfg(nu1=0, nu2=2), Cfg(nu1=2, nu2=0),
-                                 Cfg(smoother="jacobi", omega=0.8)])
+                                 Cfg(nu1=2, nu2=2), Cfg(nu1=0, nu2=2), Cfg(nu1=2, nu2=0), Cfg(nu1=3, nu2=3),
+                                 Cfg(nu1=4, nu2=5, cycle="W"), Cfg(smoother="jacobi", omega=0.8)])
 def test_one_cycle_parity(oracle, cyc):
     n = 64
     m = n - 1
@@ -128,6 +128,7 @@ def test_config2_batch32(oracle, path):
 
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("cyc", [Cfg(nu1=0, nu2=2), Cfg(nu1=2, nu2=0), Cfg(nu1=2, nu2=1, cycle="W"),
+                                 Cfg(nu1=3, nu2=3), Cfg(nu1=4, nu2=2, cycle="W"),
                                  Cfg(smoother="jacobi", omega=0.8, tol=1e-8)])
 def test_cycle_variants_solve(oracle, path, cyc):
     lams = oracle.circulant_shifts(0.01, 32, 1 / 32)[:3]
@@ -152,6 +153,17 @@ def test_config3_subset(oracle):
     lams = oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, 256)[[0, 1, 128, 255]]
     b = oracle.random_complex(2, 4 * m * m).reshape(4, m, m)
     _check_solve(oracle, n, lams, b, Cfg(nu1=2, nu2=2))
+
+
+@pytest.mark.parametrize("cyc", [Cfg(nu1=2, nu2=2), Cfg(nu1=2, nu2=2, cycle="W"), Cfg(nu1=3, nu2=4)])
+def test_two_sweep_passes_ragged(oracle, cyc):
+    """Levels n >= 64 run Vanka sweep pairs as one fused pass (k_march2): a non-power-of-two fine grid
+    (n = 200: ragged strips at every level down to 50) on the batched path, against the oracle."""
+    n, m = 200, 199
+    lams = [0.0, 8.959263353215057 - 15.395328029306036j, 300 - 40j]
+    b = oracle.random_complex(31, 3 * m * m).reshape(3, m, m)
+    cfg = Cfg(nu1=cyc.nu1, nu2=cyc.nu2, cycle=cyc.cycle, coarsest_n=25)
+    _check_solve(oracle, n, lams, b, cfg, path="batched")
 
 
 @pytest.mark.parametrize("path", PATHS)
