@@ -441,6 +441,7 @@ struct Engine : EngineBase {
   int march2_min_n = 64;  // levels with n >= this run Vanka sweep pairs as one k_march2 pass (0 = never)
   int march2_hs = 0;      // strip height override (0 = automatic)
   bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
+  int march2_loopb_min_n = 512;
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
   int nin_k = -1;         // cycle_level: the first fine pass computes the norm of iterate nin_k (>= 0)
   bool use_norm_next() const {
@@ -461,6 +462,7 @@ struct Engine : EngineBase {
     const int hA = (4 + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;  // = k_march2 hA
     const int wout = 64 - 2 * hA;
     ma.Hs = march2_hs > 0 ? march2_hs : (Lv.n >= 512 ? 128 : 64);
+    ma.loop_a = Lv.n < march2_loopb_min_n;  // measured: the split loop wins on the 512+ grids only
     ma.ntx = (Lv.n + wout - 1) / wout;
     ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
     const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
@@ -572,6 +574,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH2_PRE")) march2_pre = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH2_POST")) march2_post = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_NORM_NEXT")) norm_next = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_MARCH2_LOOPB_MIN_N")) march2_loopb_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;

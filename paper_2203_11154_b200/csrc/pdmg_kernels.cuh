@@ -1180,6 +1180,7 @@ struct MarchArgs {
   int n, nc;
   int64_t ss, ssc;
   int ntx, ntasks, Hs;  // strips across, warp tasks per shift, strip height
+  int loop_a;           // k_march2 loop shape (see there)
 };
 
 template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI, int LC>
@@ -1788,22 +1789,63 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
       }
     }
   };
-#ifndef PDMG_MARCH2_SPLIT
-#define PDMG_MARCH2_SPLIT 1
-#endif
-  auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
-    if (PDMG_MARCH2_SPLIT && col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
-    else step(j, PH, IC<1>{});
+  auto adv = [&]() __attribute__((always_inline)) {
     if (++qj == M2_NS) qj = 0, pj ^= 1;
   };
-  int j = rlo;
-  for (; j + 2 < rhi; j += 3) {
-    step_any(j, IC<0>{});
-    step_any(j + 1, IC<1>{});
-    step_any(j + 2, IC<2>{});
+  // Two loop shapes (measured per variant on B200, the prolongating passes prefer the first):
+  //  (a) every step unrolled by 3 over the window phases, each with a masked and an unmasked copy;
+  //  (b) boundary steps one at a time in window phase 0 followed by a register rotation, interior steps
+  //      unmasked and unrolled by 3 -- only unmasked copies in the hot loop (smaller code).
+  if (PROLONG || a.loop_a) {
+    auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
+      if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
+      else step(j, PH, IC<1>{});
+      adv();
+    };
+    int j = rlo;
+    for (; j + 2 < rhi; j += 3) {
+      step_any(j, IC<0>{});
+      step_any(j + 1, IC<1>{});
+      step_any(j + 2, IC<2>{});
+    }
+    if (j < rhi) step_any(j, IC<0>{});
+    if (j + 1 < rhi) step_any(j + 1, IC<1>{});
+  } else {
+    auto rotate = [&]() __attribute__((always_inline)) {
+#pragma unroll
+      for (int k = 0; k < LC; ++k) {
+        U0[0][k] = U0[1][k], U0[1][k] = U0[2][k];
+        U1[0][k] = U1[1][k], U1[1][k] = U1[2][k];
+        U2[0][k] = U2[1][k], U2[1][k] = U2[2][k];
+      }
+    };
+    const int jm_lo = col_int ? max(rlo, jlo_int) : rhi;  // interior steps: [jm_lo, jm_end)
+    const int jm_end = col_int ? max(jm_lo, min(jhi_int + 1, rhi)) : rhi;
+    int j = rlo;
+    for (; j < jm_lo; ++j) {  // leading boundary steps
+      step(j, IC<0>{}, IC<1>{});
+      rotate();
+      adv();
+    }
+    for (; j + 2 < jm_end; j += 3) {
+      step(j, IC<0>{}, IC<0>{});
+      adv();
+      step(j + 1, IC<1>{}, IC<0>{});
+      adv();
+      step(j + 2, IC<2>{}, IC<0>{});
+      adv();
+    }
+    for (; j < jm_end; ++j) {
+      step(j, IC<0>{}, IC<0>{});
+      rotate();
+      adv();
+    }
+    for (; j < rhi; ++j) {  // trailing boundary steps
+      step(j, IC<0>{}, IC<1>{});
+      rotate();
+      adv();
+    }
   }
-  if (j < rhi) step_any(j, IC<0>{});
-  if (j + 1 < rhi) step_any(j + 1, IC<1>{});
   if constexpr (POST == POST_NORM || NORM_IN) {
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
     if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
