@@ -277,9 +277,9 @@ struct KernelTable {
 
 template <class T>
 struct MarchTable {
-  void (*e[64])(MarchArgs<T>) = {};
-  static int key(bool lu, bool pr, int post, bool ja, int lc) {
-    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (ja ? 16 : 0) | (lc == 2 ? 32 : 0);
+  void (*e[128])(MarchArgs<T>) = {};
+  static int key(bool lu, bool pr, int post, bool ja, int lc, bool nin = false) {
+    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (ja ? 16 : 0) | (lc == 2 ? 32 : 0) | (nin ? 64 : 0);
   }
   template <bool LU, bool PR, int PO, bool JA>
   void reg() {
@@ -295,7 +295,15 @@ struct MarchTable {
       reg<true, true, PO, JA>();
     }
   }
+  template <bool LU, int PO, bool JA>
+  void reg_nin() {  // first fine sweep of a cycle that also yields the previous iterate's residual norm
+    e[key(LU, false, PO, JA, 2, true)] = &k_march<T, LU, false, PO, JA, 2, true>;
+  }
   MarchTable() {
+    reg_nin<false, POST_RESTRICT, false>();
+    reg_nin<true, POST_RESTRICT, false>();
+    reg_nin<false, POST_RESTRICT, true>();
+    reg_nin<true, POST_RESTRICT, true>();
     reg4<POST_NONE, false>();
     reg4<POST_NONE, true>();
     reg4<POST_NORM, false>();
@@ -444,8 +452,12 @@ struct Engine : EngineBase {
   int march2_loopb_min_n = 512;
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
   int nin_k = -1;         // cycle_level: the first fine pass computes the norm of iterate nin_k (>= 0)
+  // the first fine pass of a cycle must be a marching sweep that can also form ||b - L u_in||: the single
+  // sweep + restriction (nu1 = 1) or a fused pair (even nu1)
   bool use_norm_next() const {
-    return norm_next && march2_pre && use_march2(0) && cfg.nu1 >= 2 && cfg.nu1 % 2 == 0;
+    if (!norm_next || lv.size() < 2) return false;
+    if (cfg.nu1 == 1) return march_min_n > 0 && lv[0].n >= march_min_n && march_lc == 2;
+    return march2_pre && use_march2(0) && cfg.nu1 >= 2 && cfg.nu1 % 2 == 0;
   }
   bool use_march2(int l) const {
     return march2_min_n > 0 && lv[l].n >= march2_min_n && cfg.smoother == PDMG_SMOOTHER_VANKA;
@@ -714,7 +726,7 @@ struct Engine : EngineBase {
 
   // ---- kernel launch ------------------------------------------------------------------------
   void level_pass(int l, const Variant& v, const V* uin, V* uout, const V* b, const V* ec, V* bc, const int* active,
-                  int n_act) {
+                  int n_act, bool norm_in = false) {
     const Level& Lv = lv[l];
     LevelArgs<T> a{};
     a.u_in = uin;
@@ -739,7 +751,8 @@ struct Engine : EngineBase {
     if (v.prolong) bpp += S_ / 4;
     if (v.store || v.post == POST_RESID) bpp += S_;
     if (v.post == POST_RESTRICT) bpp += S_ / 4;
-    const std::string cls = "L" + std::to_string(l) + ":" + v.name();
+    const std::string cls = "L" + std::to_string(l) + ":" + v.name() + (norm_in ? "+norm_in" : "");
+    if (norm_in && !use_march(l, v)) throw std::logic_error("pdmg_b200: norm_in needs the marching kernel");
     if (use_march(l, v)) {
       MarchArgs<T> ma{};
       ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
@@ -749,7 +762,7 @@ struct Engine : EngineBase {
       ma.Hs = march_hs_for(Lv.n);
       ma.ntx = (Lv.n + wout - 1) / wout;
       ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
-      auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi, march_lc)];
+      auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi, march_lc, norm_in)];
       if (!fn) throw std::logic_error("pdmg_b200: no march kernel for variant " + v.name());
       dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
       timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma); });
@@ -835,7 +848,12 @@ struct Engine : EngineBase {
         continue;
       }
       Variant v{!Lv.uzero, false, true, last ? POST_RESTRICT : POST_NONE, true, jac};
-      level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, nullptr, Lc.b, active, n_act);
+      const bool nin = l == 0 && k == 0 && nin_k >= 0;  // (only with nu1 == 1: see use_norm_next)
+      level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, nullptr, Lc.b, active, n_act, nin);
+      if (nin) {
+        finalize(nin_k, last_partials, false, Lv.cur);
+        nin_k = -1;
+      }
       Lv.cur ^= 1;
       Lv.uzero = false;
     }

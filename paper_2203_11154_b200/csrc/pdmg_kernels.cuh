@@ -1183,7 +1183,7 @@ struct MarchArgs {
   int loop_a;           // k_march2 loop shape (see there)
 };
 
-template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI, int LC>
+template <class T, bool LOADU, bool PROLONG, int POST, bool JACOBI, int LC, bool NORM_IN = false>
 #ifndef PDMG_MARCH_MINB
 #define PDMG_MARCH_MINB 3
 #endif
@@ -1320,6 +1320,13 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
       for (int k = 0; k < LC; ++k)
         rn[k] = csel(rin && cin[k], res5(Bc[k], cf.inv_h2, cf.dd, U[1][k], west(U[1], k, wl), east(U[1], k, er),
                                          U[0][k], U[2][k]));
+      if constexpr (NORM_IN) {  // ||b - L u_in||^2 of the owned rows/columns (the previous iterate's residual)
+        if (row >= olo && row < ohi) {
+#pragma unroll
+          for (int k = 0; k < LC; ++k)
+            if (cst[k]) nacc += rn[k].x * rn[k].x + rn[k].y * rn[k].y;
+        }
+      }
       D2 sn[LC];
       if constexpr (!JACOBI) {
         const D2 rwl = shfl_up2(rn[LC - 1]), rer = shfl_dn2(rn[0]);
@@ -1418,7 +1425,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
       }
     }
   }
-  if constexpr (POST == POST_NORM) {
+  if constexpr (POST == POST_NORM || NORM_IN) {
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
     if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
   }
