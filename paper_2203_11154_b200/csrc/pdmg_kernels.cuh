@@ -1236,9 +1236,11 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
       out[q] = ((unsigned)J <= (unsigned)nc && (unsigned)I <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + I]) : cz<D2>();
     }
   };
-  auto load_u = [&](int row, D2* out) {
+  // u_in row `row` (out: the raw load, consumed a step later) and its prolongation term (pout, from the
+  // register window: computed now so neither the u nor the coarse loads are waited on in this step)
+  auto load_u = [&](int row, D2* out, D2* pout) {
 #pragma unroll
-    for (int k = 0; k < LC; ++k) out[k] = cz<D2>();
+    for (int k = 0; k < LC; ++k) out[k] = pout[k] = cz<D2>();
     if constexpr (PROLONG) {
       const int J = row >> 1;
       if (J == wJ + 1) {
@@ -1257,22 +1259,19 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
     for (int k = 0; k < LC; ++k) {
       if (!cin[k]) continue;
       const int c = cA + k;
-      D2 v = cz<D2>();
-      if constexpr (LOADU) v = ld2(uin[(int64_t)row * n + c]);
+      if constexpr (LOADU) out[k] = ld2(uin[(int64_t)row * n + c]);
       if constexpr (PROLONG) {  // u += prolong_bilinear(e_c) (grid.cpp:123-153)
         const int q = (c >> 1) - Ie;  // 0 .. LC-1 (runtime for odd cA): select, no local-memory indexing
         D2 a0 = E0[0], a1 = E0[1], b0 = E1[0], b1 = E1[1];
 #pragma unroll
         for (int z = 1; z < LC; ++z)
           if (q == z) a0 = E0[z], a1 = E0[z + 1], b0 = E1[z], b1 = E1[z + 1];
+        // row parity is warp-uniform: even rows never wait on the coarse row (E1) just issued
         D2 p;
-        if (!(c & 1) && !(row & 1)) p = a0;
-        else if ((c & 1) && !(row & 1)) p = cscale(0.5, cadd(a0, a1));
-        else if (!(c & 1) && (row & 1)) p = cscale(0.5, cadd(a0, b0));
-        else p = cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1));
-        v = cadd(v, p);
+        if (row & 1) p = (c & 1) ? cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1)) : cscale(0.5, cadd(a0, b0));
+        else p = (c & 1) ? cscale(0.5, cadd(a0, a1)) : a0;
+        pout[k] = p;
       }
-      out[k] = v;
     }
   };
   auto load_b = [&](int row, D2* out) {
@@ -1286,7 +1285,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
 
   D2 U[3][LC], R[3][LC], S[3][LC], Dl[3][LC];
   D2 Vp[LC], R2c[LC];  // restriction: partial vertical 1-2-1 sum of the coarse row in progress, last r2
-  D2 Bc[LC], Un[LC], Bn[LC];
+  D2 Bc[LC], Un[LC], Pn[LC], Bn[LC];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -1294,7 +1293,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
 #pragma unroll
   for (int k = 0; k < LC; ++k) Vp[k] = R2c[k] = cz<D2>();
   double nacc = 0.0;
-  load_u(rlo, Un);
+  load_u(rlo, Un, Pn);
   load_b(rlo - 1, Bn);
 
   for (int j = rlo; j < rhi; ++j) {
@@ -1303,11 +1302,11 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
     for (int k = 0; k < LC; ++k) {
       U[0][k] = U[1][k];
       U[1][k] = U[2][k];
-      U[2][k] = Un[k];
+      U[2][k] = PROLONG ? cadd(Un[k], Pn[k]) : Un[k];
       Bc[k] = Bn[k];
     }
     if (j + 1 < rhi) {
-      load_u(j + 1, Un);
+      load_u(j + 1, Un, Pn);
       load_b(j, Bn);
     }
     // ---- stage B: r at row j-1 = b - (A + lambda I) u  ---------------------------------------------

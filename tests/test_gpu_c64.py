@@ -62,3 +62,19 @@ def test_c64_config4_setA_small_shifts(oracle):
     for s in range(2):
         assert reps[s].converged, reps[s].residual_history[-4:] / reps[s].residual_history[0]
         assert rel(u[s], u64[s]) < 1e-4
+
+
+@pytest.mark.parametrize("cyc", [Cfg(nu1=2, nu2=2, tol=1e-5), Cfg(nu1=1, nu2=1, tol=1e-5)])
+def test_c64_fused_passes(oracle, cyc):
+    """complex64 through the fused two-sweep passes (V(2,2)) and the norm-next path (both), n = 256:
+    the second sweep sees the fp32-stored first-sweep iterate exactly as an unfused solve would."""
+    n, m = 256, 255
+    lams = oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, 256)[[0, 77, 200]]
+    b = oracle.random_complex(5, 3 * m * m).reshape(3, m, m)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, mg(cyc), precision="c64") as H:
+        u, reps = H.solve(b)
+    ref = oracle.solve_batch(n, lams, Cfg(nu1=cyc.nu1, nu2=cyc.nu2, tol=1e-10), b, threads=8)
+    for s in range(3):
+        assert reps[s].converged
+        assert reps[s].residual_history[-1] <= 1e-5 * reps[s].residual_history[0]
+        assert rel(u[s], ref["u"][s]) < 1e-4

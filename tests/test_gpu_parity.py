@@ -98,6 +98,9 @@ def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10, path="auto"):
         assert reps[s].iterations == it, (s, reps[s].iterations, it)
         assert reps[s].converged == bool(ref["converged"][s])
         hist_ref = ref["hist"][s, : it + 1]
+        if hist_ref[0] == 0:  # b = 0: converged before any cycle, u = 0 exactly
+            assert list(reps[s].residual_history) == [0.0] and np.all(u[s] == 0)
+            continue
         assert np.max(np.abs(reps[s].residual_history - hist_ref) / hist_ref[0]) < tol_rel
         assert rel(u[s], ref["u"][s]) < tol_rel
         # rate is a geometric mean of ratios of residuals ~1e-10 r0, so it inherits their relative error
@@ -247,3 +250,30 @@ def test_chunked_host_solve_matches(oracle, monkeypatch, chunks, path):
     for r, q in zip(reps, reps_ref):
         assert r.iterations == q.iterations and r.converged == q.converged
         assert list(r.residual_history) == list(q.residual_history)
+
+
+@pytest.mark.parametrize("cyc", [Cfg(nu1=1, nu2=1, tol=1e-14, max_iter=3), Cfg(nu1=2, nu2=2, tol=1e-14, max_iter=2),
+                                 Cfg(nu1=1, nu2=1, tol=1e-14, max_iter=1, smoother="jacobi", omega=0.8)])
+def test_norm_next_max_iter(oracle, cyc):
+    """On grids with n >= 64 the batched path forms each iterate's residual norm in the next cycle's first
+    fine pass and closes the history with one norm pass after max_iter cycles; the reports (non-convergence,
+    iteration counts, full history, rate) must match the oracle."""
+    n, m = 128, 127
+    lams = [0.0, 8.959263353215057 - 15.395328029306036j]
+    b = oracle.random_complex(41, 2 * m * m).reshape(2, m, m)
+    u, reps, ref = _check_solve(oracle, n, lams, b, cyc, path="batched")
+    for r in reps:
+        assert not r.converged and r.iterations == cyc.max_iter
+
+
+def test_norm_next_mixed_convergence(oracle):
+    """Shifts converging at different cycles (b = 0, an easy and a hard shift) through the norm-next path:
+    a converged shift's iterate stays in the buffer its last cycle wrote while the others keep cycling."""
+    n, m = 128, 127
+    lams = [5000 + 0j, 0.0, 0.0, 8.959263353215057 - 15.395328029306036j]
+    b = oracle.random_complex(42, 4 * m * m).reshape(4, m, m)
+    b[1] = 0
+    for cyc in (Cfg(nu1=1, nu2=1), Cfg(nu1=2, nu2=2), Cfg(nu1=2, nu2=2, cycle="W")):
+        u, reps, ref = _check_solve(oracle, n, lams, b, cyc, path="batched")
+        assert reps[1].iterations == 0 and np.all(u[1] == 0)
+        assert len(set(r.iterations for r in reps)) >= 2
