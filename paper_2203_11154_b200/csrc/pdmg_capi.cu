@@ -17,15 +17,18 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pdmg_b200.h"
 #include "pdmg_kernels.cuh"
+#include "pdmg_march2ws.cuh"
 
 using cplx = std::complex<double>;
 
@@ -316,13 +319,15 @@ struct MarchTable {
 // two-sweep fused Vanka passes (k_march2): key = loadu | prolong << 1 | post << 2
 template <class T>
 struct March2Table {
-  void (*e[32])(MarchArgs<T>) = {};
+  void (*e[32])(MarchArgs<T>, CoefPack) = {};
   static int key(bool lu, bool pr, int post, bool nin = false) {
     return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0);
   }
+  void (*ws[32])(MarchArgs<T>, CoefPack) = {};  // warp-specialised pair kernels (k_march2ws), same keys
   size_t smem[32] = {};
   template <bool LU, bool PR, int PO, bool NI = false>
   void reg() {
+    ws[key(LU, PR, PO, NI)] = &k_march2ws<T, LU, PR, PO, NI>;
     e[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI>;
     smem[key(LU, PR, PO, NI)] = march2_smem<T>(LU);
     if (march2_smem<T>(LU) > 0)
@@ -396,6 +401,7 @@ struct Engine : EngineBase {
     V* b = nullptr;
     int ntx = 0, nty = 0, ntiles = 0, H = 0;
     LevelCoef* coef = nullptr;
+    std::vector<LevelCoef> hcoef;  // host copy (kernel-parameter coefficient packs)
     int cur = 0;
     bool uzero = false;
   };
@@ -450,6 +456,7 @@ struct Engine : EngineBase {
   int march2_hs = 0;      // strip height override (0 = automatic)
   bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
   int march2_loopb_min_n = 512;
+  bool march2_ws = false;  // run the pair passes as warp-specialised producer/consumer warp pairs (k_march2ws)
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
   int nin_k = -1;         // cycle_level: the first fine pass computes the norm of iterate nin_k (>= 0)
   // the first fine pass of a cycle must be a marching sweep that can also form ||b - L u_in||: the single
@@ -461,6 +468,16 @@ struct Engine : EngineBase {
   }
   bool use_march2(int l) const {
     return march2_min_n > 0 && lv[l].n >= march2_min_n && cfg.smoother == PDMG_SMOOTHER_VANKA;
+  }
+  std::unique_ptr<CoefPack> cpack{new CoefPack()};
+  // coefficients of engine shifts [c0, c0 + cnt) (RangeView: engine shift s = global shift s_base + s)
+  void fill_pack(const Level& Lv, int c0, int cnt) {
+    cpack->inv_h2 = Lv.hcoef.empty() ? 0.0 : Lv.hcoef[0].inv_h2;
+    cpack->shift0 = c0;
+    for (int i = 0; i < cnt; ++i) {
+      const LevelCoef& c = Lv.hcoef[s_base + c0 + i];
+      cpack->c[i] = CoefU{c.dd, c.k0, c.k1, c.k2};
+    }
   }
   // two consecutive Vanka sweeps u[cur] -> u[cur^1] (+ prolongation of ec before, + restriction/norm after)
   void level_pass2(int l, bool loadu, bool prolong, int post, const V* uin, V* uout, const V* b, const V* ec, V* bc,
@@ -478,16 +495,24 @@ struct Engine : EngineBase {
     ma.ntx = (Lv.n + wout - 1) / wout;
     ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
     const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
-    auto fn = marches2().e[key2];
-    const size_t smem2 = marches2().smem[key2];
+    const bool ws = march2_ws;
+    auto fn = ws ? marches2().ws[key2] : marches2().e[key2];
+    const size_t smem2 = ws ? 0 : marches2().smem[key2];
     if (!fn) throw std::logic_error("pdmg_b200: no two-sweep kernel for this variant");
     const double S_ = sizeof(V), pts = (double)n_act * Lv.m * Lv.m;
     const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0);
     std::string cls = "L" + std::to_string(l) + ":" + (prolong ? (loadu ? "prolong+" : "prolong0+") : (loadu ? "" : "zero+")) +
                       "vanka2" + (post == POST_NORM ? "+norm" : post == POST_RESTRICT ? "+restrict" : "") +
                       (norm_in ? "+norm_in" : "");
-    dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
-    timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, smem2, stream>>>(ma); });
+    const int per_cta = ws ? WS_PAIRS : MARCH_WARPS;
+    timed(cls, pts * bpp, [&] {
+      for (int c0 = 0; c0 < S; c0 += COEF_MAX) {  // one launch per COEF_MAX shifts (coefficients as parameters)
+        const int cnt = std::min(COEF_MAX, S - c0);
+        fill_pack(Lv, c0, cnt);
+        dim3 grid((ma.ntasks + per_cta - 1) / per_cta, cnt);
+        fn<<<grid, ws ? WS_THREADS : 32 * MARCH_WARPS, smem2, stream>>>(ma, *cpack);
+      }
+    });
     last_partials = ma.ntasks;
   }
   // measured on B200 (C3, C4): the marcher wins for sweep+norm and sweep+restrict, the ring
@@ -550,6 +575,8 @@ struct Engine : EngineBase {
 
   // ---- construction: host validation first (no CUDA), then device allocation ----------------
   void setup_host(const pdmg_batch_desc& d) override {
+    desc_ = d;
+    desc_.lambdas = nullptr;  // (the engine keeps its own copy in `lambdas`)
     if (d.n_shifts < 1) throw ConfigError("pdmg_create: n_shifts must be >= 1");
     if (d.n_shifts > 65535) throw ConfigError("pdmg_create: n_shifts must be <= 65535 per context");
     if (!d.lambdas) throw ConfigError("pdmg_create: lambdas is NULL");
@@ -580,6 +607,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_LEVEL_H_MIN_N")) level_h_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_TAIL_MAX_N")) tail_max_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_IO_MODE")) io_mode = std::atoi(e);
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH2_MIN_N")) march2_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH2_HS")) march2_hs = std::atoi(e);
@@ -587,6 +615,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH2_POST")) march2_post = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_NORM_NEXT")) norm_next = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH2_LOOPB_MIN_N")) march2_loopb_min_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH2_WS")) march2_ws = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
@@ -594,7 +623,7 @@ struct Engine : EngineBase {
     CK(cudaGetDeviceCount(&ndev));
     if (dev < 0 || dev >= ndev) throw CudaError("pdmg_create: CUDA device " + std::to_string(dev) + " not available");
     CK(cudaSetDevice(dev));
-    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, stream_priority));
     table = &kernels();
     const int L = (int)ln.size();
     lv.resize(L);
@@ -639,6 +668,7 @@ struct Engine : EngineBase {
         c.inv_h2 = 1.0 / (h * h);
         c.pad_ = 0;
       }
+      Lv.hcoef = hc;
       CK(cudaMalloc(&Lv.coef, sizeof(LevelCoef) * S));
       CK(cudaMemcpyAsync(Lv.coef, hc.data(), sizeof(LevelCoef) * S, cudaMemcpyHostToDevice, stream));
     }
@@ -1131,6 +1161,47 @@ struct Engine : EngineBase {
 
   cudaStream_t copy_stream = nullptr;
   int io_chunks = 0;  // 0 = automatic
+  int io_mode = 1;    // 1: chunks solve concurrently on sub-engines (own streams, priorities); 0: one stream
+  int stream_priority = 0;
+  // Sub-engines of the concurrent host-buffer pipeline: shifts [sub_lo[c], sub_lo[c+1]) on their own stream,
+  // chunk c at stream priority greatest + c, so chunks finish in order while later chunks fill the SMs the
+  // earlier ones leave idle (coarse levels, convergence bookkeeping, tails of the large passes).
+  std::vector<std::unique_ptr<Engine<T>>> subs;
+  std::vector<int> sub_lo;
+  pdmg_batch_desc desc_{};
+  bool build_subs(const std::vector<int>& lo) {
+    if (subs.size() + 1 == lo.size() && sub_lo == lo) {
+      for (auto& e : subs) e->solve_path = solve_path;
+      return true;
+    }
+    subs.clear();
+    sub_lo.clear();
+    // memory: each sub-engine holds the level storage of its shifts (the main engine keeps its own)
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    size_t need = 0;
+    for (const Level& L : lv) need += L.elems * sizeof(V) * 3;
+    if (need + ((size_t)2 << 30) > fr) return false;
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    for (size_t c = 0; c + 1 < lo.size(); ++c) {
+      auto e = std::make_unique<Engine<T>>();
+      pdmg_batch_desc d = desc_;
+      std::vector<pdmg_c128> lam(lo[c + 1] - lo[c]);
+      for (int s = lo[c]; s < lo[c + 1]; ++s) lam[s - lo[c]] = pdmg_c128{lambdas[s].real(), lambdas[s].imag()};
+      d.n_shifts = lo[c + 1] - lo[c];
+      d.lambdas = lam.data();
+      e->device = -1;
+      e->setup_host(d);
+      e->stream_priority = std::min(greatest + (int)c, least);
+      e->setup_device(device);
+      e->io_chunks = 1;
+      e->solve_path = solve_path;
+      subs.push_back(std::move(e));
+    }
+    sub_lo = lo;
+    return true;
+  }
 
   // Host-buffer solve.  Large batches are pipelined over chunks of shifts: H2D of later chunks and D2H of
   // earlier ones run on a copy stream while the current chunk solves (results are identical: every shift's
@@ -1161,6 +1232,10 @@ struct Engine : EngineBase {
     }
     const auto t0 = std::chrono::steady_clock::now();
     if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    if (io_mode == 1 && solve_concurrent(b, u, rep, st, N, per)) {
+      if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return;
+    }
     std::vector<cudaEvent_t> in(nch), done(nch);
     for (int c = 0; c < nch; ++c) {
       CK(cudaEventCreateWithFlags(&in[c], cudaEventDisableTiming));
@@ -1203,6 +1278,108 @@ struct Engine : EngineBase {
     for (int c = 0; c < nch; ++c) cudaEventDestroy(in[c]), cudaEventDestroy(done[c]);
     last_updates = upd;
     if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  // Concurrent host pipeline: all H2D copies queue on the copy stream in chunk order; chunk c's host thread
+  // waits for its copy, solves on its sub-engine's stream and queues its own D2H there.  Every shift's solve
+  // is independent, so the results are bitwise those of one batch (test_chunked_host_solve_matches).
+  bool solve_concurrent(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep, double2* st, size_t N, int64_t per) {
+    // automatic: six chunks weighted 1,2,2,2,2,1 -- half-size first and last chunks shorten the exposed fill
+    // (first H2D) and drain (last D2H); measured on B200 (C3): 45.9 ms vs 47.4 (1,2,2,2,1), 48.1 (8 equal),
+    // 49.4 (1,3,3,1) and 51.4 for the one-stream three-chunk pipeline (io_mode 0)
+    int nch = io_chunks > 0 ? io_chunks : 6;
+    nch = std::max(2, std::min(nch, S));
+    std::vector<int> lo(nch + 1);
+    if (io_chunks <= 0 && nch == 6) {
+      static const int wt[6] = {1, 2, 2, 2, 2, 1};
+      int acc = 0;
+      for (int c = 0; c < 6; ++c) acc += wt[c], lo[c + 1] = (int)((int64_t)S * acc / 10);
+    } else {
+      for (int c = 0; c <= nch; ++c) lo[c] = (int)((int64_t)S * c / nch);
+    }
+    if (const char* e = std::getenv("PDMG_IO_LAYOUT")) {  // chunk sizes in parts, e.g. "1,2,2,2,1" (tuning)
+      std::vector<double> w;
+      for (const char* q = e; *q;) {
+        char* end = nullptr;
+        w.push_back(std::strtod(q, &end));
+        q = (*end == ',') ? end + 1 : end;
+        if (end == q && *q) break;
+      }
+      double tw = 0;
+      for (double x : w) tw += x;
+      lo.assign(w.size() + 1, 0);
+      double acc = 0;
+      for (size_t c = 0; c < w.size(); ++c) acc += w[c], lo[c + 1] = (int)std::lround(S * acc / tw);
+      lo.back() = S;
+      nch = (int)w.size();
+    }
+    for (int c = 0; c < nch; ++c)
+      if (lo[c + 1] <= lo[c]) return false;
+    if (!build_subs(lo)) return false;
+    std::vector<cudaEvent_t> in(nch);
+    static const bool dbg = std::getenv("PDMG_IO_DEBUG") != nullptr;
+    auto tevent = [&](cudaStream_t st_) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, st_));
+      return e;
+    };
+    std::vector<cudaEvent_t> t_in(nch), t_sol(nch), t_out(nch);
+    cudaEvent_t t_start = dbg ? tevent(copy_stream) : nullptr;
+    for (int c = 0; c < nch; ++c) {
+      CK(cudaEventCreateWithFlags(&in[c], dbg ? 0 : cudaEventDisableTiming));
+      CK(cudaMemcpyAsync(st + lo[c] * per, b + lo[c] * per, sizeof(double2) * per * (lo[c + 1] - lo[c]),
+                         cudaMemcpyHostToDevice, copy_stream));
+      CK(cudaEventRecord(in[c], copy_stream));
+    }
+    const int H = cfg.max_iter + 1;
+    std::vector<std::exception_ptr> err(nch);
+    std::vector<std::thread> th;
+    for (int c = 0; c < nch; ++c) {
+      th.emplace_back([&, c] {
+        try {
+          Engine<T>& e = *subs[c];
+          CK(cudaSetDevice(device));
+          const int s0 = lo[c], cnt = lo[c + 1] - lo[c];
+          CK(cudaStreamWaitEvent(e.stream, in[c], 0));
+          pdmg_solve_report rc{};
+          if (rep) {
+            rc.iterations = rep->iterations ? rep->iterations + s0 : nullptr;
+            rc.converged = rep->converged ? rep->converged + s0 : nullptr;
+            rc.residual_history = rep->residual_history ? rep->residual_history + (int64_t)s0 * H : nullptr;
+            rc.rate = rep->rate ? rep->rate + s0 : nullptr;
+          }
+          e.solve_device(st + s0 * per, st + N + s0 * per, rep ? &rc : nullptr);
+          if (dbg) t_sol[c] = tevent(e.stream);
+          CK(cudaMemcpyAsync(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * cnt, cudaMemcpyDeviceToHost,
+                             e.stream));
+          if (dbg) t_out[c] = tevent(e.stream);
+          CK(cudaStreamSynchronize(e.stream));
+        } catch (...) {
+          err[c] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    if (dbg) {
+      for (int c = 0; c < nch; ++c) {
+        float a = 0, b2 = 0, c2 = 0;
+        cudaEventElapsedTime(&a, t_start, in[c]);
+        if (t_sol[c]) cudaEventElapsedTime(&b2, t_start, t_sol[c]);
+        if (t_out[c]) cudaEventElapsedTime(&c2, t_start, t_out[c]);
+        std::fprintf(stderr, "pdmg io chunk %d [%d,%d): in %.2f solved %.2f out %.2f ms\n", c, lo[c], lo[c + 1], a, b2, c2);
+        if (t_sol[c]) cudaEventDestroy(t_sol[c]);
+        if (t_out[c]) cudaEventDestroy(t_out[c]);
+      }
+      cudaEventDestroy(t_start);
+    }
+    for (int c = 0; c < nch; ++c) cudaEventDestroy(in[c]);
+    for (auto& x : err)
+      if (x) std::rethrow_exception(x);
+    double upd = 0.0;
+    for (auto& e : subs) upd += e->last_updates, launches += e->launches, e->launches = 0;
+    last_updates = upd;
+    return true;
   }
 
   void cycle_host(pdmg_c128* u, const pdmg_c128* b) override {

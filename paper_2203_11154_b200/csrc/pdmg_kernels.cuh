@@ -137,6 +137,30 @@ struct LevelCoef {
   double pad_;
 };
 
+// The per-shift operator coefficients of one level, passed to the marching kernels as a __grid_constant__
+// kernel parameter: indexed by blockIdx.y (CTA-uniform) they load into uniform registers (LDCU) and feed
+// the FP64 instructions as uniform operands, which frees 18 vector registers per thread in kernels whose
+// occupancy is register-bound.  A launch covers at most COEF_MAX shifts (16 KB of parameters).
+struct CoefU {
+  double2 dd, k0, k1, k2;  // as in LevelCoef
+};
+constexpr int COEF_MAX = 256;
+struct CoefPack {
+  double inv_h2;
+  int shift0;  // global shift of blockIdx.y == 0
+  int pad_;
+  CoefU c[COEF_MAX];
+};
+__device__ __forceinline__ LevelCoef coef_of(const CoefPack& cp) {
+  LevelCoef cf;
+  const CoefU& u = cp.c[blockIdx.y];
+  cf.d = make_double2(0.0, 0.0);
+  cf.dd = u.dd, cf.k0 = u.k0, cf.k1 = u.k1, cf.k2 = u.k2;
+  cf.inv_h2 = cp.inv_h2;
+  cf.pad_ = 0.0;
+  return cf;
+}
+
 enum : int { POST_NONE = 0, POST_NORM = 1, POST_RESTRICT = 2, POST_RESID = 3 };
 
 #ifndef PDMG_CHUNK
@@ -198,6 +222,13 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, un
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(smem_dst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Bulk prefetch of [p, p + bytes) into L2 (no registers, no completion): the marching kernels issue it a
+// few rows ahead so the row loads a step later hit L2 instead of waiting a full HBM round trip.  p and
+// bytes must be 16-byte aligned / multiples.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // Halo widths and shared-memory footprint of a k_level instantiation.  Rings fed by TMA (u_in, b, e_c)
@@ -1462,6 +1493,14 @@ struct IC {
 #ifndef PDMG_MARCH2_TMA
 #define PDMG_MARCH2_TMA 0
 #endif
+#ifndef PDMG_MARCH2_PF
+#define PDMG_MARCH2_PF 0
+#endif
+constexpr int M2_PF = PDMG_MARCH2_PF;  // L2 prefetch distance (rows), 0 = off
+#ifndef PDMG_MARCH2_PD
+#define PDMG_MARCH2_PD 1
+#endif
+constexpr int M2_PD = PDMG_MARCH2_PD;  // register prefetch distance of the u_in / b rows (1 or 2 steps)
 constexpr bool M2_TMA = PDMG_MARCH2_TMA;  // input rows via the TMA ring (1) or register prefetch (0)
 constexpr int M2_D = PDMG_MARCH2_D;  // rows in flight per warp
 constexpr int M2_NS = M2_D + 6;      // ring slots: rows j-5 .. j+D
@@ -1475,7 +1514,8 @@ constexpr size_t march2_smem(bool loadu) {
 // NORM_IN: also leave the partial sums of ||b - L u_in||^2 (the first sweep's residual, i.e. the residual of
 // the previous cycle's iterate) in a.partial -- the fine-level convergence norm, read one pass later.
 template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false>
-__global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(MarchArgs<T> a) {
+__global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
+    k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
   using D2 = double2;
   constexpr int LC = 2;
@@ -1485,7 +1525,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
   constexpr int hC = HASD ? hD + 1 : 0;
   constexpr int hA = (hC + 5) & ~1;  // rounded up to even: strips start at even columns
   constexpr int WOUT = 32 * LC - 2 * hA;
-  const int shift = blockIdx.y;
+  const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
   const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
   if (task >= a.ntasks) return;
@@ -1506,7 +1546,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
   const int lofs = (x0 - hA) - cs + LC * lane;  // this lane's first column within a ring row
   const int c_lo = max(cs, 0), c_hi = min(cs + M2_ROWW, n);
   const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
-  const LevelCoef cf = a.coef[shift];
+  const LevelCoef cf = coef_of(cp);
 
   bool cin[LC], cst[LC];
 #pragma unroll
@@ -1551,6 +1591,18 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
   // steps j in [jlo_int, jhi_int] touch only interior rows (loads j-5 .. j+1, coarse rows up to (j+1)/2+1)
   const int jlo_int = max(6, rlo + 5), jhi_int = m - 3;  // (register path: loads reach j+1 and j-4)
 
+  // L2 prefetch of the u_in and b rows M2_PF steps ahead (lane 0, one bulk request per row and array): the
+  // register prefetch one step ahead does not cover a loaded HBM round trip (ncu: long-scoreboard stalls
+  // on the first use of every prefetched row)
+  const int pc0 = max(cs, 0), pc1 = min(cs + 32 * LC + (EVEN ? 2 : 0), n);
+  const unsigned pbytes = pc1 > pc0 ? (unsigned)((pc1 - pc0) * sizeof(V)) & ~15u : 0u;
+  auto l2_ahead = [&](int row) __attribute__((always_inline)) {
+    if (lane == 0 && M2_PF > 0 && pbytes != 0 && (unsigned)row <= (unsigned)m) {
+      const int64_t g = sbase + (int64_t)row * n + pc0;
+      if constexpr (LOADU) prefetch_l2(a.u_in + g, pbytes);
+      if (row >= 1) prefetch_l2(a.b + g - n, pbytes);
+    }
+  };
   // prolongation window: coarse rows J, J+1 (in use) and J+2 (prefetched) at this lane's coarse column Ie;
   // the column Ie+1 comes from the next lane (lane 31 loads it itself)
   D2 Eo0 = cz<D2>(), Eo1 = cz<D2>(), Eo2 = cz<D2>(), Ex0 = cz<D2>(), Ex1 = cz<D2>(), Ex2 = cz<D2>();
@@ -1665,6 +1717,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
   D2 U0[3][LC], U1[3][LC], U2[3][LC];
   D2 P1[LC], C1[LC], P2[LC], C2[LC], Vp[LC];
   D2 Pn[LC], Unx[LC], Bn[LC], B3n[LC], B5n[LC];  // (the last four: register-prefetch path only)
+  D2 Unx2[M2_PD > 1 ? LC : 1], Bn2[M2_PD > 1 ? LC : 1];  // rows j+2 / j+1 (prefetch distance 2)
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -1675,8 +1728,13 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
   if constexpr (M2_TMA) {
     for (int r = rlo; r < min(rlo + M2_D, rhi); ++r) issue_q(r, r - rlo);
   } else {
+    for (int r = rlo + 1; r < min(rlo + M2_PF, rhi); ++r) l2_ahead(r);
     gread_u(rlo, Unx, IC<1>{});
     gload_b(rlo - 1, Bn, IC<1>{});
+    if constexpr (M2_PD > 1) {
+      gread_u(rlo + 1, Unx2, IC<1>{});
+      gload_b(rlo, Bn2, IC<1>{});
+    }
     gload_b(rlo - 3, B3n, IC<1>{});
     if constexpr (HASD) gload_b(rlo - 5, B5n, IC<1>{});
   }
@@ -1710,13 +1768,25 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB) k_march2(M
         B3[k] = B3n[k];
         if constexpr (HASD) B5[k] = B5n[k];
       }
+      if constexpr (M2_PD > 1) {
+#pragma unroll
+        for (int k = 0; k < LC; ++k) Unx[k] = Unx2[k], Bn[k] = Bn2[k];
+      }
       if (j + 1 < rhi) {
-        gread_u(j + 1, Unx, MK);
+        if constexpr (M2_PD > 1) {
+          if (j + 2 < rhi) {
+            gread_u(j + 2, Unx2, MK);
+            gload_b(j + 1, Bn2, MK);
+          }
+        } else {
+          gread_u(j + 1, Unx, MK);
+          gload_b(j, Bn, MK);
+        }
         if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
-        gload_b(j, Bn, MK);
         gload_b(j - 2, B3n, MK);
         if constexpr (HASD) gload_b(j - 4, B5n, MK);
       }
+      if (j + M2_PF < rhi) l2_ahead(j + M2_PF);
     }
 #pragma unroll
     for (int k = 0; k < LC; ++k) U0[sn][k] = Un[k];
