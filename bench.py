@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shifts", type=int, default=0, help="override the number of shifts (0 = config's)")
+    ap.add_argument("--nu", default="", help="override the cycle's nu1,nu2 (experiments; not a BASELINE config)")
     ap.add_argument("--precision", default="c128", choices=["c128", "c64"],
                     help="c64: fp32 storage / fp64 arithmetic, tol 1e-5 (BASELINE config 4)")
     return ap.parse_args()
@@ -302,6 +303,9 @@ def main():
     n, S, alpha, nt, dt, seed, nu1, nu2, desc = CONFIGS[args.config]
     if args.shifts:
         S = args.shifts
+    if args.nu:
+        nu1, nu2 = (int(x) for x in args.nu.split(","))
+        desc += f" [nu1,nu2 = {nu1},{nu2}]"
     m = n - 1
     b0, b1 = shard(S, rank, world)
     Sr = b1 - b0
@@ -412,9 +416,17 @@ def main():
     peak = peak or 6650.0
     top_name, top = max(stats.items(), key=lambda kv: kv[1]["ms"])
     total_ms = sum(v["ms"] for v in stats.values())
-    all_bytes = sum(v["bytes"] for v in stats.values())
+    all_bytes = sum(v.get("unit_bytes", v["bytes"]) for v in stats.values())
+    moved = None
     if top["bytes"] > 0:
-        achieved = top["bytes"] / (top["ms"] / 1e3) / 1e9
+        # SURVEY 8(d) algorithmic bytes: 48 B (c128) / 24 B (c64) per grid-point smoother update + the fused
+        # transfers; a two-sweep pass performs two updates per point.  `moved_*` is what the pass must move.
+        ub = top.get("unit_bytes") or top["bytes"]
+        achieved = ub / (top["ms"] / 1e3) / 1e9
+        mv = top["bytes"] / (top["ms"] / 1e3) / 1e9
+        moved = {"moved_bytes_per_launch": top["bytes"] / top["launches"], "moved_GBps": round(mv, 1),
+                 "moved_frac": round(mv / (peaks.get("hbm_gbs") or 6650.0), 4),
+                 "updates_per_launch": top.get("updates", 0.0) / top["launches"]}
         bound = "hbm"
     else:
         # one-CTA-per-shift solve (small grids): its working set is L2/L1-resident, so report the
@@ -427,8 +439,12 @@ def main():
                 "kernel_share_of_step": round(top["ms"] / total_ms, 4),
                 "timing": "per-kernel CUDA events on the library stream, profiled pass right after the timed region",
                 "launch_avg_ms": round(top["ms"] / top["launches"], 4),
-                "algo_bytes_per_launch": top["bytes"] / top["launches"],
+                "algo_bytes_per_launch": (top.get("unit_bytes") or top["bytes"]) / top["launches"],
+                "algo_bytes_def": "SURVEY 8(d): 48 B (c128) / 24 B (c64) per grid-point smoother update, plus "
+                                  "S/4 per point for a fused restriction or prolongation",
                 "all_kernels_algorithmic_GBps": round(all_bytes / (total_ms / 1e3) / 1e9, 1)}
+    if moved:
+        roofline.update(moved)
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f).get(args.config, {}).get(top_name)
@@ -464,7 +480,8 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                            "GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] > 0 else None}
+                            "GBps": round(v.get("unit_bytes", v["bytes"]) / v["ms"] / 1e6, 1) if v["ms"] > 0 else None,
+                            "moved_GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] > 0 else None}
                         for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])[:12]},
         }
         print(json.dumps(line), flush=True)

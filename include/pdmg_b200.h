@@ -182,6 +182,11 @@ int64_t pdmg_launch_count(const pdmg_ctx* ctx); /* kernels launched since the la
  * valid, 1 past the end. */
 int pdmg_kernel_stats(const pdmg_ctx* ctx, int i, char* name, size_t name_len, int64_t* launches,
                       double* total_ms, double* algo_bytes);
+/* Kernel class i, SURVEY 8(d) accounting: unit_bytes = 48 B (c128; 24 B c64) per grid-point smoother update
+ * the class performed plus its fused transfer bytes (the bytes moved, for passes without a smoother update),
+ * and the number of smoother updates.  A fused two-sweep pass counts two updates per point while moving
+ * the bytes of one (pdmg_kernel_stats).  Returns 0 while i is valid, 1 past the end. */
+int pdmg_kernel_updates(const pdmg_ctx* ctx, int i, double* unit_bytes, double* updates);
 /* Grid-point smoother updates performed by the last solve (sum over shifts and cycles). */
 double pdmg_last_updates(const pdmg_ctx* ctx);
 

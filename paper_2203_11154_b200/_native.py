@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
         "pdmg_launch_count": (i64, [vp]),
         "pdmg_kernel_stats": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(i64), C.POINTER(f64),
                                         C.POINTER(f64)]),
+        "pdmg_kernel_updates": (C.c_int, [vp, C.c_int, C.POINTER(f64), C.POINTER(f64)]),
         "pdmg_last_updates": (f64, [vp]),
     }
     for name, (res, args) in sig.items():

@@ -319,19 +319,19 @@ struct MarchTable {
 // two-sweep fused Vanka passes (k_march2): key = loadu | prolong << 1 | post << 2
 template <class T>
 struct March2Table {
-  void (*e[32])(MarchArgs<T>, CoefPack) = {};
-  static int key(bool lu, bool pr, int post, bool nin = false) {
-    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0);
+  void (*e[64])(MarchArgs<T>, CoefPack) = {};
+  static int key(bool lu, bool pr, int post, bool nin = false, bool mid = false) {
+    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0) | (mid ? 32 : 0);
   }
-  void (*ws[32])(MarchArgs<T>, CoefPack) = {};  // warp-specialised pair kernels (k_march2ws), same keys
-  size_t smem[32] = {};
-  template <bool LU, bool PR, int PO, bool NI = false>
+  void (*ws[64])(MarchArgs<T>, CoefPack) = {};  // warp-specialised pair kernels (k_march2ws), same keys
+  size_t smem[64] = {};
+  template <bool LU, bool PR, int PO, bool NI = false, bool MID = false>
   void reg() {
-    ws[key(LU, PR, PO, NI)] = &k_march2ws<T, LU, PR, PO, NI>;
-    e[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI>;
-    smem[key(LU, PR, PO, NI)] = march2_smem<T>(LU);
+    if constexpr (!MID) ws[key(LU, PR, PO, NI)] = &k_march2ws<T, LU, PR, PO, NI>;
+    e[key(LU, PR, PO, NI, MID)] = &k_march2<T, LU, PR, PO, NI, MID>;
+    smem[key(LU, PR, PO, NI, MID)] = march2_smem<T>(LU);
     if (march2_smem<T>(LU) > 0)
-      CK(cudaFuncSetAttribute(&k_march2<T, LU, PR, PO, NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CK(cudaFuncSetAttribute(&k_march2<T, LU, PR, PO, NI, MID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)march2_smem<T>(LU)));
   }
   March2Table() {
@@ -349,6 +349,7 @@ struct March2Table {
     reg<true, false, POST_RESTRICT, true>();
     reg<false, false, POST_NONE, true>();
     reg<true, false, POST_NONE, true>();
+    reg<true, true, POST_RESTRICT, false, true>();  // V(1,1) cross-cycle fusion
   }
 };
 
@@ -357,7 +358,9 @@ struct March2Table {
 // ---------------------------------------------------------------------------------------------
 struct Stat {
   int64_t launches = 0;
-  double ms = 0.0, bytes = 0.0;
+  double ms = 0.0, bytes = 0.0;  // bytes: the minimum DRAM traffic of the fused pass (what it must move)
+  double ubytes = 0.0;           // SURVEY 8(d) algorithmic bytes: 48 B (c128) per smoother update + transfers
+  double updates = 0.0;          // grid-point smoother updates
 };
 
 // Precision-independent part of an engine (what the C ABI needs without knowing the storage type).
@@ -397,7 +400,7 @@ struct Engine : EngineBase {
     int n = 0, m = 0;
     int64_t ss = 0;  // shift stride (elements)
     size_t elems = 0;
-    V* u[2] = {nullptr, nullptr};
+    V* u[3] = {nullptr, nullptr, nullptr};  // u[2]: level 0 only, V(1,1) cross-cycle fusion
     V* b = nullptr;
     int ntx = 0, nty = 0, ntiles = 0, H = 0;
     LevelCoef* coef = nullptr;
@@ -434,7 +437,7 @@ struct Engine : EngineBase {
   struct Pending {
     std::string cls;
     cudaEvent_t e0, e1;
-    double bytes;
+    double bytes, ubytes, updates;
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -458,6 +461,17 @@ struct Engine : EngineBase {
   int march2_loopb_min_n = 512;
   bool march2_ws = false;  // run the pair passes as warp-specialised producer/consumer warp pairs (k_march2ws)
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
+  // V(1,1): fuse cycle k's fine post-sweep with cycle k+1's pre-sweep (solve_xfuse).  Off by default:
+  // measured on B200 the fused pass costs what the two single-sweep passes cost (C3 at V(1,1): 1621 vs
+  // 807 + 821 us; C4 with 256 shifts: 6.38 vs 6.75 ms; C5 9.75 vs 9.08 ms per step) -- the passes are
+  // issue/latency-bound, so halving the fine-level bytes does not pay.  PDMG_XFUSE=1 enables it.
+  bool xfuse = false;
+  // (level sizes from `ln`: also called while the levels are being allocated)
+  bool use_xfuse() const {
+    return xfuse && norm_next && cfg.nu1 == 1 && cfg.nu2 == 1 && cfg.smoother == PDMG_SMOOTHER_VANKA &&
+           ln.size() >= 3 && march2_min_n > 0 && ln[0] >= march2_min_n && march_min_n > 0 && ln[0] >= march_min_n &&
+           march_lc == 2 && ln[1] > 4;
+  }
   int nin_k = -1;         // cycle_level: the first fine pass computes the norm of iterate nin_k (>= 0)
   // the first fine pass of a cycle must be a marching sweep that can also form ||b - L u_in||: the single
   // sweep + restriction (nu1 = 1) or a fused pair (even nu1)
@@ -481,10 +495,10 @@ struct Engine : EngineBase {
   }
   // two consecutive Vanka sweeps u[cur] -> u[cur^1] (+ prolongation of ec before, + restriction/norm after)
   void level_pass2(int l, bool loadu, bool prolong, int post, const V* uin, V* uout, const V* b, const V* ec, V* bc,
-                   const int* active, int n_act, bool norm_in = false) {
+                   const int* active, int n_act, bool norm_in = false, V* umid = nullptr) {
     const Level& Lv = lv[l];
     MarchArgs<T> ma{};
-    ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
+    ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial, ma.u_mid = umid;
     ma.coef = Lv.coef, ma.active = active, ma.n = Lv.n;
     ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
     ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
@@ -494,17 +508,19 @@ struct Engine : EngineBase {
     ma.loop_a = Lv.n < march2_loopb_min_n;  // measured: the split loop wins on the 512+ grids only
     ma.ntx = (Lv.n + wout - 1) / wout;
     ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
-    const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
-    const bool ws = march2_ws;
+    const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in, umid != nullptr);
+    const bool ws = march2_ws && umid == nullptr;
     auto fn = ws ? marches2().ws[key2] : marches2().e[key2];
     const size_t smem2 = ws ? 0 : marches2().smem[key2];
     if (!fn) throw std::logic_error("pdmg_b200: no two-sweep kernel for this variant");
     const double S_ = sizeof(V), pts = (double)n_act * Lv.m * Lv.m;
-    const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0);
+    const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0) +
+                       (umid ? S_ : 0);
     std::string cls = "L" + std::to_string(l) + ":" + (prolong ? (loadu ? "prolong+" : "prolong0+") : (loadu ? "" : "zero+")) +
                       "vanka2" + (post == POST_NORM ? "+norm" : post == POST_RESTRICT ? "+restrict" : "") +
-                      (norm_in ? "+norm_in" : "");
+                      (norm_in ? "+norm_in" : "") + (umid ? "+mid" : "");
     const int per_cta = ws ? WS_PAIRS : MARCH_WARPS;
+    const double ubpp = 2 * 3 * S_ + (prolong ? S_ / 4 : 0) + (post == POST_RESTRICT ? S_ / 4 : 0) + (umid ? S_ : 0);
     timed(cls, pts * bpp, [&] {
       for (int c0 = 0; c0 < S; c0 += COEF_MAX) {  // one launch per COEF_MAX shifts (coefficients as parameters)
         const int cnt = std::min(COEF_MAX, S - c0);
@@ -512,7 +528,7 @@ struct Engine : EngineBase {
         dim3 grid((ma.ntasks + per_cta - 1) / per_cta, cnt);
         fn<<<grid, ws ? WS_THREADS : 32 * MARCH_WARPS, smem2, stream>>>(ma, *cpack);
       }
-    });
+    }, pts * ubpp, 2 * pts);
     last_partials = ma.ntasks;
   }
   // measured on B200 (C3, C4): the marcher wins for sweep+norm and sweep+restrict, the ring
@@ -546,6 +562,7 @@ struct Engine : EngineBase {
     for (auto& L : lv) {
       cudaFree(L.u[0]);
       cudaFree(L.u[1]);
+      cudaFree(L.u[2]);
       cudaFree(L.b);
       cudaFree(L.coef);
     }
@@ -614,6 +631,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH2_PRE")) march2_pre = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH2_POST")) march2_post = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_NORM_NEXT")) norm_next = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_XFUSE")) xfuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH2_LOOPB_MIN_N")) march2_loopb_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH2_WS")) march2_ws = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
@@ -636,6 +654,10 @@ struct Engine : EngineBase {
       for (V** p : {&Lv.u[0], &Lv.u[1], &Lv.b}) {
         CK(cudaMalloc(p, Lv.elems * sizeof(V)));
         CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
+      }
+      if (l == 0 && use_xfuse()) {
+        CK(cudaMalloc(&Lv.u[2], Lv.elems * sizeof(V)));
+        CK(cudaMemsetAsync(Lv.u[2], 0, Lv.elems * sizeof(V), stream));
       }
       Lv.H = std::min(Lv.n >= level_h_min_n ? 128 : 64, Lv.n + (Lv.n & 1));
       Lv.ntx = (Lv.n + TILE_W - 1) / TILE_W;
@@ -725,14 +747,15 @@ struct Engine : EngineBase {
     CK(cudaEventCreate(&e));
     return e;
   }
+  // ubytes < 0: the pass performs no smoother update, its algorithmic bytes are the bytes it moves
   template <class F>
-  void timed(const std::string& cls, double bytes, F&& launch) {
+  void timed(const std::string& cls, double bytes, F&& launch, double ubytes = -1.0, double updates = 0.0) {
     ++launches;
     if (!profiling) {
       launch();
       return;
     }
-    Pending p{cls, get_event(), get_event(), bytes};
+    Pending p{cls, get_event(), get_event(), bytes, ubytes < 0 ? bytes : ubytes, updates};
     CK(cudaEventRecord(p.e0, stream));
     launch();
     CK(cudaEventRecord(p.e1, stream));
@@ -748,6 +771,8 @@ struct Engine : EngineBase {
       st.launches += 1;
       st.ms += ms;
       st.bytes += p.bytes;
+      st.ubytes += p.ubytes;
+      st.updates += p.updates;
       event_pool.push_back(p.e0);
       event_pool.push_back(p.e1);
     }
@@ -782,6 +807,9 @@ struct Engine : EngineBase {
     if (v.store || v.post == POST_RESID) bpp += S_;
     if (v.post == POST_RESTRICT) bpp += S_ / 4;
     const std::string cls = "L" + std::to_string(l) + ":" + v.name() + (norm_in ? "+norm_in" : "");
+    // a smoother update is 3 S (u in, b in, u out) whatever the pass actually moves
+    const double ubpp = v.sweep ? 3 * S_ + (v.prolong ? S_ / 4 : 0) + (v.post == POST_RESTRICT ? S_ / 4 : 0) : -1.0;
+    const double ub = ubpp < 0 ? -1.0 : pts * ubpp, nupd = v.sweep ? pts : 0.0;
     if (norm_in && !use_march(l, v)) throw std::logic_error("pdmg_b200: norm_in needs the marching kernel");
     if (use_march(l, v)) {
       MarchArgs<T> ma{};
@@ -795,13 +823,13 @@ struct Engine : EngineBase {
       auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi, march_lc, norm_in)];
       if (!fn) throw std::logic_error("pdmg_b200: no march kernel for variant " + v.name());
       dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
-      timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma); });
+      timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma); }, ub, nupd);
       last_partials = ma.ntasks;
       return;
     }
     const KernelEntry<T>& k = table->get(v);
     dim3 grid(Lv.ntiles, S);
-    timed(cls, pts * bpp, [&] { k.fn<<<grid, NTHREADS, k.smem, stream>>>(a); });
+    timed(cls, pts * bpp, [&] { k.fn<<<grid, NTHREADS, k.smem, stream>>>(a); }, ub, nupd);
     last_partials = Lv.ntiles;
   }
 
@@ -950,12 +978,13 @@ struct Engine : EngineBase {
     timed("unpack", (double)total * 2 * sizeof(V),
           [&] { k_unpack<T><<<blocks, 256, 0, stream>>>(src, dst, Lv.n, Lv.ss, total); });
   }
-  void pack(const V* b0, const V* b1, const int* iters, const int* parity, double2* dst, int l) {
+  void pack(const V* b0, const V* b1, const int* iters, const int* parity, double2* dst, int l,
+            const V* b2 = nullptr) {
     const Level& Lv = lv[l];
     const int64_t total = (int64_t)S * Lv.m * Lv.m;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     timed("pack", (double)total * 2 * sizeof(V),
-          [&] { k_pack<T><<<blocks, 256, 0, stream>>>(b0, b1, iters, parity, dst, Lv.n, Lv.ss, total); });
+          [&] { k_pack<T><<<blocks, 256, 0, stream>>>(b0, b1, b2 ? b2 : b0, iters, parity, dst, Lv.n, Lv.ss, total); });
   }
 
   // ---- MultigridHierarchy::solve for all shifts (multigrid.cpp:85-110) -----------------------
@@ -1001,6 +1030,12 @@ struct Engine : EngineBase {
       CK(cudaGetLastError());
       CK(cudaMemsetAsync(d_parity, 0, sizeof(int) * H, stream));
       pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+      finish_report(rep, t0, H);
+      return;
+    }
+    if (use_xfuse() && !any_singular && !use_small_path()) {
+      solve_xfuse();
+      pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0, F.u[2]);
       finish_report(rep, t0, H);
       return;
     }
@@ -1051,6 +1086,48 @@ struct Engine : EngineBase {
     }
     pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
     finish_report(rep, t0, H);
+  }
+
+  // V(1,1) with the fine level fused across cycles: after cycle 1's pre-sweep, every fine pass is
+  //   [u_in + P e_c -> post-sweep of cycle k -> u_k (stored to a third buffer) -> pre-sweep of cycle k+1
+  //    -> residual -> restriction]
+  // one k_march2<MID> pass: 4.5 S of HBM traffic per fine point and cycle instead of 6.5 S for the two
+  // single-sweep passes.  Its partials are ||b - L u_k||^2 (the second sweep's residual), so k_finalize(k)
+  // runs right after it; shifts converged at k are frozen with u_k in buffer X, the rest continue from the
+  // pre-smoothed iterate in Y.  The buffers rotate over three (pass input, u_k, pre-smoothed), parity[k]
+  // records X for k_pack.  Host pipelining as in the norm-next loop: count(k-1) is read once cycle k is
+  // enqueued.  At max_iter the last post-sweep runs alone with the norm.  Every point gets exactly the
+  // arithmetic of the unfused cycle (same sweeps, same residual formula), so iterates and histories match.
+  void solve_xfuse() {
+    Level& F = lv[0];
+    Level& Lc = lv[1];
+    const int gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+    int n_act = S;
+    // cycle 1's pre-sweep from the zero guess + restriction; its input residual is b, i.e. r0 (finalize(0))
+    level_pass(0, Variant{false, false, true, POST_RESTRICT, true, false}, F.u[0], F.u[1], F.b, nullptr, Lc.b,
+               d_active, n_act, true);
+    finalize(0, last_partials, false, 0);
+    F.cur = 1;
+    F.uzero = false;
+    for (int k = 1;; ++k) {
+      for (int g = 0; g < gamma; ++g) cycle_level(1, g == 0, d_active, n_act, false);
+      const V* ec = Lc.u[Lc.cur];
+      if (k == cfg.max_iter) {
+        const int w = (F.cur + 1) % 3;
+        level_pass(0, Variant{true, true, true, POST_NORM, true, false}, F.u[F.cur], F.u[w], F.b, ec, nullptr,
+                   d_active, n_act);
+        finalize(k, last_partials, true, w);
+        F.cur = w;
+        break;
+      }
+      const int X = (F.cur + 1) % 3, Y = (F.cur + 2) % 3;
+      level_pass2(0, true, true, POST_RESTRICT, F.u[F.cur], F.u[Y], F.b, ec, Lc.b, d_active, n_act, false, F.u[X]);
+      finalize(k, last_partials, false, X);
+      F.cur = Y;
+      n_act = read_nactive(k - 1);
+      if (n_act == 0) break;
+    }
+    F.cur = 0;  // (level state for the op-level entry points)
   }
 
   // Copy the per-shift report back; counts the smoother updates performed (sum over shifts of cycles).
@@ -1127,7 +1204,7 @@ struct Engine : EngineBase {
   struct RangeView {
     Engine& e;
     int S0;
-    std::vector<std::array<V*, 3>> saved_lv;
+    std::vector<std::array<V*, 4>> saved_lv;
     std::vector<LevelCoef*> saved_coef;
     std::vector<size_t> saved_elems;
     double2* ainv;
@@ -1135,10 +1212,11 @@ struct Engine : EngineBase {
     double *r0, *hist;
     RangeView(Engine& en, int s0, int cnt) : e(en), S0(en.S) {
       for (auto& L : e.lv) {
-        saved_lv.push_back({L.u[0], L.u[1], L.b});
+        saved_lv.push_back({L.u[0], L.u[1], L.b, L.u[2]});
         saved_coef.push_back(L.coef);
         saved_elems.push_back(L.elems);
         L.u[0] += s0 * L.ss, L.u[1] += s0 * L.ss, L.b += s0 * L.ss, L.coef += s0;
+        if (L.u[2]) L.u[2] += s0 * L.ss;
         L.elems = (size_t)L.ss * cnt + (s0 + cnt == en.S ? L.n + 2 : 0);
       }
       ainv = e.d_ainv, act = e.d_active, it = e.d_iters, cv = e.d_conv, ones = e.d_ones, r0 = e.d_r0, hist = e.d_hist;
@@ -1151,6 +1229,7 @@ struct Engine : EngineBase {
     ~RangeView() {
       for (size_t l = 0; l < e.lv.size(); ++l) {
         e.lv[l].u[0] = saved_lv[l][0], e.lv[l].u[1] = saved_lv[l][1], e.lv[l].b = saved_lv[l][2];
+        e.lv[l].u[2] = saved_lv[l][3];
         e.lv[l].coef = saved_coef[l], e.lv[l].elems = saved_elems[l];
       }
       e.d_ainv = ainv, e.d_active = act, e.d_iters = it, e.d_conv = cv, e.d_ones = ones, e.d_r0 = r0, e.d_hist = hist;
@@ -1886,6 +1965,14 @@ void pdmg_reset_stats(pdmg_ctx* c) {
   c->e->launches = 0;
 }
 int64_t pdmg_launch_count(const pdmg_ctx* c) { return c ? c->e->launches : 0; }
+int pdmg_kernel_updates(const pdmg_ctx* c, int i, double* unit_bytes, double* updates) {
+  if (!c || i < 0 || i >= (int)c->e->stats.size()) return 1;
+  auto it = c->e->stats.begin();
+  std::advance(it, i);
+  if (unit_bytes) *unit_bytes = it->second.ubytes;
+  if (updates) *updates = it->second.updates;
+  return 0;
+}
 int pdmg_kernel_stats(const pdmg_ctx* c, int i, char* name, size_t name_len, int64_t* launches, double* total_ms,
                       double* algo_bytes) {
   if (!c || i < 0 || i >= (int)c->e->stats.size()) return 1;

@@ -760,18 +760,19 @@ __global__ void k_unpack(const double2* __restrict__ src, typename vec2<T>::type
   }
 }
 
-// Gather u out of the double buffer each shift finished in: sel = parity[iterations[s]].
+// Gather u out of the buffer each shift finished in (level 0 has two, three with the V(1,1) cross-cycle
+// fusion): sel = parity[iterations[s]].
 template <class T>
 __global__ void k_pack(const typename vec2<T>::type* __restrict__ buf0, const typename vec2<T>::type* __restrict__ buf1,
-                       const int* __restrict__ iters, const int* __restrict__ parity, double2* __restrict__ dst, int n,
-                       int64_t ss, int64_t total) {
+                       const typename vec2<T>::type* __restrict__ buf2, const int* __restrict__ iters,
+                       const int* __restrict__ parity, double2* __restrict__ dst, int n, int64_t ss, int64_t total) {
   const int m = n - 1;
   const int64_t N = (int64_t)m * m;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = q / N, p = q % N;
     const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
     const int sel = (iters == nullptr) ? 0 : parity[iters[s]];
-    const typename vec2<T>::type* src = sel ? buf1 : buf0;
+    const typename vec2<T>::type* src = sel == 0 ? buf0 : sel == 1 ? buf1 : buf2;
     dst[q] = ld2(src[s * ss + (int64_t)j * n + i]);
   }
 }
@@ -1205,6 +1206,7 @@ struct MarchArgs {
   const V* b;
   const V* ec;
   V* bc;
+  V* u_mid;  // k_march2<MID>: the first sweep's iterate (the previous cycle's final iterate) is stored here
   double* partial;
   const LevelCoef* coef;
   const int* active;
@@ -1513,7 +1515,10 @@ constexpr size_t march2_smem(bool loadu) {
 }
 // NORM_IN: also leave the partial sums of ||b - L u_in||^2 (the first sweep's residual, i.e. the residual of
 // the previous cycle's iterate) in a.partial -- the fine-level convergence norm, read one pass later.
-template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false>
+// MID (V(1,1) cross-cycle fusion): the pass is cycle k's prolongate-and-correct + post-sweep followed by
+// cycle k+1's pre-sweep + restriction; the first sweep's iterate u1 (= cycle k's result) is also stored to
+// a.u_mid and the partials hold ||b - L u1||^2 (the second sweep's residual), i.e. cycle k's residual norm.
+template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool MID = false>
 __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
     k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
@@ -1525,6 +1530,15 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   constexpr int hC = HASD ? hD + 1 : 0;
   constexpr int hA = (hC + 5) & ~1;  // rounded up to even: strips start at even columns
   constexpr int WOUT = 32 * LC - 2 * hA;
+  // the largest variant (prolongation + restriction + mid store) loads b rows j-3 / j-5 inside the step
+  // instead of holding them in prefetch registers (otherwise it spills)
+  constexpr bool B_INSTEP = MID;
+  // NO_EX: lane 31 skips the coarse column beyond its strip, so the prolongation at the strip's last
+  // column (cA + 63, odd) is wrong.  With the restriction's halo (hA = 6) that error reaches u1/u2 at
+  // columns >= cA + 59 and r2 at >= cA + 58 only, outside the stored columns (<= cA + 57) and the stored
+  // coarse points (fine column <= cA + 56): the results are unchanged and 12 registers are saved.
+  constexpr bool NO_EX = PROLONG && POST == POST_RESTRICT;
+  static_assert(!NO_EX || hA >= 6, "NO_EX needs the restriction halo");
   const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
   const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
@@ -1536,6 +1550,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   const int64_t sbase = (int64_t)shift * a.ss;
   const int cA = x0 - hA + LC * lane;
   V* __restrict__ uout = a.u_out + sbase + cA;  // per-lane column pointer (row 0)
+  V* __restrict__ umid = MID ? a.u_mid + sbase + cA : nullptr;
   // ---- TMA ring: slot q holds u_in row r and b row r for r = rlo + q (mod M2_NS) ----------------------
   extern __shared__ __align__(128) unsigned char m2_smem[];
   const int wid = threadIdx.x >> 5;
@@ -1620,7 +1635,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       o = (jok && (unsigned)Ie <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie]) : cz<D2>();
     else
       o = ld2(ecs[(int64_t)J * nc + Ie]);
-    if (lane == 31) x = (jok && (unsigned)(Ie + 1) <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie + 1]) : cz<D2>();
+    if (!NO_EX && lane == 31) x = (jok && (unsigned)(Ie + 1) <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie + 1]) : cz<D2>();
 #endif
   };
   // u_in row `row` (ring) and the prolongation of e_c onto fine row `row` (register window E0/E1, rows
@@ -1670,7 +1685,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
     }
     const D2 a0 = Eo0, b0 = Eo1;
     D2 a1 = shfl_dn2(Eo0), b1 = shfl_dn2(Eo1);
-    if (lane == 31) a1 = Ex0, b1 = Ex1;
+    if (!NO_EX && lane == 31) a1 = Ex0, b1 = Ex1;
     const bool rin = !MASK || row_ok(row);
     // prolong_bilinear (grid.cpp:123-153): even/odd fine column and row (both warp-uniform)
     D2 p[LC];
@@ -1765,8 +1780,14 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       for (int k = 0; k < LC; ++k) {
         Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
         Bc[k] = Bn[k];
-        B3[k] = B3n[k];
-        if constexpr (HASD) B5[k] = B5n[k];
+        if constexpr (!B_INSTEP) {
+          B3[k] = B3n[k];
+          if constexpr (HASD) B5[k] = B5n[k];
+        }
+      }
+      if constexpr (B_INSTEP) {  // (L1 hits: b rows j-3 and j-5 were loaded 2 and 4 steps ago)
+        gload_b(j - 3, B3, MK);
+        if constexpr (HASD) gload_b(j - 5, B5, MK);
       }
       if constexpr (M2_PD > 1) {
 #pragma unroll
@@ -1783,8 +1804,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
           gload_b(j, Bn, MK);
         }
         if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
-        gload_b(j - 2, B3n, MK);
-        if constexpr (HASD) gload_b(j - 4, B5n, MK);
+        if constexpr (!B_INSTEP) {
+          gload_b(j - 2, B3n, MK);
+          if constexpr (HASD) gload_b(j - 4, B5n, MK);
+        }
       }
       if (j + M2_PF < rhi) l2_ahead(j + M2_PF);
     }
@@ -1802,17 +1825,28 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
         }
       }
       vanka_row(r, P1, C1, row_in(j - 2), dl, MK);
+      const bool rst1 = MID && j - 2 >= olo && j - 2 < ohi;
 #pragma unroll
       for (int k = 0; k < LC; ++k) {
         D2 u1 = cadd(U0[so][k], dl[k]);
         if constexpr (EVEN) u1 = ld2(st2<V>(u1));  // the iterate the unfused sweep would have stored
         U1[sn][k] = u1;
+        if constexpr (MID) {
+          if (rst1 && cst[k]) umid[(int64_t)(j - 2) * n + k] = st2<V>(u1);
+        }
       }
     }
     // ---- sweep 2: r' = b - L u1 at j-3, delta2 / u2 at j-4 (stored) ----------------------------------
     {
       D2 r[LC], dl[LC];
       resid(U1[so], U1[sm], U1[sn], B3, row_in(j - 3), r, MK);
+      if constexpr (MID) {  // ||b - L u1||^2 over the owned rows/columns: the residual of cycle k's iterate
+        if (j - 3 >= olo && j - 3 < ohi) {
+#pragma unroll
+          for (int k = 0; k < LC; ++k)
+            if (cst[k]) nacc += r[k].x * r[k].x + r[k].y * r[k].y;
+        }
+      }
       const int row = j - 4;
       vanka_row(r, P2, C2, row_in(row), dl, MK);
       const bool rst = row >= olo && row < ohi;
@@ -1872,7 +1906,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   //  (a) every step unrolled by 3 over the window phases, each with a masked and an unmasked copy;
   //  (b) boundary steps one at a time in window phase 0 followed by a register rotation, interior steps
   //      unmasked and unrolled by 3 -- only unmasked copies in the hot loop (smaller code).
-  if (PROLONG || a.loop_a) {
+  if ((PROLONG && !MID) || (!MID && a.loop_a)) {  // (MID: shape (b) only -- one loop shape keeps it under 255 registers)
     auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
       if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
       else step(j, PH, IC<1>{});
@@ -1922,7 +1956,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       adv();
     }
   }
-  if constexpr (POST == POST_NORM || NORM_IN) {
+  if constexpr (POST == POST_NORM || NORM_IN || MID) {
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
     if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
   }

@@ -347,7 +347,10 @@ class BatchedMultigridHierarchy:
             la, ms, by = C.c_int64(), C.c_double(), C.c_double()
             if N.lib().pdmg_kernel_stats(self._h, i, name, 128, C.byref(la), C.byref(ms), C.byref(by)):
                 break
-            out[name.value.decode()] = dict(launches=la.value, ms=ms.value, bytes=by.value)
+            ub, nu = C.c_double(), C.c_double()
+            N.lib().pdmg_kernel_updates(self._h, i, C.byref(ub), C.byref(nu))
+            out[name.value.decode()] = dict(launches=la.value, ms=ms.value, bytes=by.value, unit_bytes=ub.value,
+                                            updates=nu.value)
             i += 1
         return out
 

@@ -88,10 +88,15 @@ def test_one_cycle_parity(oracle, cyc):
         assert rel(out[s], oracle.cycle(n, lam, cyc, u[s], b[s])) < 1e-12
 
 
-def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10, path="auto"):
+def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10, path="auto", expect_kernel=None):
     with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, mgcfg(cfg)) as H:
         H.set_solve_path(path)
+        if expect_kernel:
+            H.set_profiling(True)
         u, reps = H.solve(b)
+        if expect_kernel:
+            names = list(H.kernel_stats())
+            assert any(expect_kernel in k for k in names), names
     ref = oracle.solve_batch(n, np.asarray(lams, np.complex128), cfg, b, threads=8)
     for s in range(len(lams)):
         it = int(ref["iterations"][s])
@@ -277,3 +282,17 @@ def test_norm_next_mixed_convergence(oracle):
         u, reps, ref = _check_solve(oracle, n, lams, b, cyc, path="batched")
         assert reps[1].iterations == 0 and np.all(u[1] == 0)
         assert len(set(r.iterations for r in reps)) >= 2
+
+
+@pytest.mark.parametrize("cyc", [Cfg(nu1=1, nu2=1), Cfg(nu1=1, nu2=1, cycle="W"), Cfg(nu1=1, nu2=1, tol=1e-14, max_iter=3)])
+def test_xfuse_matches_oracle(oracle, monkeypatch, cyc):
+    """V(1,1) cross-cycle fusion (PDMG_XFUSE=1): cycle k's fine post-sweep and cycle k+1's pre-sweep run as
+    one k_march2<MID> pass that also stores u_k and forms ||b - L u_k||; mixed convergence (b = 0, an easy
+    and a hard shift) and max_iter exhaustion must reproduce the oracle's counts, histories and iterates."""
+    monkeypatch.setenv("PDMG_XFUSE", "1")
+    n, m = 128, 127
+    lams = [5000 + 0j, 0.0, 0.0, 8.959263353215057 - 15.395328029306036j]
+    b = oracle.random_complex(43, 4 * m * m).reshape(4, m, m)
+    b[1] = 0
+    u, reps, ref = _check_solve(oracle, n, lams, b, cyc, path="batched", expect_kernel="+mid")
+    assert reps[1].iterations == 0 and np.all(u[1] == 0)
