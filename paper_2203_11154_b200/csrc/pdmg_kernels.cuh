@@ -224,13 +224,6 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, un
       : "memory");
 }
 
-// Bulk prefetch of [p, p + bytes) into L2 (no registers, no completion): the marching kernels issue it a
-// few rows ahead so the row loads a step later hit L2 instead of waiting a full HBM round trip.  p and
-// bytes must be 16-byte aligned / multiples.
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
-
 // Halo widths and shared-memory footprint of a k_level instantiation.  Rings fed by TMA (u_in, b, e_c)
 // hold the storage type; r, delta and the restriction sums hold fp64.  With 8-byte elements the TMA-fed
 // buffers start at an even column (16-byte aligned segments), so their halos are rounded up to even.
@@ -1489,29 +1482,11 @@ struct IC {
 #ifndef PDMG_MARCH2_MINB
 #define PDMG_MARCH2_MINB 2
 #endif
-#ifndef PDMG_MARCH2_D
-#define PDMG_MARCH2_D 4
-#endif
-#ifndef PDMG_MARCH2_TMA
-#define PDMG_MARCH2_TMA 0
-#endif
-#ifndef PDMG_MARCH2_PF
-#define PDMG_MARCH2_PF 0
-#endif
-constexpr int M2_PF = PDMG_MARCH2_PF;  // L2 prefetch distance (rows), 0 = off
-#ifndef PDMG_MARCH2_PD
-#define PDMG_MARCH2_PD 1
-#endif
-constexpr int M2_PD = PDMG_MARCH2_PD;  // register prefetch distance of the u_in / b rows (1 or 2 steps)
-constexpr bool M2_TMA = PDMG_MARCH2_TMA;  // input rows via the TMA ring (1) or register prefetch (0)
-constexpr int M2_D = PDMG_MARCH2_D;  // rows in flight per warp
-constexpr int M2_NS = M2_D + 6;      // ring slots: rows j-5 .. j+D
-constexpr int M2_ROWW = 68;          // ring row width (64 columns + even-alignment slack for 8-byte elements)
+// (measured and removed, DESIGN 3.2b: input rows through a TMA ring in shared memory, L2 bulk prefetch,
+// register prefetch two rows ahead -- all slower than the one-row register prefetch)
 template <class T>
-constexpr size_t march2_smem(bool loadu) {
-  if (!M2_TMA) return 0;
-  return (size_t)MARCH_WARPS * M2_NS * 8 + (size_t)MARCH_WARPS * M2_NS * M2_ROWW * sizeof(typename vec2<T>::type) *
-                                               (loadu ? 2 : 1);
+constexpr size_t march2_smem(bool) {
+  return 0;
 }
 // NORM_IN: also leave the partial sums of ||b - L u_in||^2 (the first sweep's residual, i.e. the residual of
 // the previous cycle's iterate) in a.partial -- the fine-level convergence norm, read one pass later.
@@ -1551,15 +1526,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   const int cA = x0 - hA + LC * lane;
   V* __restrict__ uout = a.u_out + sbase + cA;  // per-lane column pointer (row 0)
   V* __restrict__ umid = MID ? a.u_mid + sbase + cA : nullptr;
-  // ---- TMA ring: slot q holds u_in row r and b row r for r = rlo + q (mod M2_NS) ----------------------
-  extern __shared__ __align__(128) unsigned char m2_smem[];
-  const int wid = threadIdx.x >> 5;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(m2_smem) + wid * M2_NS;
-  V* ring_b = reinterpret_cast<V*>(m2_smem + MARCH_WARPS * M2_NS * 8) + (size_t)wid * M2_NS * M2_ROWW * (LOADU ? 2 : 1);
-  V* ring_u = ring_b + M2_NS * M2_ROWW;  // LOADU only
-  const int cs = (x0 - hA) & (EVEN ? ~1 : ~0);  // first ring column (even for 8-byte elements)
-  const int lofs = (x0 - hA) - cs + LC * lane;  // this lane's first column within a ring row
-  const int c_lo = max(cs, 0), c_hi = min(cs + M2_ROWW, n);
   const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
   const LevelCoef cf = coef_of(cp);
 
@@ -1575,49 +1541,13 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   auto row_in = [&](int row) __attribute__((always_inline)) { return (unsigned)(row - 1) < (unsigned)m; };
   // rows before rlo are never loaded: they read as zero (they only reach halo rows, which are not stored)
   auto row_ok = [&](int row) __attribute__((always_inline)) { return row_in(row) && row >= rlo; };
-  const V* __restrict__ uin = a.u_in + sbase + cA;  // register-prefetch path: per-lane column pointers
+  const V* __restrict__ uin = a.u_in + sbase + cA;  // per-lane column pointers
   const V* __restrict__ bb = a.b + sbase + cA;
-  if (M2_TMA && lane == 0) {
-    for (int q = 0; q < M2_NS; ++q) mbar_init(&bars[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncwarp();
-  // ring slot of row rlo + i is i mod M2_NS; qj = slot of the current row j, pj = its mbarrier phase
-  int qj = 0, pj = 0;
-  auto wrap = [&](int q) __attribute__((always_inline)) { return q >= M2_NS ? q - M2_NS : (q < 0 ? q + M2_NS : q); };
-  auto issue_q = [&](int row, int q) __attribute__((always_inline)) {  // lane 0: TMA of u_in and b row into slot q
-    if (lane != 0) return;
-    const bool ok = row_in(row) && c_hi > c_lo;
-    const unsigned bytes = ok ? (unsigned)((c_hi - c_lo) * sizeof(V)) : 0u;
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_arrive_expect_tx(&bars[q], LOADU ? 2 * bytes : bytes);
-    if (ok) {
-      const int64_t g = sbase + (int64_t)row * n + c_lo;
-      tma_load_1d(ring_b + q * M2_ROWW + (c_lo - cs), a.b + g, bytes, &bars[q]);
-      if constexpr (LOADU) tma_load_1d(ring_u + q * M2_ROWW + (c_lo - cs), a.u_in + g, bytes, &bars[q]);
-    }
-  };
-  // ring element of row j - back (back = 0, 1, 3, 5: slots relative to qj)
-  auto ring_at = [&](const V* ring, int back, int k) __attribute__((always_inline)) {
-    return ld2(ring[wrap(qj - back) * M2_ROWW + lofs + k]);
-  };
   // warp-uniform: every column of the strip (and its coarse prolongation columns) is interior
   const bool col_int = (x0 - hA >= 1) && (x0 - hA + 32 * LC + 1 <= m - 1);
   // steps j in [jlo_int, jhi_int] touch only interior rows (loads j-5 .. j+1, coarse rows up to (j+1)/2+1)
   const int jlo_int = max(6, rlo + 5), jhi_int = m - 3;  // (register path: loads reach j+1 and j-4)
 
-  // L2 prefetch of the u_in and b rows M2_PF steps ahead (lane 0, one bulk request per row and array): the
-  // register prefetch one step ahead does not cover a loaded HBM round trip (ncu: long-scoreboard stalls
-  // on the first use of every prefetched row)
-  const int pc0 = max(cs, 0), pc1 = min(cs + 32 * LC + (EVEN ? 2 : 0), n);
-  const unsigned pbytes = pc1 > pc0 ? (unsigned)((pc1 - pc0) * sizeof(V)) & ~15u : 0u;
-  auto l2_ahead = [&](int row) __attribute__((always_inline)) {
-    if (lane == 0 && M2_PF > 0 && pbytes != 0 && (unsigned)row <= (unsigned)m) {
-      const int64_t g = sbase + (int64_t)row * n + pc0;
-      if constexpr (LOADU) prefetch_l2(a.u_in + g, pbytes);
-      if (row >= 1) prefetch_l2(a.b + g - n, pbytes);
-    }
-  };
   // prolongation window: coarse rows J, J+1 (in use) and J+2 (prefetched) at this lane's coarse column Ie;
   // the column Ie+1 comes from the next lane (lane 31 loads it itself)
   D2 Eo0 = cz<D2>(), Eo1 = cz<D2>(), Eo2 = cz<D2>(), Ex0 = cz<D2>(), Ex1 = cz<D2>(), Ex2 = cz<D2>();
@@ -1638,18 +1568,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
     if (!NO_EX && lane == 31) x = (jok && (unsigned)(Ie + 1) <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie + 1]) : cz<D2>();
 #endif
   };
-  // u_in row `row` (ring) and the prolongation of e_c onto fine row `row` (register window E0/E1, rows
-  // visited in increasing order; computed a step ahead so the coarse loads are not waited on)
-  auto read_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
-#pragma unroll
-    for (int k = 0; k < LC; ++k) {
-      out[k] = cz<D2>();
-      if constexpr (LOADU) {
-        if (!MASK || (row_ok(row) && cin[k])) out[k] = ring_at(ring_u, 0, k);
-      }
-    }
-  };
+  // u_in row `row`, and the prolongation of e_c onto fine row `row` (register window E0/E1, rows visited
+  // in increasing order; computed a step ahead so the coarse loads are not waited on)
   auto gread_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value;
 #pragma unroll
@@ -1731,8 +1651,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
 
   D2 U0[3][LC], U1[3][LC], U2[3][LC];
   D2 P1[LC], C1[LC], P2[LC], C2[LC], Vp[LC];
-  D2 Pn[LC], Unx[LC], Bn[LC], B3n[LC], B5n[LC];  // (the last four: register-prefetch path only)
-  D2 Unx2[M2_PD > 1 ? LC : 1], Bn2[M2_PD > 1 ? LC : 1];  // rows j+2 / j+1 (prefetch distance 2)
+  // rows prefetched one step ahead (indexing these by window phase, so a step reads one slot and loads the
+  // next, was measured to make ptxas keep three copies live and spill)
+  D2 Pn[LC], Unx[LC], Bn[LC], B3n[LC], B5n[LC];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -1740,16 +1661,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
 #pragma unroll
   for (int k = 0; k < LC; ++k) P1[k] = C1[k] = P2[k] = C2[k] = Vp[k] = cz<D2>();
   double nacc = 0.0;
-  if constexpr (M2_TMA) {
-    for (int r = rlo; r < min(rlo + M2_D, rhi); ++r) issue_q(r, r - rlo);
-  } else {
-    for (int r = rlo + 1; r < min(rlo + M2_PF, rhi); ++r) l2_ahead(r);
-    gread_u(rlo, Unx, IC<1>{});
-    gload_b(rlo - 1, Bn, IC<1>{});
-    if constexpr (M2_PD > 1) {
-      gread_u(rlo + 1, Unx2, IC<1>{});
-      gload_b(rlo, Bn2, IC<1>{});
-    }
+  gread_u(rlo, Unx, IC<1>{});
+  gload_b(rlo - 1, Bn, IC<1>{});
+  if constexpr (!B_INSTEP) {
     gload_b(rlo - 3, B3n, IC<1>{});
     if constexpr (HASD) gload_b(rlo - 5, B5n, IC<1>{});
   }
@@ -1761,55 +1675,27 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
     constexpr int so = ph % 3, sm = (ph + 1) % 3, sn = (ph + 2) % 3;
     // ---- loads: u0 row j (prefetched last step), prefetch u0 row j+1 and b row j; b rows j-3, j-5 ----
     D2 B3[LC], B5[LC], Bc[LC], Un[LC];
-    if constexpr (M2_TMA) {
-      __syncwarp();  // every lane is done with the slot row j + D - M2_NS last held (read at step j-1)
-      if (j + M2_D < rhi) issue_q(j + M2_D, wrap(qj + M2_D));
-      mbar_wait(&bars[qj], pj);
-      load_b(j, 1, Bc, MK);
-      load_b(j, 3, B3, MK);
-      if constexpr (HASD) load_b(j, 5, B5, MK);
-      read_u(j, Un, MK);
 #pragma unroll
-      for (int k = 0; k < LC; ++k)
-        if constexpr (PROLONG) Un[k] = cadd(Un[k], Pn[k]);
-      if constexpr (PROLONG) {
-        if (j + 1 < rhi) prolong_row(j + 1, Pn, MK);
+    for (int k = 0; k < LC; ++k) {
+      Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
+      Bc[k] = Bn[k];
+      if constexpr (!B_INSTEP) {
+        B3[k] = B3n[k];
+        if constexpr (HASD) B5[k] = B5n[k];
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < LC; ++k) {
-        Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
-        Bc[k] = Bn[k];
-        if constexpr (!B_INSTEP) {
-          B3[k] = B3n[k];
-          if constexpr (HASD) B5[k] = B5n[k];
-        }
+    }
+    if constexpr (B_INSTEP) {  // (L1 hits: b rows j-3 and j-5 were loaded 2 and 4 steps ago)
+      gload_b(j - 3, B3, MK);
+      if constexpr (HASD) gload_b(j - 5, B5, MK);
+    }
+    if (j + 1 < rhi) {
+      gread_u(j + 1, Unx, MK);
+      gload_b(j, Bn, MK);
+      if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
+      if constexpr (!B_INSTEP) {
+        gload_b(j - 2, B3n, MK);
+        if constexpr (HASD) gload_b(j - 4, B5n, MK);
       }
-      if constexpr (B_INSTEP) {  // (L1 hits: b rows j-3 and j-5 were loaded 2 and 4 steps ago)
-        gload_b(j - 3, B3, MK);
-        if constexpr (HASD) gload_b(j - 5, B5, MK);
-      }
-      if constexpr (M2_PD > 1) {
-#pragma unroll
-        for (int k = 0; k < LC; ++k) Unx[k] = Unx2[k], Bn[k] = Bn2[k];
-      }
-      if (j + 1 < rhi) {
-        if constexpr (M2_PD > 1) {
-          if (j + 2 < rhi) {
-            gread_u(j + 2, Unx2, MK);
-            gload_b(j + 1, Bn2, MK);
-          }
-        } else {
-          gread_u(j + 1, Unx, MK);
-          gload_b(j, Bn, MK);
-        }
-        if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
-        if constexpr (!B_INSTEP) {
-          gload_b(j - 2, B3n, MK);
-          if constexpr (HASD) gload_b(j - 4, B5n, MK);
-        }
-      }
-      if (j + M2_PF < rhi) l2_ahead(j + M2_PF);
     }
 #pragma unroll
     for (int k = 0; k < LC; ++k) U0[sn][k] = Un[k];
@@ -1878,8 +1764,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
             Vp[k] = r2[k];
           }
           const int J = (row - 1) >> 1;
+          // (shuffles outside the task-dependent test: no divergence check around them)
+          const D2 vwl = shfl_up2(v[LC - 1]), ver = shfl_dn2(v[0]);
           if (row >= r0 + 1 && row <= r0 + Hs && J >= 1 && J <= nc - 1) {
-            const D2 vwl = shfl_up2(v[LC - 1]), ver = shfl_dn2(v[0]);
 #pragma unroll
             for (int k = 0; k < LC; ++k) {
               const int c = cA + k;
@@ -1899,9 +1786,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       }
     }
   };
-  auto adv = [&]() __attribute__((always_inline)) {
-    if (++qj == M2_NS) qj = 0, pj ^= 1;
-  };
   // Two loop shapes (measured per variant on B200, the prolongating passes prefer the first):
   //  (a) every step unrolled by 3 over the window phases, each with a masked and an unmasked copy;
   //  (b) boundary steps one at a time in window phase 0 followed by a register rotation, interior steps
@@ -1910,7 +1794,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
     auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
       if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
       else step(j, PH, IC<1>{});
-      adv();
     };
     int j = rlo;
     for (; j + 2 < rhi; j += 3) {
@@ -1935,25 +1818,19 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
     for (; j < jm_lo; ++j) {  // leading boundary steps
       step(j, IC<0>{}, IC<1>{});
       rotate();
-      adv();
     }
     for (; j + 2 < jm_end; j += 3) {
       step(j, IC<0>{}, IC<0>{});
-      adv();
       step(j + 1, IC<1>{}, IC<0>{});
-      adv();
       step(j + 2, IC<2>{}, IC<0>{});
-      adv();
     }
     for (; j < jm_end; ++j) {
       step(j, IC<0>{}, IC<0>{});
       rotate();
-      adv();
     }
     for (; j < rhi; ++j) {  // trailing boundary steps
       step(j, IC<0>{}, IC<1>{});
       rotate();
-      adv();
     }
   }
   if constexpr (POST == POST_NORM || NORM_IN || MID) {
