@@ -350,6 +350,20 @@ struct March2Table {
     reg<false, false, POST_NONE, true>();
     reg<true, false, POST_NONE, true>();
     reg<true, true, POST_RESTRICT, false, true>();  // V(1,1) cross-cycle fusion
+    reg1<false>();
+    reg1<true>();
+  }
+  // one-sweep passes (k_march2<..., TWO = false>), same keys
+  void (*e1[64])(MarchArgs<T>, CoefPack) = {};
+  template <bool LU>
+  void reg1() {
+    e1[key(LU, false, POST_NONE)] = &k_march2<T, LU, false, POST_NONE, false, false, false>;
+    e1[key(LU, false, POST_RESTRICT)] = &k_march2<T, LU, false, POST_RESTRICT, false, false, false>;
+    e1[key(LU, false, POST_NORM)] = &k_march2<T, LU, false, POST_NORM, false, false, false>;
+    e1[key(LU, true, POST_NONE)] = &k_march2<T, LU, true, POST_NONE, false, false, false>;
+    e1[key(LU, true, POST_NORM)] = &k_march2<T, LU, true, POST_NORM, false, false, false>;
+    e1[key(LU, false, POST_RESTRICT, true)] = &k_march2<T, LU, false, POST_RESTRICT, true, false, false>;
+    e1[key(LU, false, POST_NONE, true)] = &k_march2<T, LU, false, POST_NONE, true, false, false>;
   }
 };
 
@@ -457,8 +471,18 @@ struct Engine : EngineBase {
   }
   int march2_min_n = 64;  // levels with n >= this run Vanka sweep pairs as one k_march2 pass (0 = never)
   int march2_hs = 0;      // strip height override (0 = automatic)
+  // per-level strip heights (tuning: PDMG_MARCH2_HS_R / _P = "n:H,n:H,..." for the non-prolongating /
+  // prolongating passes; levels not listed use march2_hs_default)
+  std::vector<std::pair<int, int>> march2_hs_r, march2_hs_p;
+  int march2_prolong_b = 0;  // prolongating passes may use loop shape (b) on levels with n >= march2_loopb_min_n
+  int march2_hs_for(int n, bool prolong) const {
+    if (march2_hs > 0) return march2_hs;
+    for (auto& e : prolong ? march2_hs_p : march2_hs_r)
+      if (e.first == n) return e.second;
+    return n >= 512 ? 128 : n >= 256 ? 64 : 32;  // measured at C3 (DESIGN 3.2b)
+  }
   bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
-  int march2_loopb_min_n = 512;
+  int march2_loopb_min_n = 128;  // (prolongating passes: shape (a), see march2_prolong_b)
   bool march2_ws = false;  // run the pair passes as warp-specialised producer/consumer warp pairs (k_march2ws)
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
   // V(1,1): fuse cycle k's fine post-sweep with cycle k+1's pre-sweep (solve_xfuse).  Off by default:
@@ -494,33 +518,35 @@ struct Engine : EngineBase {
     }
   }
   // two consecutive Vanka sweeps u[cur] -> u[cur^1] (+ prolongation of ec before, + restriction/norm after)
+  // two = false: ONE Vanka sweep through the same kernel (k_march2<..., TWO = false>)
   void level_pass2(int l, bool loadu, bool prolong, int post, const V* uin, V* uout, const V* b, const V* ec, V* bc,
-                   const int* active, int n_act, bool norm_in = false, V* umid = nullptr) {
+                   const int* active, int n_act, bool norm_in = false, V* umid = nullptr, bool two = true) {
     const Level& Lv = lv[l];
     MarchArgs<T> ma{};
     ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial, ma.u_mid = umid;
     ma.coef = Lv.coef, ma.active = active, ma.n = Lv.n;
     ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
     ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
-    const int hA = (4 + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;  // = k_march2 hA
+    const int hA = ((two ? 4 : 2) + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;  // = k_march2 hA
     const int wout = 64 - 2 * hA;
-    ma.Hs = march2_hs > 0 ? march2_hs : (Lv.n >= 512 ? 128 : 64);
-    ma.loop_a = Lv.n < march2_loopb_min_n;  // measured: the split loop wins on the 512+ grids only
+    ma.Hs = march2_hs_for(Lv.n, prolong);
+    // loop shape (a) for prolongating passes unless march2_prolong_b (measured, DESIGN 3.2b)
+    ma.loop_a = Lv.n < march2_loopb_min_n || (prolong && !march2_prolong_b);
     ma.ntx = (Lv.n + wout - 1) / wout;
     ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
     const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in, umid != nullptr);
-    const bool ws = march2_ws && umid == nullptr;
-    auto fn = ws ? marches2().ws[key2] : marches2().e[key2];
-    const size_t smem2 = ws ? 0 : marches2().smem[key2];
+    const bool ws = two && march2_ws && umid == nullptr;
+    auto fn = !two ? marches2().e1[key2] : ws ? marches2().ws[key2] : marches2().e[key2];
+    const size_t smem2 = ws || !two ? 0 : marches2().smem[key2];
     if (!fn) throw std::logic_error("pdmg_b200: no two-sweep kernel for this variant");
     const double S_ = sizeof(V), pts = (double)n_act * Lv.m * Lv.m;
     const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0) +
                        (umid ? S_ : 0);
     std::string cls = "L" + std::to_string(l) + ":" + (prolong ? (loadu ? "prolong+" : "prolong0+") : (loadu ? "" : "zero+")) +
-                      "vanka2" + (post == POST_NORM ? "+norm" : post == POST_RESTRICT ? "+restrict" : "") +
+                      (two ? "vanka2" : "vanka") + (post == POST_NORM ? "+norm" : post == POST_RESTRICT ? "+restrict" : "") +
                       (norm_in ? "+norm_in" : "") + (umid ? "+mid" : "");
     const int per_cta = ws ? WS_PAIRS : MARCH_WARPS;
-    const double ubpp = 2 * 3 * S_ + (prolong ? S_ / 4 : 0) + (post == POST_RESTRICT ? S_ / 4 : 0) + (umid ? S_ : 0);
+    const double ubpp = (two ? 2 : 1) * 3 * S_ + (prolong ? S_ / 4 : 0) + (post == POST_RESTRICT ? S_ / 4 : 0) + (umid ? S_ : 0);
     timed(cls, pts * bpp, [&] {
       for (int c0 = 0; c0 < S; c0 += COEF_MAX) {  // one launch per COEF_MAX shifts (coefficients as parameters)
         const int cnt = std::min(COEF_MAX, S - c0);
@@ -528,12 +554,19 @@ struct Engine : EngineBase {
         dim3 grid((ma.ntasks + per_cta - 1) / per_cta, cnt);
         fn<<<grid, ws ? WS_THREADS : 32 * MARCH_WARPS, smem2, stream>>>(ma, *cpack);
       }
-    }, pts * ubpp, 2 * pts);
+    }, pts * ubpp, (two ? 2 : 1) * pts);
     last_partials = ma.ntasks;
   }
   // measured on B200 (C3, C4): the marcher wins for sweep+norm and sweep+restrict, the ring
   // kernel for the plain and prolongating sweeps; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher
   bool march_all = false;
+  // single Vanka sweeps on levels with n >= march2_min_n through k_march2<TWO = false> (PDMG_MARCH1=0: the
+  // older k_level / k_march kernels)
+  bool march1 = true;
+  bool use_march1(int l, const Variant& v) const {
+    return march1 && march2_min_n > 0 && lv[l].n >= march2_min_n && v.sweep && v.store && !v.jacobi &&
+           v.post != POST_RESID && marches2().e1[March2Table<T>::key(v.loadu, v.prolong, v.post)] != nullptr;
+  }
   bool use_march(int l, const Variant& v) const {
     if (!(march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store && v.post != POST_RESID)) return false;
     if (march_all) return true;
@@ -628,6 +661,18 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH2_MIN_N")) march2_min_n = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH2_HS")) march2_hs = std::atoi(e);
+    auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
+      out.clear();
+      for (const char* q = e; *q;) {
+        int n = 0, h = 0;
+        if (std::sscanf(q, "%d:%d", &n, &h) == 2 && n > 0 && h > 0) out.emplace_back(n, h);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    };
+    if (const char* e = std::getenv("PDMG_MARCH2_HS_R")) parse_hs(e, march2_hs_r);
+    if (const char* e = std::getenv("PDMG_MARCH2_HS_P")) parse_hs(e, march2_hs_p);
+    if (const char* e = std::getenv("PDMG_MARCH2_PROLONG_B")) march2_prolong_b = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH2_PRE")) march2_pre = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH2_POST")) march2_post = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_NORM_NEXT")) norm_next = std::atoi(e) != 0;
@@ -636,6 +681,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH2_WS")) march2_ws = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_MARCH1")) march1 = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
@@ -810,6 +856,10 @@ struct Engine : EngineBase {
     // a smoother update is 3 S (u in, b in, u out) whatever the pass actually moves
     const double ubpp = v.sweep ? 3 * S_ + (v.prolong ? S_ / 4 : 0) + (v.post == POST_RESTRICT ? S_ / 4 : 0) : -1.0;
     const double ub = ubpp < 0 ? -1.0 : pts * ubpp, nupd = v.sweep ? pts : 0.0;
+    if (use_march1(l, v)) {
+      level_pass2(l, v.loadu, v.prolong, v.post, uin, uout, b, ec, bc, active, n_act, norm_in, nullptr, false);
+      return;
+    }
     if (norm_in && !use_march(l, v)) throw std::logic_error("pdmg_b200: norm_in needs the marching kernel");
     if (use_march(l, v)) {
       MarchArgs<T> ma{};

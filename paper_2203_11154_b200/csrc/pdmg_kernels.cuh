@@ -1493,21 +1493,32 @@ constexpr size_t march2_smem(bool) {
 // MID (V(1,1) cross-cycle fusion): the pass is cycle k's prolongate-and-correct + post-sweep followed by
 // cycle k+1's pre-sweep + restriction; the first sweep's iterate u1 (= cycle k's result) is also stored to
 // a.u_mid and the partials hold ||b - L u1||^2 (the second sweep's residual), i.e. cycle k's residual norm.
-template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool MID = false>
-__global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
+// TWO = false: ONE Vanka sweep per pass with the same machinery (the single-sweep passes of V(1,1) and odd
+// nu): u1 at row j-2 is the stored iterate and the post stage reads r2 = b - L u1 at row j-3.
+#ifndef PDMG_MARCH1_MINB
+#define PDMG_MARCH1_MINB 3
+#endif
+template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool MID = false, bool TWO = true>
+__global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB)
     k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
   using D2 = double2;
   constexpr int LC = 2;
   constexpr bool EVEN = sizeof(V) == 8;
   constexpr bool HASD = POST != POST_NONE;
+  static_assert(TWO || !MID, "the cross-cycle pass is a two-sweep pass");
   constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
   constexpr int hC = HASD ? hD + 1 : 0;
-  constexpr int hA = (hC + 5) & ~1;  // rounded up to even: strips start at even columns
+  // 2 halo columns/rows per sweep (residual + Vanka patch) + the post stage, rounded up to even (strips
+  // start at even columns)
+  constexpr int hA = (hC + (TWO ? 4 : 2) + 1) & ~1;
   constexpr int WOUT = 32 * LC - 2 * hA;
   // the largest variant (prolongation + restriction + mid store) loads b rows j-3 / j-5 inside the step
   // instead of holding them in prefetch registers (otherwise it spills)
-  constexpr bool B_INSTEP = MID;
+#ifndef PDMG_M2_BINSTEP
+#define PDMG_M2_BINSTEP 0
+#endif
+  constexpr bool B_INSTEP = MID || (PDMG_M2_BINSTEP && TWO);
   // NO_EX: lane 31 skips the coarse column beyond its strip, so the prolongation at the strip's last
   // column (cA + 63, odd) is wrong.  With the restriction's halo (hA = 6) that error reaches u1/u2 at
   // columns >= cA + 59 and r2 at >= cA + 58 only, outside the stored columns (<= cA + 57) and the stored
@@ -1547,6 +1558,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   const bool col_int = (x0 - hA >= 1) && (x0 - hA + 32 * LC + 1 <= m - 1);
   // steps j in [jlo_int, jhi_int] touch only interior rows (loads j-5 .. j+1, coarse rows up to (j+1)/2+1)
   const int jlo_int = max(6, rlo + 5), jhi_int = m - 3;  // (register path: loads reach j+1 and j-4)
+  // (one sweep: the b rows read are j-1 and j-3 only)
+  constexpr bool NEED_B3 = TWO || HASD, NEED_B5 = TWO && HASD;
 
   // prolongation window: coarse rows J, J+1 (in use) and J+2 (prefetched) at this lane's coarse column Ie;
   // the column Ie+1 comes from the next lane (lane 31 loads it itself)
@@ -1664,8 +1677,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   gread_u(rlo, Unx, IC<1>{});
   gload_b(rlo - 1, Bn, IC<1>{});
   if constexpr (!B_INSTEP) {
-    gload_b(rlo - 3, B3n, IC<1>{});
-    if constexpr (HASD) gload_b(rlo - 5, B5n, IC<1>{});
+    if constexpr (NEED_B3) gload_b(rlo - 3, B3n, IC<1>{});
+    if constexpr (NEED_B5) gload_b(rlo - 5, B5n, IC<1>{});
   }
   if constexpr (PROLONG) prolong_row(rlo, Pn, IC<1>{});
 
@@ -1680,8 +1693,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
       Bc[k] = Bn[k];
       if constexpr (!B_INSTEP) {
-        B3[k] = B3n[k];
-        if constexpr (HASD) B5[k] = B5n[k];
+        if constexpr (NEED_B3) B3[k] = B3n[k];
+        if constexpr (NEED_B5) B5[k] = B5n[k];
       }
     }
     if constexpr (B_INSTEP) {  // (L1 hits: b rows j-3 and j-5 were loaded 2 and 4 steps ago)
@@ -1693,8 +1706,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       gload_b(j, Bn, MK);
       if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
       if constexpr (!B_INSTEP) {
-        gload_b(j - 2, B3n, MK);
-        if constexpr (HASD) gload_b(j - 4, B5n, MK);
+        if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
+        if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
       }
     }
 #pragma unroll
@@ -1711,7 +1724,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
         }
       }
       vanka_row(r, P1, C1, row_in(j - 2), dl, MK);
-      const bool rst1 = MID && j - 2 >= olo && j - 2 < ohi;
+      const bool rst1 = (MID || !TWO) && j - 2 >= olo && j - 2 < ohi;
 #pragma unroll
       for (int k = 0; k < LC; ++k) {
         D2 u1 = cadd(U0[so][k], dl[k]);
@@ -1720,10 +1733,13 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
         if constexpr (MID) {
           if (rst1 && cst[k]) umid[(int64_t)(j - 2) * n + k] = st2<V>(u1);
         }
+        if constexpr (!TWO) {
+          if (rst1 && cst[k]) uout[(int64_t)(j - 2) * n + k] = st2<V>(u1);
+        }
       }
     }
     // ---- sweep 2: r' = b - L u1 at j-3, delta2 / u2 at j-4 (stored) ----------------------------------
-    {
+    if constexpr (TWO) {
       D2 r[LC], dl[LC];
       resid(U1[so], U1[sm], U1[sn], B3, row_in(j - 3), r, MK);
       if constexpr (MID) {  // ||b - L u1||^2 over the owned rows/columns: the residual of cycle k's iterate
@@ -1744,10 +1760,11 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
       }
     }
     if constexpr (HASD) {
-      // ---- r2 = b - L u2 at j-5: norm or restriction (grid.cpp:102-121) ------------------------------
-      const int row = j - 5;
+      // ---- r2 = b - L u2 at j-5 (one sweep: b - L u1 at j-3): norm or restriction (grid.cpp:102-121) ----
+      const int row = TWO ? j - 5 : j - 3;
       D2 r2[LC];
-      resid(U2[so], U2[sm], U2[sn], B5, row_in(row), r2, MK);
+      if constexpr (TWO) resid(U2[so], U2[sm], U2[sn], B5, row_in(row), r2, MK);
+      else resid(U1[so], U1[sm], U1[sn], B3, row_in(row), r2, MK);
       if constexpr (POST == POST_NORM) {
         if (row >= olo && row < ohi) {
 #pragma unroll
@@ -1790,7 +1807,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH2_MINB)
   //  (a) every step unrolled by 3 over the window phases, each with a masked and an unmasked copy;
   //  (b) boundary steps one at a time in window phase 0 followed by a register rotation, interior steps
   //      unmasked and unrolled by 3 -- only unmasked copies in the hot loop (smaller code).
-  if ((PROLONG && !MID) || (!MID && a.loop_a)) {  // (MID: shape (b) only -- one loop shape keeps it under 255 registers)
+  // (MID: shape (b) only -- one loop shape keeps it under 255 registers; prolongating passes with a
+  //  post stage: shape (a) only -- both shapes in one function spill)
+  if (!MID && (a.loop_a || (PROLONG && POST != POST_NONE))) {
     auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
       if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
       else step(j, PH, IC<1>{});

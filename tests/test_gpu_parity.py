@@ -174,6 +174,22 @@ def test_two_sweep_passes_ragged(oracle, cyc):
     _check_solve(oracle, n, lams, b, cfg, path="batched")
 
 
+@pytest.mark.parametrize("march1", ["1", "0"])
+@pytest.mark.parametrize("cyc", [Cfg(nu1=1, nu2=1), Cfg(nu1=1, nu2=2), Cfg(nu1=3, nu2=1), Cfg(nu1=1, nu2=1, cycle="W"),
+                                 Cfg(nu1=0, nu2=1)])
+def test_single_sweep_passes_ragged(oracle, monkeypatch, cyc, march1):
+    """Single Vanka sweeps on levels n >= 64 run through the marching kernel in its one-sweep form
+    (k_march2<TWO = false>: sweep + restriction / norm / norm of the input iterate, prolongation + sweep);
+    PDMG_MARCH1=0 routes them to the older k_level / k_march kernels.  Ragged strips (n = 200), V/W cycles
+    with odd nu, against the oracle."""
+    monkeypatch.setenv("PDMG_MARCH1", march1)
+    n, m = 200, 199
+    lams = [0.0, 8.959263353215057 - 15.395328029306036j, 300 - 40j]
+    b = oracle.random_complex(32, 3 * m * m).reshape(3, m, m)
+    cfg = Cfg(nu1=cyc.nu1, nu2=cyc.nu2, cycle=cyc.cycle, coarsest_n=25)
+    _check_solve(oracle, n, lams, b, cfg, path="batched")
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_edge_cases(oracle, path):
     """multigrid test 'report edge cases' (test_multigrid.cpp:128-163) on the GPU path."""
