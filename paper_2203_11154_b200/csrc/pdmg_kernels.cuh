@@ -1475,6 +1475,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
 // enough bytes moving to saturate HBM at 8 warps/SM, without spending registers on prefetch.  b rows stay
 // in the ring until the second sweep (row j-3) and the post-residual (row j-5) have read them.
 // ===================================================================================================
+__device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <int X>
 struct IC {
   static constexpr int value = X;
@@ -1519,6 +1520,12 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
 #define PDMG_M2_BINSTEP 0
 #endif
   constexpr bool B_INSTEP = MID || (PDMG_M2_BINSTEP && TWO);
+  // L2 prefetch distance in rows (0 = none).  Measured at C3 (DESIGN 3.2b): 2 rows ahead speeds up the
+  // non-prolongating pairs and the one-sweep passes and slows the prolongating pairs, which keep none.
+#ifndef PDMG_M2_PF
+#define PDMG_M2_PF 2
+#endif
+  constexpr int M2_PF = (TWO && PROLONG) ? 0 : PDMG_M2_PF;
   // NO_EX: lane 31 skips the coarse column beyond its strip, so the prolongation at the strip's last
   // column (cA + 63, odd) is wrong.  With the restriction's halo (hA = 6) that error reaches u1/u2 at
   // columns >= cA + 59 and r2 at >= cA + 58 only, outside the stored columns (<= cA + 57) and the stored
@@ -1702,6 +1709,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
       if constexpr (HASD) gload_b(j - 5, B5, MK);
     }
     if (j + 1 < rhi) {
+      if constexpr (M2_PF > 0) {  // L2 prefetch of the rows M2_PF steps ahead (one hint per lane)
+        if constexpr (LOADU) l2_prefetch(uin + (int64_t)min(j + 1 + M2_PF, n) * n);
+        l2_prefetch(bb + (int64_t)min(j + M2_PF, n) * n);
+      }
       gread_u(j + 1, Unx, MK);
       gload_b(j, Bn, MK);
       if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
