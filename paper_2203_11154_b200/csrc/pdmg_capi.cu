@@ -485,6 +485,7 @@ struct Engine : EngineBase {
   int march2_loopb_min_n = 128;  // (prolongating passes: shape (a), see march2_prolong_b)
   bool march2_ws = false;  // run the pair passes as warp-specialised producer/consumer warp pairs (k_march2ws)
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
+  double pred_final = 0.5;  // predicted-last-norm threshold (solve_device; 0 = off, PDMG_PRED_FINAL)
   // V(1,1): fuse cycle k's fine post-sweep with cycle k+1's pre-sweep (solve_xfuse).  Off by default:
   // measured on B200 the fused pass costs what the two single-sweep passes cost (C3 at V(1,1): 1621 vs
   // 807 + 821 us; C4 with 256 shifts: 6.38 vs 6.75 ms; C5 9.75 vs 9.08 ms per step) -- the passes are
@@ -682,6 +683,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH_HS")) march_hs = std::atoi(e);
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH1")) march1 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_PRED_FINAL")) pred_final = std::atof(e);
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
@@ -764,7 +766,7 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&d_active, sizeof(int) * S));
     CK(cudaMalloc(&d_iters, sizeof(int) * S));
     CK(cudaMalloc(&d_conv, sizeof(int) * S));
-    CK(cudaMalloc(&d_nactive, 2 * sizeof(int)));
+    CK(cudaMalloc(&d_nactive, 6 * sizeof(int)));  // [n_active slot 0, 1][pred slot 0, 1 (8 B each)]
     CK(cudaMalloc(&d_parity, sizeof(int) * (cfg.max_iter + 1)));
     CK(cudaMalloc(&d_ones, sizeof(int) * S));
     CK(cudaMalloc(&d_r0, sizeof(double) * S));
@@ -773,7 +775,7 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&d_norms, sizeof(double) * S));
     std::vector<int> ones(S, 1);
     CK(cudaMemcpyAsync(d_ones, ones.data(), sizeof(int) * S, cudaMemcpyHostToDevice, stream));
-    CK(cudaHostAlloc((void**)&h_map, map_nact() + 2 * sizeof(int), cudaHostAllocMapped));
+    CK(cudaHostAlloc((void**)&h_map, map_nact() + 6 * sizeof(int), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&d_map, h_map, 0));
     CK(cudaEventCreateWithFlags(&ev_nactive[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_nactive[1], cudaEventDisableTiming));
@@ -1008,17 +1010,27 @@ struct Engine : EngineBase {
   // (converged shifts are frozen on the device, so a speculative extra cycle leaves them untouched).
   void finalize(int k, int ntiles, bool wait = true, int cur = 0) {
     const int slot = k & 1;
+    unsigned long long* d_pred = reinterpret_cast<unsigned long long*>(d_nactive + 2) + slot;
     CK(cudaMemsetAsync(d_nactive + slot, 0, sizeof(int), stream));
-    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol, d_parity, cur};
+    CK(cudaMemsetAsync(d_pred, 0, sizeof(unsigned long long), stream));
+    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol, d_parity, cur,
+                  d_pred};
     const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
     timed("finalize", 0.0, [&] { k_finalize<<<blocks, threads, 0, stream>>>(d_partial, ntiles, k, st); });
-    to_host(d_nactive + slot, map_nact() + sizeof(int) * slot, sizeof(int));
+    to_host(d_nactive, map_nact(), 6 * sizeof(int));  // both slots' counts and predictions (24 B, one launch)
     CK(cudaEventRecord(ev_nactive[slot], stream));
     if (wait) n_active_host = read_nactive(k);
   }
   int read_nactive(int k) {
     CK(cudaEventSynchronize(ev_nactive[k & 1]));
     return ((volatile int*)(h_map + map_nact()))[k & 1];
+  }
+  // after read_nactive(k): max over the still-active shifts of the predicted r_{k+1} / (tol r0)
+  double read_pred(int k) {
+    const unsigned long long v = ((volatile unsigned long long*)(h_map + map_nact() + 2 * sizeof(int)))[k & 1];
+    double q;
+    std::memcpy(&q, &v, sizeof(q));
+    return q;
   }
 
   void unpack(const double2* src, V* dst, int l) {
@@ -1095,13 +1107,30 @@ struct Engine : EngineBase {
       // shifts, whose iterate stays in the other buffer) and the rest of cycle k runs for the active ones.
       // The host reads count(k-1) once cycle k is enqueued, so it enqueues cycle k+1 while the GPU is
       // still in cycle k.  After max_iter cycles one norm pass closes the history.
+      // Predicted last norm: when every active shift's predicted r_{k-1} (from finalize(k-2): the last
+      // ratio times the last contraction) is below pred_final * tol * r0, iterate k-1's norm is formed by
+      // a residual-only pass instead of cycle k's first (fused, two-sweep) pass, which would otherwise be
+      // spent only to find that every shift has converged.  Mispredicted, cycle k runs without norm_in.
       int n_act = S, k = 1;
+      double pred = 1e300;
       for (; k <= cfg.max_iter; ++k) {
+        if (pred_final > 0 && k >= 4 && pred <= pred_final) {
+          level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr,
+                     nullptr, d_active, n_act);
+          finalize(k - 1, last_partials, true, F.cur);
+          n_act = n_active_host;
+          if (n_act == 0) break;
+          pred = read_pred(k - 1);
+          nin_k = -1;
+          cycle_level(0, false, d_active, n_act, false);
+          continue;
+        }
         nin_k = k - 1;
         const bool normed = cycle_level(0, k == 1, d_active, n_act, false);
         (void)normed;
         n_act = read_nactive(k - 1);
         if (n_act == 0) break;
+        pred = read_pred(k - 1);
       }
       if (k > cfg.max_iter) {
         level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr,

@@ -664,6 +664,10 @@ struct SolveState {
   double tol;
   int* parity;       // [max_iter+1]: which u buffer holds the iterate after cycle k (written by k_finalize)
   int cur;
+  // max over the shifts still active after cycle k of the predicted next residual ratio
+  // (r_k / r0) (r_k / r_{k-1}) / tol, as double bits (atomicMax; k >= 2): the host's cue that the next
+  // iterate is likely the last one (solve_device)
+  unsigned long long* pred;
 };
 
 __global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k, SolveState st) {
@@ -699,6 +703,10 @@ __global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k
   }
   st.active[s] = act;
   if (act) atomicAdd(st.n_active, 1);
+  if (act && st.pred) {
+    const double q = k >= 2 ? (r / st.r0[s]) * (r / st.hist[(int64_t)s * H + k - 1]) / st.tol : 1e300;
+    atomicMax(st.pred, (unsigned long long)__double_as_longlong(q));
+  }
 }
 
 // Device -> mapped pinned host words, written by SMs over PCIe: small result copies that never queue

@@ -300,6 +300,24 @@ def test_norm_next_mixed_convergence(oracle):
         assert len(set(r.iterations for r in reps)) >= 2
 
 
+@pytest.mark.parametrize("pred", ["1e300", "0"])
+@pytest.mark.parametrize("cyc", [Cfg(nu1=1, nu2=1), Cfg(nu1=2, nu2=2), Cfg(nu1=2, nu2=2, cycle="W"),
+                                 Cfg(nu1=1, nu2=1, tol=1e-14, max_iter=6)])
+def test_predicted_last_norm(oracle, monkeypatch, cyc, pred):
+    """Predicted last norm (solve_device): when the host predicts that every active shift converges at
+    iterate k-1, that iterate's norm comes from a residual-only pass instead of cycle k's fused first pass.
+    PDMG_PRED_FINAL=1e300 forces the prediction from cycle 4 on, so most of them are wrong (the shifts
+    are still far from converged, or never converge with tol 1e-14): counts, histories and iterates must
+    still match the oracle; 0 disables it."""
+    monkeypatch.setenv("PDMG_PRED_FINAL", pred)
+    n, m = 128, 127
+    lams = [5000 + 0j, 0.0, 0.0, 8.959263353215057 - 15.395328029306036j]
+    b = oracle.random_complex(44, 4 * m * m).reshape(4, m, m)
+    b[1] = 0
+    u, reps, ref = _check_solve(oracle, n, lams, b, cyc, path="batched")
+    assert reps[1].iterations == 0 and np.all(u[1] == 0)
+
+
 @pytest.mark.parametrize("cyc", [Cfg(nu1=1, nu2=1), Cfg(nu1=1, nu2=1, cycle="W"), Cfg(nu1=1, nu2=1, tol=1e-14, max_iter=3)])
 def test_xfuse_matches_oracle(oracle, monkeypatch, cyc):
     """V(1,1) cross-cycle fusion (PDMG_XFUSE=1): cycle k's fine post-sweep and cycle k+1's pre-sweep run as
