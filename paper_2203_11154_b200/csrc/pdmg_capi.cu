@@ -475,6 +475,13 @@ struct Engine : EngineBase {
   // prolongating passes; levels not listed use march2_hs_default)
   std::vector<std::pair<int, int>> march2_hs_r, march2_hs_p;
   int march2_prolong_b = 0;  // prolongating passes may use loop shape (b) on levels with n >= march2_loopb_min_n
+  static int march2_ha(int post, bool two) {  // = k_march2's hA
+    return ((two ? 4 : 2) + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;
+  }
+  int march2_tasks(int n, int post, bool two, bool prolong) const {  // warp tasks per shift of a k_march2 pass
+    const int wout = 64 - 2 * march2_ha(post, two), hs = march2_hs_for(n, prolong);
+    return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
+  }
   int march2_hs_for(int n, bool prolong) const {
     if (march2_hs > 0) return march2_hs;
     for (auto& e : prolong ? march2_hs_p : march2_hs_r)
@@ -528,13 +535,13 @@ struct Engine : EngineBase {
     ma.coef = Lv.coef, ma.active = active, ma.n = Lv.n;
     ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
     ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
-    const int hA = ((two ? 4 : 2) + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;  // = k_march2 hA
-    const int wout = 64 - 2 * hA;
+    const int wout = 64 - 2 * march2_ha(post, two);
     ma.Hs = march2_hs_for(Lv.n, prolong);
     // loop shape (a) for prolongating passes unless march2_prolong_b (measured, DESIGN 3.2b)
     ma.loop_a = Lv.n < march2_loopb_min_n || (prolong && !march2_prolong_b);
     ma.ntx = (Lv.n + wout - 1) / wout;
     ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
+    if (ma.ntasks != march2_tasks(Lv.n, post, two, prolong)) throw std::logic_error("pdmg_b200: march2 task count");
     const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in, umid != nullptr);
     const bool ws = two && march2_ws && umid == nullptr;
     auto fn = !two ? marches2().e1[key2] : ws ? marches2().ws[key2] : marches2().e[key2];
@@ -564,6 +571,7 @@ struct Engine : EngineBase {
   // single Vanka sweeps on levels with n >= march2_min_n through k_march2<TWO = false> (PDMG_MARCH1=0: the
   // older k_level / k_march kernels)
   bool march1 = true;
+  bool resid_norm_kernel = true;  // residual-only norm passes through k_resid_norm (PDMG_RESID_NORM=0: k_level)
   bool use_march1(int l, const Variant& v) const {
     return march1 && march2_min_n > 0 && lv[l].n >= march2_min_n && v.sweep && v.store && !v.jacobi &&
            v.post != POST_RESID && marches2().e1[March2Table<T>::key(v.loadu, v.prolong, v.post)] != nullptr;
@@ -684,6 +692,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH_ALL")) march_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH1")) march1 = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_PRED_FINAL")) pred_final = std::atof(e);
+    if (const char* e = std::getenv("PDMG_RESID_NORM")) resid_norm_kernel = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_MARCH_LC")) march_lc = std::atoi(e) == 1 ? 1 : 2;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
@@ -761,7 +770,12 @@ struct Engine : EngineBase {
     int maxtiles = 1;
     for (size_t l = 0; l < lv.size(); ++l) {
       maxtiles = std::max(maxtiles, lv[l].ntiles);
-      for (int post : {POST_NONE, POST_NORM, POST_RESTRICT}) maxtiles = std::max(maxtiles, march_tasks((int)l, post));
+      for (int post : {POST_NONE, POST_NORM, POST_RESTRICT}) {
+        maxtiles = std::max(maxtiles, march_tasks((int)l, post));
+        for (int two = 0; two < 2; ++two)
+          for (int pr = 0; pr < 2; ++pr) maxtiles = std::max(maxtiles, march2_tasks(lv[l].n, post, two != 0, pr != 0));
+      }
+      maxtiles = std::max(maxtiles, (lv[l].n - 1 + RN_ROWS - 1) / RN_ROWS);  // k_resid_norm
     }
     CK(cudaMalloc(&d_active, sizeof(int) * S));
     CK(cudaMalloc(&d_iters, sizeof(int) * S));
@@ -858,6 +872,15 @@ struct Engine : EngineBase {
     // a smoother update is 3 S (u in, b in, u out) whatever the pass actually moves
     const double ubpp = v.sweep ? 3 * S_ + (v.prolong ? S_ / 4 : 0) + (v.post == POST_RESTRICT ? S_ / 4 : 0) : -1.0;
     const double ub = ubpp < 0 ? -1.0 : pts * ubpp, nupd = v.sweep ? pts : 0.0;
+    if (resid_norm_kernel && v.loadu && !v.prolong && !v.sweep && !v.store && v.post == POST_NORM && !norm_in) {
+      const int ntiles = (Lv.m + RN_ROWS - 1) / RN_ROWS;
+      dim3 grid(ntiles, S);
+      timed(cls, pts * bpp, [&] {
+        k_resid_norm<T><<<grid, RN_THREADS, 0, stream>>>(uin, b, Lv.coef, active, Lv.n, Lv.ss, d_partial);
+      }, ub, nupd);
+      last_partials = ntiles;
+      return;
+    }
     if (use_march1(l, v)) {
       level_pass2(l, v.loadu, v.prolong, v.post, uin, uout, b, ec, bc, active, n_act, norm_in, nullptr, false);
       return;

@@ -716,6 +716,45 @@ __global__ void k_copy_words(const uint32_t* __restrict__ src, volatile uint32_t
     dst[i] = src[i];
 }
 
+// Residual-only norm pass ||b - (A + lambda I) u||^2 (multigrid.cpp:91, 96-105) for the convergence
+// test outside a smoothing pass (predicted last norm, the max_iter closing norm).  HBM-bound: u and b are
+// each read once (the neighbour rows and columns are L1 hits); one CTA per (RN_ROWS-row block, shift),
+// each thread two adjacent columns per row, so a row is one coalesced 1 KB-per-warp sweep; the partial
+// layout is k_finalize's [shift][tile].  The ghost ring reads as zero (homogeneous Dirichlet).
+constexpr int RN_ROWS = 16, RN_THREADS = 256;
+template <class T>
+__global__ void __launch_bounds__(RN_THREADS) k_resid_norm(const typename vec2<T>::type* __restrict__ u,
+                                                            const typename vec2<T>::type* __restrict__ b,
+                                                            const LevelCoef* __restrict__ coef,
+                                                            const int* __restrict__ active, int n, int64_t ss,
+                                                            double* __restrict__ partial) {
+  __shared__ double red[RN_THREADS / 32];
+  const int shift = blockIdx.y, tile = blockIdx.x, ntiles = gridDim.x;
+  if (active != nullptr && active[shift] == 0) return;
+  const int m = n - 1;
+  const LevelCoef cf = coef[shift];
+  const auto* us = u + (int64_t)shift * ss;
+  const auto* bs = b + (int64_t)shift * ss;
+  const int j0 = 1 + tile * RN_ROWS, j1 = min(j0 + RN_ROWS, m + 1);
+  double acc = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    for (int i = 1 + threadIdx.x; i <= m; i += RN_THREADS) {
+      const int64_t p = (int64_t)j * n + i;
+      const double2 r = res5(ld2(bs[p]), cf.inv_h2, cf.dd, ld2(us[p]), ld2(us[p - 1]), ld2(us[p + 1]), ld2(us[p - n]),
+                             ld2(us[p + n]));
+      acc += r.x * r.x + r.y * r.y;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < RN_THREADS / 32; ++w) t += red[w];
+    partial[(int64_t)shift * ntiles + tile] = t;
+  }
+}
+
 // Per-shift norms (op-level pdmg_norm): sum partials -> sqrt.
 __global__ void k_sum_partials(const double* __restrict__ partial, int ntiles, int S, double* out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
