@@ -1572,12 +1572,19 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
 #ifndef PDMG_M2_PF
 #define PDMG_M2_PF 2
 #endif
-  constexpr int M2_PF = (TWO && PROLONG) ? 0 : PDMG_M2_PF;
+#ifndef PDMG_M2_PF_PROLONG
+#define PDMG_M2_PF_PROLONG 0
+#endif
+  constexpr int M2_PF = (TWO && PROLONG && !PDMG_M2_PF_PROLONG) ? 0 : PDMG_M2_PF;
   // NO_EX: lane 31 skips the coarse column beyond its strip, so the prolongation at the strip's last
   // column (cA + 63, odd) is wrong.  With the restriction's halo (hA = 6) that error reaches u1/u2 at
   // columns >= cA + 59 and r2 at >= cA + 58 only, outside the stored columns (<= cA + 57) and the stored
   // coarse points (fine column <= cA + 56): the results are unchanged and 12 registers are saved.
   constexpr bool NO_EX = PROLONG && POST == POST_RESTRICT;
+#ifndef PDMG_M2_PRO_DIRECT
+#define PDMG_M2_PRO_DIRECT 1
+#endif
+  constexpr bool PRO_DIRECT = PDMG_M2_PRO_DIRECT && !MID;
   static_assert(!NO_EX || hA >= 6, "NO_EX needs the restriction halo");
   const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
@@ -1657,8 +1664,26 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
         out[k] = ld2(bb[(int64_t)row * n + k]);
     }
   };
-  auto prolong_row = [&](int row, D2* pout, auto MK) __attribute__((always_inline)) {
+  // prolong_bilinear (grid.cpp:123-153) onto fine row `row` from the coarse values a0 = e(J, Ie),
+  // a1 = e(J, Ie+1), b0 = e(J+1, Ie), b1 = e(J+1, Ie+1): even/odd fine column and row (both warp-uniform)
+  auto prolong_of = [&](int row, const D2& a0, const D2& a1, const D2& b0, const D2& b1, D2* pout, auto MK)
+                        __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value;
+    const bool rin = !MASK || row_ok(row);
+    D2 p[LC];
+    if (row & 1) {
+      const D2 q4 = cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1));
+      p[0] = codd ? q4 : cscale(0.5, cadd(a0, b0));
+      p[1] = codd ? cscale(0.5, cadd(a1, b1)) : q4;
+    } else {
+      const D2 q2 = cscale(0.5, cadd(a0, a1));
+      p[0] = codd ? q2 : a0;
+      p[1] = codd ? a1 : q2;
+    }
+#pragma unroll
+    for (int k = 0; k < LC; ++k) pout[k] = MASK ? csel(rin && cin[k], p[k]) : p[k];
+  };
+  auto prolong_row = [&](int row, D2* pout, auto MK) __attribute__((always_inline)) {
     const int J = row >> 1;
     if (J == wJ + 1) {
       Eo0 = Eo1, Eo1 = Eo2, Ex0 = Ex1, Ex1 = Ex2;
@@ -1673,20 +1698,22 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     const D2 a0 = Eo0, b0 = Eo1;
     D2 a1 = shfl_dn2(Eo0), b1 = shfl_dn2(Eo1);
     if (!NO_EX && lane == 31) a1 = Ex0, b1 = Ex1;
-    const bool rin = !MASK || row_ok(row);
-    // prolong_bilinear (grid.cpp:123-153): even/odd fine column and row (both warp-uniform)
-    D2 p[LC];
-    if (row & 1) {
-      const D2 q4 = cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1));
-      p[0] = codd ? q4 : cscale(0.5, cadd(a0, b0));
-      p[1] = codd ? cscale(0.5, cadd(a1, b1)) : q4;
-    } else {
-      const D2 q2 = cscale(0.5, cadd(a0, a1));
-      p[0] = codd ? q2 : a0;
-      p[1] = codd ? a1 : q2;
-    }
-#pragma unroll
-    for (int k = 0; k < LC; ++k) pout[k] = MASK ? csel(rin && cin[k], p[k]) : p[k];
+    prolong_of(row, a0, a1, b0, b1, pout, MK);
+  };
+  // PRO_DIRECT: the four coarse values of fine row `row` -- e(J, Ie), e(J, Ie+1), e(J+1, Ie), e(J+1, Ie+1),
+  // J = row >> 1 -- are loaded unconditionally (indices clamped into the array; out-of-domain points are
+  // masked when the prolongation is formed) one step before the row is consumed: no window rotation, no
+  // branch around the loads, so no register copy waits on a load that was just issued
+  D2 Cq[4];
+  auto load_coarse = [&](int row, auto MK) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value;
+    int J = row >> 1, I = Ie;
+    if constexpr (MASK) J = min(max(J, 0), nc - 1), I = min(max(I, 0), nc - 1);
+    const V* p0 = ecs + (int64_t)J * nc + I;
+    Cq[0] = ld2(p0[0]), Cq[1] = ld2(p0[1]), Cq[2] = ld2(p0[nc]), Cq[3] = ld2(p0[nc + 1]);
+  };
+  auto prolong_direct = [&](int row, D2* pout, auto MK) __attribute__((always_inline)) {
+    prolong_of(row, Cq[0], Cq[1], Cq[2], Cq[3], pout, MK);
   };
   auto west = [&](const D2* x, int k, const D2& wl) __attribute__((always_inline)) { return k == 0 ? wl : x[k - 1]; };
   auto east = [&](const D2* x, int k, const D2& er) __attribute__((always_inline)) { return k == LC - 1 ? er : x[k + 1]; };
@@ -1734,7 +1761,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     if constexpr (NEED_B3) gload_b(rlo - 3, B3n, IC<1>{});
     if constexpr (NEED_B5) gload_b(rlo - 5, B5n, IC<1>{});
   }
-  if constexpr (PROLONG) prolong_row(rlo, Pn, IC<1>{});
+  if constexpr (PROLONG) {
+    if constexpr (PRO_DIRECT) load_coarse(rlo, IC<1>{});
+    else prolong_row(rlo, Pn, IC<1>{});
+  }
 
   // one step at row j; window slot of (oldest, middle, newest) row = ((PH + 0, 1, 2) % 3)
   auto step = [&](int j, auto PH, auto MK) __attribute__((always_inline)) {
@@ -1744,12 +1774,19 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     D2 B3[LC], B5[LC], Bc[LC], Un[LC];
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
-      Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
+      if constexpr (PRO_DIRECT) Un[k] = Unx[k];
+      else Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
       Bc[k] = Bn[k];
       if constexpr (!B_INSTEP) {
         if constexpr (NEED_B3) B3[k] = B3n[k];
         if constexpr (NEED_B5) B5[k] = B5n[k];
       }
+    }
+    if constexpr (PROLONG && PRO_DIRECT) {  // u row j += P e_c (coarse values loaded last step)
+      D2 Pc[LC];
+      prolong_direct(j, Pc, MK);
+#pragma unroll
+      for (int k = 0; k < LC; ++k) Un[k] = cadd(Un[k], Pc[k]);
     }
     if constexpr (B_INSTEP) {  // (L1 hits: b rows j-3 and j-5 were loaded 2 and 4 steps ago)
       gload_b(j - 3, B3, MK);
@@ -1762,7 +1799,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
       }
       gread_u(j + 1, Unx, MK);
       gload_b(j, Bn, MK);
-      if constexpr (PROLONG) prolong_row(j + 1, Pn, MK);
+      if constexpr (PROLONG && !PRO_DIRECT) prolong_row(j + 1, Pn, MK);
+      if constexpr (PROLONG && PRO_DIRECT) load_coarse(j + 1, MK);
       if constexpr (!B_INSTEP) {
         if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
         if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
