@@ -1567,15 +1567,12 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
 #define PDMG_M2_BINSTEP 0
 #endif
   constexpr bool B_INSTEP = MID || (PDMG_M2_BINSTEP && TWO);
-  // L2 prefetch distance in rows (0 = none).  Measured at C3 (DESIGN 3.2b): 2 rows ahead speeds up the
-  // non-prolongating pairs and the one-sweep passes and slows the prolongating pairs, which keep none.
+  // L2 prefetch distance in rows (0 = none).  Measured at C3 (DESIGN 3.2b): 2 rows ahead speeds up every
+  // marching pass (the prolongating pairs only since their coarse values are loaded directly, PRO_DIRECT)
 #ifndef PDMG_M2_PF
 #define PDMG_M2_PF 2
 #endif
-#ifndef PDMG_M2_PF_PROLONG
-#define PDMG_M2_PF_PROLONG 0
-#endif
-  constexpr int M2_PF = (TWO && PROLONG && !PDMG_M2_PF_PROLONG) ? 0 : PDMG_M2_PF;
+  constexpr int M2_PF = PDMG_M2_PF;
   // NO_EX: lane 31 skips the coarse column beyond its strip, so the prolongation at the strip's last
   // column (cA + 63, odd) is wrong.  With the restriction's halo (hA = 6) that error reaches u1/u2 at
   // columns >= cA + 59 and r2 at >= cA + 58 only, outside the stored columns (<= cA + 57) and the stored
