@@ -5,8 +5,10 @@ A "step" is one full batched solve (every shift to relative residual 1e-10) of t
 Default workload = BASELINE config 3: h=1/512 (511x511 interior), n=256 shifts
 lambda_j = (1 - alpha^(1/n) e^(2 pi i j/n))/dt with alpha=1e-3, dt=1/256, RHS uniform[-1,1]^2 from
 std::mt19937(2) drawn shift-major, V(2,2) Vanka cycles (omega = 24/25), coarsest 3x3, complex128.
-Shifts are sharded contiguously over ranks (paradiag.cpp:217-236 chunking); there is no data-path
-collective, so `value` = all ranks' updates / max-over-ranks time.
+N>1 (torchrun): by default (`--scaling weak`) every rank solves its own full batch of the config's
+shifts, rank r's RHS from mt19937(seed + 100 r), so per-GPU work is fixed; `--scaling strong` instead
+shards the config's batch contiguously over the ranks (paradiag.cpp:217-236 chunking). Either way there
+is no data-path collective, so `value` = all ranks' updates / max-over-ranks time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl b200|reference]
 
@@ -59,6 +61,9 @@ def parse():
     ap.add_argument("--nu", default="", help="override the cycle's nu1,nu2 (experiments; not a BASELINE config)")
     ap.add_argument("--precision", default="c128", choices=["c128", "c64"],
                     help="c64: fp32 storage / fp64 arithmetic, tol 1e-5 (BASELINE config 4)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = every rank solves its own full batch of the config (rank r's RHS from "
+                         "mt19937(seed + 100 r)); strong = the config's batch is split over the ranks")
     return ap.parse_args()
 
 
@@ -307,15 +312,17 @@ def main():
         nu1, nu2 = (int(x) for x in args.nu.split(","))
         desc += f" [nu1,nu2 = {nu1},{nu2}]"
     m = n - 1
-    b0, b1 = shard(S, rank, world)
+    weak = world > 1 and args.scaling == "weak"
+    b0, b1 = (0, S) if weak else shard(S, rank, world)
     Sr = b1 - b0
+    rhs_seed = seed + 100 * rank if weak else seed
     j0 = 3 if args.config == "c1" else 0  # BASELINE config 1 is slot j = 3 of the n_t = 32 family
     lams_all = P.circulant_shifts(alpha, nt, dt, j0, S)
     lams = lams_all[b0:b1]
     tol = 1e-5 if args.precision == "c64" else 1e-10
     cfg = P.MultigridConfig(P.CycleKind.V, nu1, nu2, 4, tol, 200, P.SmootherConfig.vanka())
     # inputs: one mt19937(seed) stream, shift-major; each rank keeps its shard
-    b_all = P.random_rhs(n, seed, count=b1)
+    b_all = P.random_rhs(n, rhs_seed, count=b1)
     b_host = np.ascontiguousarray(b_all.reshape(b1, m, m)[b0:b1])
     del b_all
     H = P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg, device=local, precision=args.precision)
@@ -372,7 +379,8 @@ def main():
     ms_max = max_over_ranks(ms)
     upd_all = sum_over_ranks(upd)
     value = upd_all / (ms_max / 1e3)
-    shifts_per_s = args.steps * S / (ms_max / 1e3)
+    S_job = Sr * world if weak else S
+    shifts_per_s = args.steps * S_job / (ms_max / 1e3)
     iters = [r.iterations for r in reps]
     conv = all(r.converged for r in reps)
 
@@ -468,11 +476,14 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": desc + (f" [{S} shifts]" if args.shifts else ""), "shifts": S,
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic",
+            "config": {"workload": desc + (f" [{S} shifts]" if args.shifts else "")
+                       + (f" per rank (rank r: RHS seed {seed} + 100 r)" if weak else ""), "shifts": S_job,
                        "precision": args.precision + (" (fp32 storage, fp64 arithmetic), tol 1e-5"
                                                       if args.precision == "c64" else ", tol 1e-10"),
-                       "shifts_per_rank": Sr, "parallelism": f"shift-sharded x{world}",
+                       "shifts_per_rank": Sr, "parallelism": (f"independent {Sr}-shift batch per rank x{world}" if weak
+                                       else f"shift-sharded x{world}"),
                        "l2": "inputs larger than L2 (each fine array %.2f GB)" % (S * (n + 1) * n * 16 / 1e9)
                        if S * (n + 1) * n * 16 > 126e6 else "working set fits in L2 (latency-bound config)"},
             "shifts_per_s": shifts_per_s, "cycles_per_shift": sorted(set(iters)), "all_converged": conv,
