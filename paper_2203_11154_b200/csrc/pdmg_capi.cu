@@ -602,10 +602,12 @@ struct Engine : EngineBase {
   ~Engine() {
     if (device >= 0) cudaSetDevice(device);
     for (auto& L : lv) {
-      cudaFree(L.u[0]);
-      cudaFree(L.u[1]);
-      cudaFree(L.u[2]);
-      cudaFree(L.b);
+      if (!borrow) {
+        cudaFree(L.u[0]);
+        cudaFree(L.u[1]);
+        cudaFree(L.u[2]);
+        cudaFree(L.b);
+      }
       cudaFree(L.coef);
     }
     cudaFree(d_ainv);
@@ -708,13 +710,23 @@ struct Engine : EngineBase {
       Lv.m = Lv.n - 1;
       Lv.ss = (int64_t)(Lv.n + 1) * Lv.n;
       Lv.elems = (size_t)Lv.ss * S + Lv.n + 2;  // + guard so the last shift's ghost reads stay in bounds
-      for (V** p : {&Lv.u[0], &Lv.u[1], &Lv.b}) {
-        CK(cudaMalloc(p, Lv.elems * sizeof(V)));
-        CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
-      }
-      if (l == 0 && use_xfuse()) {
-        CK(cudaMalloc(&Lv.u[2], Lv.elems * sizeof(V)));
-        CK(cudaMemsetAsync(Lv.u[2], 0, Lv.elems * sizeof(V), stream));
+      if (borrow) {
+        // the parent's arrays are zeroed (ghost rings included); past the last shift of a middle range the
+        // guard reads land in the next range's first shift, exactly as they do inside the parent
+        const Level& P = borrow->lv[l];
+        const int64_t off = (int64_t)borrow_s0 * Lv.ss;
+        Lv.u[0] = P.u[0] + off, Lv.u[1] = P.u[1] + off, Lv.b = P.b + off;
+        Lv.u[2] = P.u[2] ? P.u[2] + off : nullptr;
+        if (borrow_s0 + S < borrow->S) Lv.elems = (size_t)Lv.ss * S;
+      } else {
+        for (V** p : {&Lv.u[0], &Lv.u[1], &Lv.b}) {
+          CK(cudaMalloc(p, Lv.elems * sizeof(V)));
+          CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
+        }
+        if (l == 0 && use_xfuse()) {
+          CK(cudaMalloc(&Lv.u[2], Lv.elems * sizeof(V)));
+          CK(cudaMemsetAsync(Lv.u[2], 0, Lv.elems * sizeof(V), stream));
+        }
       }
       Lv.H = std::min(Lv.n >= level_h_min_n ? 128 : 64, Lv.n + (Lv.n & 1));
       Lv.ntx = (Lv.n + TILE_W - 1) / TILE_W;
@@ -1344,6 +1356,10 @@ struct Engine : EngineBase {
   int io_chunks = 0;  // 0 = automatic
   int io_mode = 1;    // 1: chunks solve concurrently on sub-engines (own streams, priorities); 0: one stream
   int stream_priority = 0;
+  // sub-engine of a concurrent host solve: its level arrays are the shift range [borrow_s0, borrow_s0 + S)
+  // of the parent engine's (a contiguous block of the shift-major storage), not allocations of its own
+  Engine* borrow = nullptr;
+  int borrow_s0 = 0;
   // Sub-engines of the concurrent host-buffer pipeline: shifts [sub_lo[c], sub_lo[c+1]) on their own stream,
   // chunk c at stream priority greatest + c, so chunks finish in order while later chunks fill the SMs the
   // earlier ones leave idle (coarse levels, convergence bookkeeping, tails of the large passes).
@@ -1357,12 +1373,8 @@ struct Engine : EngineBase {
     }
     subs.clear();
     sub_lo.clear();
-    // memory: each sub-engine holds the level storage of its shifts (the main engine keeps its own)
-    size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot));
-    size_t need = 0;
-    for (const Level& L : lv) need += L.elems * sizeof(V) * 3;
-    if (need + ((size_t)2 << 30) > fr) return false;
+    // memory: each sub-engine works in its shift range of this engine's level arrays (borrow); it only
+    // allocates its coefficient tables, coarse factors and bookkeeping
     int least = 0, greatest = 0;
     CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     for (size_t c = 0; c + 1 < lo.size(); ++c) {
@@ -1375,6 +1387,8 @@ struct Engine : EngineBase {
       e->device = -1;
       e->setup_host(d);
       e->stream_priority = std::min(greatest + (int)c, least);
+      e->borrow = this;
+      e->borrow_s0 = lo[c];
       e->setup_device(device);
       e->io_chunks = 1;
       e->solve_path = solve_path;
