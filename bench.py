@@ -5,10 +5,10 @@ A "step" is one full batched solve (every shift to relative residual 1e-10) of t
 Default workload = BASELINE config 3: h=1/512 (511x511 interior), n=256 shifts
 lambda_j = (1 - alpha^(1/n) e^(2 pi i j/n))/dt with alpha=1e-3, dt=1/256, RHS uniform[-1,1]^2 from
 std::mt19937(2) drawn shift-major, V(2,2) Vanka cycles (omega = 24/25), coarsest 3x3, complex128.
-N>1 (torchrun): by default (`--scaling weak`) every rank solves its own full batch of the config's
-shifts, rank r's RHS from mt19937(seed + 100 r), so per-GPU work is fixed; `--scaling strong` instead
-shards the config's batch contiguously over the ranks (paradiag.cpp:217-236 chunking). Either way there
-is no data-path collective, so `value` = all ranks' updates / max-over-ranks time.
+N>1 (torchrun): by default (`--scaling strong`) the config's batch is sharded contiguously over the ranks
+(paradiag.cpp:217-236 chunking), as BASELINE config 3 words it; `--scaling weak` instead has every rank solve
+its own full batch of the config's shifts (rank r's RHS from mt19937(seed + 100 r)).  Either way there is no
+data-path collective, so `value` = all ranks' updates / max-over-ranks time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl b200|reference]
 
@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--nu", default="", help="override the cycle's nu1,nu2 (experiments; not a BASELINE config)")
     ap.add_argument("--precision", default="c128", choices=["c128", "c64"],
                     help="c64: fp32 storage / fp64 arithmetic, tol 1e-5 (BASELINE config 4)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1: weak = every rank solves its own full batch of the config (rank r's RHS from "
                          "mt19937(seed + 100 r)); strong = the config's batch is split over the ranks")
     return ap.parse_args()
@@ -134,12 +134,41 @@ class ClockSampler:
                 "samples": len(self.samples), "source": self.src}
 
 
-def cpu_reference_run(n, lams, nu1, nu2, b, threads):
+def so_sha16() -> str:
+    import hashlib
+
+    from paper_2203_11154_b200 import _native as N
+
+    with open(N.LIB_PATH, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def traffic_for(config: str, kernel: str) -> dict:
+    """ncu DRAM traffic per launch of `kernel` (dram__bytes_read.sum + dram__bytes_write.sum, one `ncu --set full`
+    capture, profiles/traffic.json).  Each capture is stamped with the sha256 of the libpdmg_b200.so it profiled;
+    a capture of another build is not reported as this build's traffic."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+    except Exception:
+        return {"traffic": None, "traffic_note": "no ncu capture in profiles/traffic.json"}
+    ent = tj.get(config, {}).get(kernel)
+    if not ent:
+        return {"traffic": None, "traffic_note": f"no ncu capture of {kernel} for {config}"}
+    cur = so_sha16()
+    if ent.get("so_sha16") != cur:
+        return {"traffic": None, "traffic_note": f"ncu capture is of build {ent.get('so_sha16')}, this build is {cur}",
+                "traffic_stale": ent.get("bytes")}
+    return {"traffic": ent["bytes"], "traffic_source": ent.get("source", "profiles/traffic.json"),
+            "traffic_build": cur}
+
+
+def cpu_reference_run(n, lams, nu1, nu2, b, threads, tol=1e-10):
     """Reference CPU path: the reference's own grid.cpp/smoother.cpp (oracle/_ref) when built, else the C port.
     Shifts split over `threads` std::threads in contiguous chunks (paradiag.cpp:217-236)."""
     from oracle_lib import Cfg, Oracle, RefLib
 
-    cfg = Cfg(nu1=nu1, nu2=nu2)
+    cfg = Cfg(nu1=nu1, nu2=nu2, tol=tol)
     try:
         lib, kind = RefLib(), "reference"
     except (FileNotFoundError, OSError):
@@ -150,24 +179,57 @@ def cpu_reference_run(n, lams, nu1, nu2, b, threads):
     return out, dt, kind
 
 
-def cpu_sample(n, lams_all, nu1, nu2, seed, threads, budget_s):
-    """Time a bounded, contiguous sample of the workload's shifts on the host cores."""
-    from oracle_lib import Oracle
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    o = Oracle()
+
+def cpu_sample(n, lams_all, nu1, nu2, b_all, threads, budget_s, tol=1e-10):
+    """Time a bounded, contiguous sample of the workload's shifts (the workload's own right-hand sides) on the
+    host cores with `threads` std::threads, plus one shift on one core (BASELINE.md 4: T = nproc and T = 1).
+    Returns the baseline record and the oracle's per-shift results for the parity check."""
     m = n - 1
     upc = updates_per_cycle(n, nu1, nu2)
-    b1 = o.random_complex(seed, m * m).reshape(1, m, m)
-    _, t1, _ = cpu_reference_run(n, lams_all[:1], nu1, nu2, b1, 1)  # calibrate one shift on one core
+    out1, t1, kind = cpu_reference_run(n, lams_all[:1], nu1, nu2, b_all[:1], 1, tol)  # one shift on one core
     count = int(max(threads, min(len(lams_all), threads * max(1, round(budget_s / max(t1, 1e-3))))))
     count = min(count, len(lams_all))
-    b = o.random_complex(seed, count * m * m).reshape(count, m, m)
-    out, dt, kind = cpu_reference_run(n, lams_all[:count], nu1, nu2, b, threads)
+    out, dt, kind = cpu_reference_run(n, lams_all[:count], nu1, nu2, b_all[:count], threads, tol)
     upd = float(np.sum(out["iterations"])) * upc
-    return dict(value=upd / dt, unit=UNIT, cores=threads, kind=kind,
-                sample=f"shifts 0..{count - 1} of the workload ({count} of {len(lams_all)}), "
-                       f"{threads} std::threads, {dt:.2f} s wall",
-                shifts_per_s=count / dt, seconds=dt)
+    rec = dict(value=upd / dt, unit=UNIT, cores=threads, kind=kind, cpu_model=cpu_model(),
+               sample=f"shifts 0..{count - 1} of the workload ({count} of {len(lams_all)}, the workload's own "
+                      f"right-hand sides), {threads} std::threads, {dt:.2f} s wall",
+               shifts_per_s=count / dt, seconds=dt,
+               single_core={"value": float(out1["iterations"][0]) * upc / t1, "unit": UNIT, "cores": 1,
+                            "sample": f"shift 0 on one core, {t1:.3f} s", "shifts_per_s": 1.0 / t1})
+    return rec, out, count
+
+
+def parity_block(reps, u_dev, cpu_out, count, tol):
+    """GPU vs the CPU reference path on the same inputs (north_star: identical per-shift V-cycle counts, solution and
+    residual history within 1e-10 relative): shifts 0..count-1 of the workload."""
+    it_ref = np.asarray(cpu_out["iterations"][:count])
+    it_gpu = np.array([r.iterations for r in reps[:count]])
+    u_err = h_err = 0.0
+    margin = np.inf
+    for s in range(count):
+        it = int(it_ref[s])
+        h_ref = cpu_out["hist"][s, : it + 1]
+        if h_ref[0] > 0:
+            if it_gpu[s] == it:
+                h_err = max(h_err, float(np.max(np.abs(reps[s].residual_history - h_ref)) / h_ref[0]))
+            margin = min(margin, abs(h_ref[-1] / h_ref[0] - tol) / tol)
+        ref_u = cpu_out["u"][s]
+        u_err = max(u_err, float(np.linalg.norm((u_dev[s] - ref_u).ravel()) / max(np.linalg.norm(ref_u.ravel()), 1e-300)))
+    return {"shifts_compared": int(count), "iters_equal": bool(np.array_equal(it_ref, it_gpu)),
+            "iters_equal_count": int(np.sum(it_ref == it_gpu)), "max_rel_err_u": u_err,
+            "max_rel_err_history": h_err, "min_stop_margin": float(margin),
+            "reference": "oracle/_ref (the reference's own grid.cpp/smoother.cpp + restated driver) on the box's host"}
 
 
 def run_reference(args):
@@ -182,14 +244,17 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     m = n - 1
     upc = updates_per_cycle(n, nu1, nu2)
-    # per step: a bounded sample of `threads` shifts (one per core), cycling through the shift list
+    # per step: a bounded sample of `threads` shifts (one per core) of the workload itself -- its own shifts and
+    # right-hand sides (the seed's shift-major stream) -- cycling through the shift list
     per = min(S, threads)
+    if args.config == "c1":
+        lams = o.circulant_shifts(alpha, nt, dt, 3, 1)
+    b_all = o.random_complex(seed, S * m * m).reshape(S, m, m)
     vals, times, kind = [], [], "port"
     for step in range(args.warmup + args.steps):
         j0 = (step * per) % S
         idx = [(j0 + q) % S for q in range(per)]
-        b = o.random_complex(seed + 1000 * step, per * m * m).reshape(per, m, m)
-        out, t, kind = cpu_reference_run(n, lams[idx], nu1, nu2, b, threads)
+        out, t, kind = cpu_reference_run(n, lams[idx], nu1, nu2, np.ascontiguousarray(b_all[idx]), threads)
         if step >= args.warmup:
             vals.append(float(np.sum(out["iterations"])) * upc / t)
             times.append(t)
@@ -198,9 +263,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": desc, "sample_per_step": f"{per} shifts on {threads} host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{per} shifts per step (one per core) of {args.config}"},
+        "config": {"workload": desc, "sample_per_step": f"{per} shifts on {threads} host threads",
+                   "same_inputs": "the workload's own shifts and seed-stream right-hand sides"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"{per} shifts per step (one per core) of {args.config}: the workload's own "
+                                   "shifts and right-hand sides, cycling through the batch"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -478,19 +545,16 @@ def main():
                              "peak; moved_GBps / moved_frac are the bytes the pass physically moves"}
     if moved:
         roofline.update(moved)
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(args.config, {}).get(top_name)
-            if tr:
-                roofline["traffic"] = tr
-    except Exception:
-        pass
-
-    cpu = None
+    roofline.update(traffic_for(args.config, top_name))
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             lam_np = np.asarray(lams_all, np.complex128)
-            cpu = cpu_sample(n, lam_np, nu1, nu2, seed, os.cpu_count() or 1, budget_s=10.0)
+            cpu, cpu_out, count = cpu_sample(n, lam_np, nu1, nu2, b_host, os.cpu_count() or 1, budget_s=10.0, tol=tol)
+            u_s = d_u.view(S, m, m, 2)[:count].cpu().numpy()
+            parity = parity_block(reps, u_s[..., 0] + 1j * u_s[..., 1], cpu_out, count, tol)
+            if args.precision == "c64":
+                parity["note"] = "complex64 (fp32 storage) vs the fp64 reference at the same tol: north_star bound 1e-4 on u"
         except Exception as e:  # the baseline is reported, never required for the GPU number
             cpu = {"error": str(e)}
 
@@ -515,6 +579,7 @@ def main():
             "roofline": roofline,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "parity": parity,
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                             "GBps": round(v.get("unit_bytes", v["bytes"]) / v["ms"] / 1e6, 1) if v["ms"] > 0 else None,
                             "moved_GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] > 0 else None}

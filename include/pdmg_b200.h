@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PDMG_B200_ABI_VERSION 1
+#define PDMG_B200_ABI_VERSION 2
 
 typedef struct {
   double re, im;
@@ -67,7 +67,13 @@ typedef struct {
   const pdmg_c128* lambdas; /* host [n_shifts]: Shift.lambda (grid.hpp:44) */
   pdmg_mg_config cfg;
   int32_t precision;        /* PDMG_PREC_C128 (the reference's type)       */
-  int32_t device;           /* CUDA device ordinal                         */
+  int32_t device;           /* CUDA device ordinal (when n_devices == 0)   */
+  /* Optional device list: the reference's `threads` argument of paradiag_solve (paradiag.cpp:207-236) becomes a
+   * list of devices.  Shard p = shifts [p*chunk, min(S, (p+1)*chunk)), chunk = ceil(S / n_devices), runs on
+   * devices[p] in its own engine; every call runs the shards concurrently (one host thread each).  A device may
+   * repeat.  NULL / 0: a single engine on `device`. */
+  const int32_t* devices;
+  int32_t n_devices;
 } pdmg_batch_desc;
 
 typedef struct pdmg_ctx pdmg_ctx;
@@ -103,6 +109,13 @@ int pdmg_solve(pdmg_ctx* ctx, const pdmg_c128* b, pdmg_c128* u, pdmg_solve_repor
 /* Same with b, u already resident in device memory of ctx's device (compact layout as above). */
 int pdmg_solve_device(pdmg_ctx* ctx, const void* d_b, void* d_u, pdmg_solve_report* report);
 
+/* Device-resident solve of a context sharded over devices: d_b[p], d_u[p] hold shard p's shifts (compact layout) in
+ * the memory of shard p's device (pdmg_part_range).  For a single-device context this is pdmg_solve_device. */
+int pdmg_solve_device_shards(pdmg_ctx* ctx, const void* const* d_b, void* const* d_u, pdmg_solve_report* report);
+int pdmg_num_parts(const pdmg_ctx* ctx);
+/* Shard `part`: its first shift, shift count and device. */
+int pdmg_part_range(const pdmg_ctx* ctx, int part, int32_t* shift0, int32_t* count, int32_t* device);
+
 /* MultigridHierarchy::cycle: one cycle applied in place to every shift's u (multigrid.cpp:79-83). */
 int pdmg_cycle(pdmg_ctx* ctx, pdmg_c128* u, const pdmg_c128* b);
 
@@ -130,8 +143,28 @@ int pdmg_coarse_solve(pdmg_ctx* ctx, const pdmg_c128* b, pdmg_c128* u);      /* 
 typedef struct pdmg_paradiag pdmg_paradiag;
 int pdmg_paradiag_create(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t device,
                          pdmg_paradiag** out);
+/* The same with the time slices (and their shift slots) sharded over a device list -- the reference's `threads`
+ * argument of paradiag_solve (paradiag.cpp:207-236): shard p holds slices [p*chunk, min(nt, (p+1)*chunk)),
+ * chunk = ceil(nt / n_devices), on devices[p].  Both time transforms gather their time columns from every shard
+ * and scatter the results to the owners through NVLink peer pointers inside the transform kernel (no separate
+ * all-to-all); peer access between distinct devices is enabled at creation (status 3 if unavailable). */
+int pdmg_paradiag_create_multi(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg,
+                               const int32_t* devices, int32_t n_devices, pdmg_paradiag** out);
+/* General diagonalizable time matrix (HeatBVM: diagonalize_time_matrix, paradiag.cpp:71-82): B = V diag(lambdas)
+ * V^{-1} supplied by the caller (host, nt x nt row-major; B real).  The time transforms g = (V^{-1} (x) I) f and
+ * u = (V (x) I) w are hand-written complex fp64 GEMM kernels over the time index (k_time_gemm), sharded like the
+ * circulant scheme; relres = ||f - (B (x) I + I (x) A) u|| / ||f||. */
+int pdmg_paradiag_create_general(int32_t n, int32_t nt, const pdmg_c128* lambdas, const pdmg_c128* V,
+                                 const pdmg_c128* Vinv, const double* B, const pdmg_mg_config* cfg,
+                                 const int32_t* devices, int32_t n_devices, pdmg_paradiag** out);
+int pdmg_paradiag_num_parts(const pdmg_paradiag* p);
+/* Shard `part`: first time slice, slice count, device. */
+int pdmg_paradiag_part_range(const pdmg_paradiag* p, int part, int32_t* t0, int32_t* count, int32_t* device);
+/* Device-resident run of a sharded solver: d_f[p], d_u[p] = shard p's slices in its device's memory. */
+int pdmg_paradiag_run_shards(pdmg_paradiag* p, const void* const* d_f, void* const* d_u, pdmg_solve_report* report,
+                             double* relres);
 void pdmg_paradiag_destroy(pdmg_paradiag* p);
-pdmg_ctx* pdmg_paradiag_solver(pdmg_paradiag* p); /* the inner batched solver (stats, levels) */
+pdmg_ctx* pdmg_paradiag_solver(pdmg_paradiag* p); /* shard 0's batched solver (stats, levels, stream) */
 int pdmg_paradiag_run(pdmg_paradiag* p, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* report,
                       double* relres);
 int pdmg_paradiag_run_device(pdmg_paradiag* p, const void* d_f, void* d_u, pdmg_solve_report* report,
@@ -140,10 +173,7 @@ int pdmg_paradiag_run_device(pdmg_paradiag* p, const void* d_f, void* d_u, pdmg_
 int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg,
                             int32_t device, const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* report,
                             double* relres);
-/* General diagonalizable time matrix (the reference's HeatBVM path: diagonalize_time_matrix, paradiag.cpp:71-82,
- * then paradiag_solve, paradiag.cpp:185-248): the caller supplies B = V diag(lambdas) V^{-1} (host, nt x nt
- * row-major; B real).  g = (V^{-1} (x) I) f and u = (V (x) I) w run as dense complex GEMMs over the time index
- * on the GPU; relres = ||f - (B (x) I + I (x) A) u|| / ||f||. */
+/* One-shot general-scheme solve on one device (pdmg_paradiag_create_general + run + destroy). */
 int pdmg_paradiag_general(int32_t n, int32_t nt, const pdmg_c128* lambdas, const pdmg_c128* V, const pdmg_c128* Vinv,
                           const double* B, const pdmg_mg_config* cfg, int32_t device, const pdmg_c128* f,
                           pdmg_c128* u, pdmg_solve_report* report, double* relres);

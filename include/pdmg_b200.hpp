@@ -100,10 +100,17 @@ struct SolveReport {
 class BatchedMultigridHierarchy {
  public:
   BatchedMultigridHierarchy(Grid2D fine, const std::vector<Shift>& shifts, const MultigridConfig& cfg, int device = 0)
+      : BatchedMultigridHierarchy(fine, shifts, cfg, std::vector<int>{}, device) {}
+  // Shifts sharded over `devices` (the reference's `threads` argument of paradiag_solve, paradiag.cpp:207-236):
+  // contiguous chunks of ceil(S / devices.size()), one engine and host thread per device.
+  BatchedMultigridHierarchy(Grid2D fine, const std::vector<Shift>& shifts, const MultigridConfig& cfg,
+                            const std::vector<int>& devices, int device = 0)
       : grid_(fine), cfg_(cfg), S_(static_cast<int>(shifts.size())) {
     std::vector<pdmg_c128> lam(shifts.size());
     for (size_t s = 0; s < shifts.size(); ++s) lam[s] = {shifts[s].lambda.real(), shifts[s].lambda.imag()};
-    pdmg_batch_desc d{fine.n, S_, lam.data(), cfg.c(), PDMG_PREC_C128, device};
+    std::vector<int32_t> devs(devices.begin(), devices.end());
+    pdmg_batch_desc d{fine.n, S_, lam.data(), cfg.c(), PDMG_PREC_C128, device,
+                      devs.empty() ? nullptr : devs.data(), static_cast<int32_t>(devs.size())};
     check(pdmg_create(&d, &ctx_));
   }
   ~BatchedMultigridHierarchy() { pdmg_destroy(ctx_); }
@@ -143,6 +150,7 @@ class BatchedMultigridHierarchy {
     check(pdmg_cycle(ctx_, reinterpret_cast<pdmg_c128*>(u.data()), reinterpret_cast<const pdmg_c128*>(b.data())));
   }
 
+  int num_parts() const { return pdmg_num_parts(ctx_); }
   pdmg_ctx* handle() const { return ctx_; }
 
  private:

@@ -375,10 +375,14 @@ int orc_dense_factor(int n, orc_cplx lambda, orc_dense* d) { /* dense.cpp:82-88 
   fro = sqrt(fro);
   orc_cplx* a = d->lu;
   double min_pivot = INFINITY;
+  /* A is banded (lower bandwidth m, upper m; with partial pivoting U's bandwidth grows to 2m): the loops
+   * below skip only entries that are exactly zero, so the factors and pivots are those of the dense
+   * elimination, operation for operation. */
   for (int k = 0; k < N; ++k) {
+    const int rmax = k + m < N - 1 ? k + m : N - 1, cmax = k + 2 * m < N - 1 ? k + 2 * m : N - 1;
     int p = k;
     double best = cabs(a[(long)k * N + k]);
-    for (int r = k + 1; r < N; ++r) {
+    for (int r = k + 1; r <= rmax; ++r) {
       const double v = cabs(a[(long)r * N + k]);
       if (v > best) best = v, p = r;
     }
@@ -392,10 +396,10 @@ int orc_dense_factor(int n, orc_cplx lambda, orc_dense* d) { /* dense.cpp:82-88 
     const orc_cplx piv = a[(long)k * N + k];
     if (cabs(piv) < min_pivot) min_pivot = cabs(piv);
     if (piv == 0.0) continue;
-    for (int r = k + 1; r < N; ++r) {
+    for (int r = k + 1; r <= rmax; ++r) {
       const orc_cplx f = a[(long)r * N + k] / piv;
       a[(long)r * N + k] = f;
-      for (int c = k + 1; c < N; ++c) a[(long)r * N + c] -= f * a[(long)k * N + c];
+      for (int c = k + 1; c <= cmax; ++c) a[(long)r * N + c] -= f * a[(long)k * N + c];
     }
   }
   d->singular = !(min_pivot > 1e-14 * fro);

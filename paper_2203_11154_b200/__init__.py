@@ -7,12 +7,13 @@ from .multigrid import (BatchedMultigridHierarchy, ConfigError, CycleKind, Devic
                         MultigridHierarchy, Shift, ShiftKind, SingularOperatorError, SmootherConfig, SmootherKind,
                         SolveReport, circulant_shifts, multigrid_solve, random_rhs)
 
-from .paradiag import (ParadiagCirculant, TimeDiagonalization, TimeDiscretization, TimeSchemeKind,  # noqa: E402
-                       all_at_once_apply, diagonalize_time_matrix, helmholtz_shifts, manufactured_field,
+from .paradiag import (ParadiagCirculant, ParadiagGeneral, TimeDiagonalization, TimeDiscretization, TimeSchemeKind,  # noqa: E402
+                       all_at_once_apply, diagonalize_qbv_closed_form, diagonalize_time_matrix, helmholtz_shifts,
+                       manufactured_field,
                        paradiag_solve, time_stepping_matrix)
 
 __all__ = [
-    "ParadiagCirculant", "TimeDiagonalization", "TimeDiscretization", "TimeSchemeKind", "all_at_once_apply",
+    "ParadiagCirculant", "ParadiagGeneral", "diagonalize_qbv_closed_form", "TimeDiagonalization", "TimeDiscretization", "TimeSchemeKind", "all_at_once_apply",
     "diagonalize_time_matrix", "helmholtz_shifts", "manufactured_field", "paradiag_solve", "time_stepping_matrix",
     "BatchedMultigridHierarchy", "ConfigError", "CycleKind", "DeviceError", "Grid2D", "MultigridConfig",
     "MultigridHierarchy", "Shift", "ShiftKind", "SingularOperatorError", "SmootherConfig", "SmootherKind",

@@ -27,7 +27,7 @@ class MgConfig(C.Structure):
 
 class BatchDesc(C.Structure):
     _fields_ = [("n", C.c_int32), ("n_shifts", C.c_int32), ("lambdas", C.c_void_p), ("cfg", MgConfig),
-                ("precision", C.c_int32), ("device", C.c_int32)]
+                ("precision", C.c_int32), ("device", C.c_int32), ("devices", C.c_void_p), ("n_devices", C.c_int32)]
 
 
 class SolveReport(C.Structure):
@@ -60,6 +60,9 @@ def lib() -> C.CDLL:
         "pdmg_coarse_singular": (C.c_int, [vp, C.c_int]),
         "pdmg_solve": (C.c_int, [vp, vp, vp, C.POINTER(SolveReport)]),
         "pdmg_solve_device": (C.c_int, [vp, vp, vp, C.POINTER(SolveReport)]),
+        "pdmg_solve_device_shards": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(SolveReport)]),
+        "pdmg_num_parts": (C.c_int, [vp]),
+        "pdmg_part_range": (C.c_int, [vp, C.c_int, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         "pdmg_cycle": (C.c_int, [vp, vp, vp]),
         "pdmg_apply_smoother": (C.c_int, [vp, C.c_int, vp, vp, vp]),
         "pdmg_residual": (C.c_int, [vp, C.c_int, vp, vp, vp]),
@@ -70,6 +73,13 @@ def lib() -> C.CDLL:
         "pdmg_paradiag_circulant": (C.c_int, [i32, i32, f64, f64, C.POINTER(MgConfig), i32, vp, vp,
                                               C.POINTER(SolveReport), C.POINTER(f64)]),
         "pdmg_paradiag_create": (C.c_int, [i32, i32, f64, f64, C.POINTER(MgConfig), i32, C.POINTER(vp)]),
+        "pdmg_paradiag_create_multi": (C.c_int, [i32, i32, f64, f64, C.POINTER(MgConfig), vp, i32, C.POINTER(vp)]),
+        "pdmg_paradiag_create_general": (C.c_int, [i32, i32, vp, vp, vp, vp, C.POINTER(MgConfig), vp, i32,
+                                                   C.POINTER(vp)]),
+        "pdmg_paradiag_num_parts": (C.c_int, [vp]),
+        "pdmg_paradiag_part_range": (C.c_int, [vp, C.c_int, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
+        "pdmg_paradiag_run_shards": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(SolveReport),
+                                               C.POINTER(f64)]),
         "pdmg_paradiag_destroy": (None, [vp]),
         "pdmg_paradiag_solver": (vp, [vp]),
         "pdmg_paradiag_run": (C.c_int, [vp, vp, vp, C.POINTER(SolveReport), C.POINTER(f64)]),
@@ -97,7 +107,7 @@ def lib() -> C.CDLL:
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.pdmg_abi_version() != 1:
+    if L.pdmg_abi_version() != 2:
         raise ImportError("libpdmg_b200.so ABI version mismatch")
     _lib = L
     return L

@@ -260,8 +260,9 @@ def cmd_paradiag(a) -> int:
     if kind_t == PD.TimeSchemeKind.HeatBVM:
         dg = PD.diagonalize_time_matrix(PD.time_stepping_matrix(td))
         lams, cond = dg.eigenvalues, dg.cond_estimate
-    else:
-        lams, cond = M.circulant_shifts(td.circulant_alpha(), td.dim(), td.tau), float("nan")
+    else:  # reference eigenvalue order (paradiag_solve already reports in it)
+        dg = PD.diagonalize_qbv_closed_form(td)
+        lams, cond = dg.eigenvalues, dg.cond_estimate
     m = RunManifest("paradiag")
     m.add("scheme", a.scheme)
     m.add("h", f"1/{N}")

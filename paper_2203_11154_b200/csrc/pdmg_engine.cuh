@@ -1,0 +1,1337 @@
+// pdmg_engine.cuh -- the batched multigrid engine (host orchestration of the sm_100a kernels in
+// pdmg_kernels.cuh) for one batch of shifts on one device, templated on the storage type T (double:
+// complex128, float: complex64).  Mirrors the reference solver path (proj/src/multigrid.cpp) for a BATCH of
+// shifts: one engine holds, for every shift, what one pdmg::MultigridHierarchy holds (level list,
+// per-level smoother coefficients, coarsest factorization) plus device storage for all levels.  Every
+// cycle is a short sequence of batched level passes over all still-active shifts; convergence is decided
+// on the device per shift (k_finalize) exactly as in MultigridHierarchy::solve, so per-shift cycle counts
+// match the reference.
+#pragma once
+#include <array>
+#include <thread>
+
+#include "pdmg_host.h"
+#include "pdmg_kernels.cuh"
+
+namespace pdmg_b200 {
+
+// ---------------------------------------------------------------------------------------------
+// Kernel variant table: flags -> instantiation of k_level.
+// ---------------------------------------------------------------------------------------------
+struct Variant {
+  bool loadu, prolong, sweep;
+  int post;
+  bool store, jacobi;
+  int key() const {
+    return (loadu ? 1 : 0) | (prolong ? 2 : 0) | (sweep ? 4 : 0) | (post << 3) | (store ? 32 : 0) | (jacobi ? 64 : 0);
+  }
+  std::string name() const {
+    std::string s;
+    if (prolong) s += loadu ? "prolong+" : "prolong0+";
+    else if (!loadu) s += "zero+";
+    if (sweep) s += jacobi ? "jacobi" : "vanka";
+    else if (!prolong) s += "pass";
+    else s.pop_back();
+    if (post == POST_NORM) s += "+norm";
+    if (post == POST_RESTRICT) s += "+restrict";
+    if (post == POST_RESID) s += "+resid";
+    return s;
+  }
+};
+
+template <class T>
+struct KernelEntry {
+  void (*fn)(LevelArgs<T>) = nullptr;
+  size_t smem = 0;
+};
+
+template <class T>
+struct KernelTable {
+  KernelEntry<T> e[128];
+  template <bool LU, bool PR, bool SW, int PO, bool ST, bool JA>
+  void reg() {
+    const int k = (LU ? 1 : 0) | (PR ? 2 : 0) | (SW ? 4 : 0) | (PO << 3) | (ST ? 32 : 0) | (JA ? 64 : 0);
+    e[k].fn = &k_level<T, LU, PR, SW, PO, ST, JA>;
+    e[k].smem = LevelShape<T, LU || PR, SW, PO, PR>::bytes;
+  }
+  template <bool LU, bool PR, int PO, bool JA>
+  void reg_sweep() {
+    reg<LU, PR, true, PO, true, JA>();
+  }
+  template <bool LU, bool PR, int PO>
+  void reg_sweep2() {
+    reg_sweep<LU, PR, PO, false>();
+    reg_sweep<LU, PR, PO, true>();
+  }
+  template <int PO>
+  void reg_sweep4() {
+    reg_sweep2<false, false, PO>();
+    reg_sweep2<true, false, PO>();
+    reg_sweep2<false, true, PO>();
+    reg_sweep2<true, true, PO>();
+  }
+  KernelTable() {
+    reg_sweep4<POST_NONE>();
+    reg_sweep4<POST_NORM>();
+    // restriction follows pre-smoothing only, which never prolongates
+    reg_sweep2<false, false, POST_RESTRICT>();
+    reg_sweep2<true, false, POST_RESTRICT>();
+    // prolongate-and-correct without a sweep (nu2 == 0)
+    reg<false, true, false, POST_NONE, true, false>();
+    reg<true, true, false, POST_NONE, true, false>();
+    reg<false, true, false, POST_NORM, true, false>();
+    reg<true, true, false, POST_NORM, true, false>();
+    // residual passes without a sweep (nu1 == 0, convergence norm, level operators)
+    reg<false, false, false, POST_NORM, false, false>();
+    reg<true, false, false, POST_NORM, false, false>();
+    reg<false, false, false, POST_RESTRICT, false, false>();
+    reg<true, false, false, POST_RESTRICT, false, false>();
+    reg<true, false, false, POST_RESID, false, false>();
+  }
+  const KernelEntry<T>& get(const Variant& v) const {
+    const KernelEntry<T>& k = e[v.key()];
+    if (!k.fn) throw std::logic_error("pdmg_b200: no kernel instantiated for variant " + v.name());
+    return k;
+  }
+};
+
+template <class T>
+struct MarchTable {
+  void (*e[128])(MarchArgs<T>) = {};
+  static int key(bool lu, bool pr, int post, bool ja, int lc, bool nin = false) {
+    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (ja ? 16 : 0) | (lc == 2 ? 32 : 0) | (nin ? 64 : 0);
+  }
+  template <bool LU, bool PR, int PO, bool JA>
+  void reg() {
+    e[key(LU, PR, PO, JA, 1)] = &k_march<T, LU, PR, PO, JA, 1>;
+    e[key(LU, PR, PO, JA, 2)] = &k_march<T, LU, PR, PO, JA, 2>;
+  }
+  template <int PO, bool JA>
+  void reg4() {
+    reg<false, false, PO, JA>();
+    reg<true, false, PO, JA>();
+    if constexpr (PO != POST_RESTRICT) {
+      reg<false, true, PO, JA>();
+      reg<true, true, PO, JA>();
+    }
+  }
+  template <bool LU, int PO, bool JA>
+  void reg_nin() {  // first fine sweep of a cycle that also yields the previous iterate's residual norm
+    e[key(LU, false, PO, JA, 2, true)] = &k_march<T, LU, false, PO, JA, 2, true>;
+  }
+  MarchTable() {
+    reg_nin<false, POST_RESTRICT, false>();
+    reg_nin<true, POST_RESTRICT, false>();
+    reg_nin<false, POST_RESTRICT, true>();
+    reg_nin<true, POST_RESTRICT, true>();
+    reg4<POST_NONE, false>();
+    reg4<POST_NONE, true>();
+    reg4<POST_NORM, false>();
+    reg4<POST_NORM, true>();
+    reg4<POST_RESTRICT, false>();
+    reg4<POST_RESTRICT, true>();
+  }
+};
+
+// fused Vanka passes (k_march2): key = loadu | prolong << 1 | post << 2 | norm_in << 4
+template <class T>
+struct March2Table {
+  using Fn = void (*)(MarchArgs<T>, CoefPack);
+  Fn e[32] = {};   // two sweeps per pass
+  Fn e1[32] = {};  // one sweep per pass (k_march2<..., TWO = false>)
+  static int key(bool lu, bool pr, int post, bool nin = false) {
+    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0);
+  }
+  template <bool LU, bool PR, int PO, bool NI = false>
+  void reg() {
+    e[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI, true>;
+    e1[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI, false>;
+  }
+  template <bool LU>
+  void reg_lu() {
+    reg<LU, false, POST_NONE>();
+    reg<LU, false, POST_RESTRICT>();
+    reg<LU, false, POST_NORM>();
+    reg<LU, true, POST_NONE>();
+    reg<LU, true, POST_NORM>();
+    reg<LU, false, POST_RESTRICT, true>();
+    reg<LU, false, POST_NONE, true>();
+  }
+  March2Table() {
+    reg_lu<false>();
+    reg_lu<true>();
+  }
+};
+
+
+template <class T>
+struct Engine : EngineBase {
+  using V = typename vec2<T>::type;
+  struct Level {
+    int n = 0, m = 0;
+    int64_t ss = 0;  // shift stride (elements)
+    size_t elems = 0;
+    V* u[2] = {nullptr, nullptr};
+    V* b = nullptr;
+    int ntx = 0, nty = 0, ntiles = 0, H = 0;
+    LevelCoef* coef = nullptr;
+    std::vector<LevelCoef> hcoef;  // host copy (kernel-parameter coefficient packs)
+    int cur = 0;
+    bool uzero = false;
+  };
+
+  std::vector<Level> lv;
+  double2* d_ainv = nullptr;
+  int coarse_N = 0;
+  int last_partials = 0;  // partial sums written by the last level pass (tiles or warp tasks per shift)
+  int *d_active = nullptr, *d_iters = nullptr, *d_conv = nullptr, *d_nactive = nullptr, *d_parity = nullptr;
+  int* d_ones = nullptr;
+  double *d_r0 = nullptr, *d_hist = nullptr, *d_partial = nullptr, *d_norms = nullptr;
+  double2* d_stage = nullptr;  // compact complex128 host-I/O staging
+  size_t stage_elems = 0;
+  // mapped pinned results, written by k_copy_words: [hist S*H doubles][iters S][conv S][nactive 2]
+  char* h_map = nullptr;
+  char* d_map = nullptr;
+  size_t map_hist() const { return 0; }
+  size_t map_iters() const { return sizeof(double) * (size_t)S * (cfg.max_iter + 1); }
+  size_t map_conv() const { return map_iters() + sizeof(int) * S; }
+  size_t map_nact() const { return map_conv() + sizeof(int) * S; }
+  void to_host(const void* dsrc, size_t map_off, size_t bytes) {
+    const int64_t w = (int64_t)(bytes / 4);
+    const int blocks = (int)std::min<int64_t>((w + 255) / 256, 148);
+    k_copy_words<<<std::max(blocks, 1), 256, 0, stream>>>((const uint32_t*)dsrc, (uint32_t*)(d_map + map_off), w);
+  }
+  cudaEvent_t ev_nactive[2] = {nullptr, nullptr};
+  int n_active_host = 0;
+  const KernelTable<T>* table = nullptr;
+  int march_min_n = 64;  // levels with n >= this use the warp-marching sweep kernel (0 = never)
+  int level_h_min_n = 512;  // levels with n >= this use 128-row strips in k_level (else 64)
+  int tail_max_n = 64;      // levels with n <= this run as one per-shift CTA cycle (k_small_cycle); 0 = off
+  int march_hs = 0;       // strip height override (0 = automatic)
+  int march_lc = 2;       // columns per lane of the marcher (1 or 2)
+
+  static const MarchTable<T>& marches() {
+    static MarchTable<T> t;
+    return t;
+  }
+  static const March2Table<T>& marches2() {
+    static March2Table<T> t;
+    return t;
+  }
+  int march2_min_n = 64;  // levels with n >= this run Vanka sweep pairs as one k_march2 pass (0 = never)
+  int march2_hs = 0;      // strip height override (0 = automatic)
+  // per-level strip heights (tuning: PDMG_MARCH2_HS_R / _P = "n:H,n:H,..." for the non-prolongating /
+  // prolongating passes; levels not listed use march2_hs_default)
+  std::vector<std::pair<int, int>> march2_hs_r, march2_hs_p;
+  int march2_prolong_b = 0;  // prolongating passes may use loop shape (b) on levels with n >= march2_loopb_min_n
+  static int march2_ha(int post, bool two) {  // = k_march2's hA
+    return ((two ? 4 : 2) + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;
+  }
+  int march2_tasks(int n, int post, bool two, bool prolong) const {  // warp tasks per shift of a k_march2 pass
+    const int wout = 64 - 2 * march2_ha(post, two), hs = march2_hs_for(n, prolong);
+    return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
+  }
+  int march2_hs_for(int n, bool prolong) const {
+    if (march2_hs > 0) return march2_hs;
+    for (auto& e : prolong ? march2_hs_p : march2_hs_r)
+      if (e.first == n) return e.second;
+    return n >= 512 ? 128 : n >= 256 ? 64 : 32;  // measured at C3 (DESIGN 3.2b)
+  }
+  bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
+  int march2_loopb_min_n = 128;  // (prolongating passes: shape (a), see march2_prolong_b)
+  bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
+  double pred_final = 0.5;  // predicted-last-norm threshold (solve_device; 0 = off, PDMG_PRED_FINAL)
+  int nin_k = -1;         // cycle_level: the first fine pass computes the norm of iterate nin_k (>= 0)
+  // the first fine pass of a cycle must be a marching sweep that can also form ||b - L u_in||: the single
+  // sweep + restriction (nu1 = 1) or a fused pair (even nu1)
+  bool use_norm_next() const {
+    if (!norm_next || lv.size() < 2) return false;
+    if (cfg.nu1 == 1) return march_min_n > 0 && lv[0].n >= march_min_n && march_lc == 2;
+    return march2_pre && use_march2(0) && cfg.nu1 >= 2 && cfg.nu1 % 2 == 0;
+  }
+  bool use_march2(int l) const {
+    return march2_min_n > 0 && lv[l].n >= march2_min_n && cfg.smoother == PDMG_SMOOTHER_VANKA;
+  }
+  std::unique_ptr<CoefPack> cpack{new CoefPack()};
+  // coefficients of engine shifts [c0, c0 + cnt) (RangeView: engine shift s = global shift s_base + s)
+  void fill_pack(const Level& Lv, int c0, int cnt) {
+    cpack->inv_h2 = Lv.hcoef.empty() ? 0.0 : Lv.hcoef[0].inv_h2;
+    cpack->shift0 = c0;
+    for (int i = 0; i < cnt; ++i) {
+      const LevelCoef& c = Lv.hcoef[s_base + c0 + i];
+      cpack->c[i] = CoefU{c.dd, c.k0, c.k1, c.k2};
+    }
+  }
+  // two consecutive Vanka sweeps u[cur] -> u[cur^1] (+ prolongation of ec before, + restriction/norm after)
+  // two = false: ONE Vanka sweep through the same kernel (k_march2<..., TWO = false>)
+  void level_pass2(int l, bool loadu, bool prolong, int post, const V* uin, V* uout, const V* b, const V* ec, V* bc,
+                   const int* active, int n_act, bool norm_in = false, bool two = true) {
+    const Level& Lv = lv[l];
+    MarchArgs<T> ma{};
+    ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
+    ma.coef = Lv.coef, ma.active = active, ma.n = Lv.n;
+    ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
+    ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
+    const int wout = 64 - 2 * march2_ha(post, two);
+    ma.Hs = march2_hs_for(Lv.n, prolong);
+    // loop shape (a) for prolongating passes unless march2_prolong_b (measured, DESIGN 3.2b)
+    ma.loop_a = Lv.n < march2_loopb_min_n || (prolong && !march2_prolong_b);
+    ma.ntx = (Lv.n + wout - 1) / wout;
+    ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
+    if (ma.ntasks != march2_tasks(Lv.n, post, two, prolong)) throw std::logic_error("pdmg_b200: march2 task count");
+    const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
+    auto fn = two ? marches2().e[key2] : marches2().e1[key2];
+    if (!fn) throw std::logic_error("pdmg_b200: no two-sweep kernel for this variant");
+    const double S_ = sizeof(V), pts = (double)n_act * Lv.m * Lv.m;
+    const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0);
+    std::string cls = "L" + std::to_string(l) + ":" + (prolong ? (loadu ? "prolong+" : "prolong0+") : (loadu ? "" : "zero+")) +
+                      (two ? "vanka2" : "vanka") + (post == POST_NORM ? "+norm" : post == POST_RESTRICT ? "+restrict" : "") +
+                      (norm_in ? "+norm_in" : "");
+    const double ubpp = (two ? 2 : 1) * 3 * S_ + (prolong ? S_ / 4 : 0) + (post == POST_RESTRICT ? S_ / 4 : 0);
+    timed(cls, pts * bpp, [&] {
+      for (int c0 = 0; c0 < S; c0 += COEF_MAX) {  // one launch per COEF_MAX shifts (coefficients as parameters)
+        const int cnt = std::min(COEF_MAX, S - c0);
+        fill_pack(Lv, c0, cnt);
+        dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, cnt);
+        fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma, *cpack);
+      }
+    }, pts * ubpp, (two ? 2 : 1) * pts);
+    last_partials = ma.ntasks;
+  }
+  // measured on B200 (C3, C4): the marcher wins for sweep+norm and sweep+restrict, the ring
+  // kernel for the plain and prolongating sweeps; PDMG_MARCH_ALL=1 routes every sweep variant to the marcher
+  bool march_all = false;
+  // single Vanka sweeps on levels with n >= march2_min_n through k_march2<TWO = false> (PDMG_MARCH1=0: the
+  // older k_level / k_march kernels)
+  bool march1 = true;
+  bool resid_norm_kernel = true;  // residual-only norm passes through k_resid_norm (PDMG_RESID_NORM=0: k_level)
+  bool use_march1(int l, const Variant& v) const {
+    return march1 && march2_min_n > 0 && lv[l].n >= march2_min_n && v.sweep && v.store && !v.jacobi &&
+           v.post != POST_RESID && marches2().e1[March2Table<T>::key(v.loadu, v.prolong, v.post)] != nullptr;
+  }
+  bool use_march(int l, const Variant& v) const {
+    if (!(march_min_n > 0 && lv[l].n >= march_min_n && v.sweep && v.store && v.post != POST_RESID)) return false;
+    if (march_all) return true;
+    return !v.prolong && (v.post == POST_NORM || v.post == POST_RESTRICT);
+  }
+  int march_hs_for(int n) const { return march_hs > 0 ? march_hs : (n >= 512 ? 128 : 64); }
+  int march_tasks(int l, int post) const {
+    const int hA = (post == POST_RESTRICT ? 1 : post == POST_NONE ? -1 : 0) + 3;
+    const int wout = 32 - 2 * hA, n = lv[l].n, hs = march_hs_for(n);  // LC = 1 (most tasks): sizing bound
+    return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
+  }
+
+  bool use_small_path() const {
+    if (solve_path == 1) return false;
+    if (solve_path == 2) return true;
+    return lv[0].n <= 128 && lv.size() <= MAX_LEVELS;  // BASELINE configs 1-2: launch/sync latency bound
+  }
+
+  static const KernelTable<T>& kernels() {
+    static KernelTable<T> t;
+    return t;
+  }
+
+  ~Engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& L : lv) {
+      if (!borrow) {
+        cudaFree(L.u[0]);
+        cudaFree(L.u[1]);
+        cudaFree(L.b);
+      }
+      cudaFree(L.coef);
+    }
+    cudaFree(d_ainv);
+    cudaFree(d_active);
+    cudaFree(d_iters);
+    cudaFree(d_conv);
+    cudaFree(d_nactive);
+    cudaFree(d_parity);
+    cudaFree(d_ones);
+    cudaFree(d_r0);
+    cudaFree(d_hist);
+    cudaFree(d_partial);
+    cudaFree(d_norms);
+    cudaFree(d_stage);
+    if (h_map) cudaFreeHost(h_map);
+    for (auto e : ev_nactive)
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ---- construction: host validation first (no CUDA), then device allocation ----------------
+  void setup_host(const pdmg_batch_desc& d) override {
+    desc_ = d;
+    desc_.lambdas = nullptr;  // (the engine keeps its own copy in `lambdas`)
+    if (d.n_shifts < 1) throw ConfigError("pdmg_create: n_shifts must be >= 1");
+    if (d.n_shifts > 65535) throw ConfigError("pdmg_create: n_shifts must be <= 65535 per context");
+    if (!d.lambdas) throw ConfigError("pdmg_create: lambdas is NULL");
+    cfg = d.cfg;
+    ln = level_list(d.n, cfg);
+    S = d.n_shifts;
+    lambdas.resize(S);
+    for (int s = 0; s < S; ++s) lambdas[s] = cplx(d.lambdas[s].re, d.lambdas[s].im);
+    // smoother validity on every non-coarsest level (multigrid.cpp:47-58), in shift order
+    for (int s = 0; s < S; ++s)
+      for (size_t l = 0; l + 1 < ln.size(); ++l) {
+        const double h = 1.0 / ln[l];
+        try {
+          if (cfg.smoother == PDMG_SMOOTHER_VANKA) (void)vanka_coeffs(lambdas[s] * (h * h));
+          else (void)jacobi_weight(lambdas[s] * (h * h), h);
+        } catch (const SingularOperatorError& e) {
+          throw SingularOperatorError("level " + std::to_string(l) + " (n = " + std::to_string(ln[l]) + "): " + e.what());
+        }
+      }
+    if (ln.back() > 128)
+      throw ConfigError("dense_shifted_operator: dense assembly refused for n = " + std::to_string(ln.back()) +
+                        " (limit 128)");
+  }
+
+  void setup_device(int dev) override {
+    device = dev;
+    if (const char* e = std::getenv("PDMG_TAIL_MAX_N")) tail_max_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
+    auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
+      out.clear();
+      for (const char* q = e; *q;) {
+        int n = 0, h = 0;
+        if (std::sscanf(q, "%d:%d", &n, &h) == 2 && n > 0 && h > 0) out.emplace_back(n, h);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    };
+    if (const char* e = std::getenv("PDMG_MARCH2_HS_R")) parse_hs(e, march2_hs_r);
+    if (const char* e = std::getenv("PDMG_MARCH2_HS_P")) parse_hs(e, march2_hs_p);
+    if (const char* e = std::getenv("PDMG_MARCH1")) march1 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_PRED_FINAL")) pred_final = std::atof(e);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (dev < 0 || dev >= ndev) throw CudaError("pdmg_create: CUDA device " + std::to_string(dev) + " not available");
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, stream_priority));
+    table = &kernels();
+    const int L = (int)ln.size();
+    lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+      Level& Lv = lv[l];
+      Lv.n = ln[l];
+      Lv.m = Lv.n - 1;
+      Lv.ss = (int64_t)(Lv.n + 1) * Lv.n;
+      Lv.elems = (size_t)Lv.ss * S + Lv.n + 2;  // + guard so the last shift's ghost reads stay in bounds
+      if (borrow) {
+        // the parent's arrays are zeroed (ghost rings included); past the last shift of a middle range the
+        // guard reads land in the next range's first shift, exactly as they do inside the parent
+        const Level& P = borrow->lv[l];
+        const int64_t off = (int64_t)borrow_s0 * Lv.ss;
+        Lv.u[0] = P.u[0] + off, Lv.u[1] = P.u[1] + off, Lv.b = P.b + off;
+        if (borrow_s0 + S < borrow->S) Lv.elems = (size_t)Lv.ss * S;
+      } else {
+        for (V** p : {&Lv.u[0], &Lv.u[1], &Lv.b}) {
+          CK(cudaMalloc(p, Lv.elems * sizeof(V)));
+          CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
+        }
+      }
+      Lv.H = std::min(Lv.n >= level_h_min_n ? 128 : 64, Lv.n + (Lv.n & 1));
+      Lv.ntx = (Lv.n + TILE_W - 1) / TILE_W;
+      Lv.nty = (Lv.n + Lv.H - 1) / Lv.H;
+      Lv.ntiles = Lv.ntx * Lv.nty;
+      // coefficients (multigrid.cpp:47-58 per level; smoother.cpp:31-40 stencil; grid.cpp:73 diagonal)
+      std::vector<LevelCoef> hc(S);
+      const double h = 1.0 / Lv.n;
+      for (int s = 0; s < S; ++s) {
+        const cplx eta = lambdas[s] * (h * h);
+        const cplx dd = cplx(4.0, 0.0) + eta;
+        cplx k0(0, 0), k1(0, 0), k2(0, 0);
+        if (l + 1 < L) {
+          if (cfg.smoother == PDMG_SMOOTHER_VANKA) {
+            const Vanka v = vanka_coeffs(eta);
+            const double sc = cfg.omega * (h * h / 4.0);
+            k0 = sc * (4.0 * v.a);
+            k1 = sc * (2.0 * v.b);
+            k2 = sc * v.c;
+          } else {
+            k0 = cfg.omega * jacobi_weight(eta, h);
+          }
+        }
+        LevelCoef& c = hc[s];
+        c.d = make_double2(dd.real(), dd.imag());
+        c.dd = make_double2(dd.real() / (h * h), dd.imag() / (h * h));
+        c.k0 = make_double2(k0.real(), k0.imag());
+        c.k1 = make_double2(k1.real(), k1.imag());
+        c.k2 = make_double2(k2.real(), k2.imag());
+        c.inv_h2 = 1.0 / (h * h);
+        c.pad_ = 0;
+      }
+      Lv.hcoef = hc;
+      CK(cudaMalloc(&Lv.coef, sizeof(LevelCoef) * S));
+      CK(cudaMemcpyAsync(Lv.coef, hc.data(), sizeof(LevelCoef) * S, cudaMemcpyHostToDevice, stream));
+    }
+    // coarsest factorizations (dense.cpp:82-88), one per shift
+    const int nc = ln.back(), mc = nc - 1;
+    coarse_N = mc * mc;
+    coarse_singular.assign(S, 0);
+    std::vector<double2> hinv((size_t)S * coarse_N * coarse_N);
+    for (int s = 0; s < S; ++s) {
+      CoarseFactor cf = factor_coarse(nc, lambdas[s]);
+      coarse_singular[s] = cf.singular;
+      any_singular |= cf.singular;
+      for (size_t q = 0; q < cf.inv.size(); ++q) {
+        hinv[(size_t)s * coarse_N * coarse_N + q] = make_double2(cf.inv[q].real(), cf.inv[q].imag());
+      }
+    }
+    // the coarse-solve kernels stage the coarsest right-hand side (coarse_N complex values) in dynamic shared
+    // memory: opt in above the 48 KB default, and refuse grids whose coarsest level cannot fit (the reference
+    // accepts coarsest_n up to 128, dense.cpp:9-15; 16 B per unknown caps it at 119 here)
+    {
+      int optin = 0;
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      const size_t need = (size_t)coarse_N * sizeof(double2), static_red = 33 * sizeof(double);
+      if (need + static_red > (size_t)optin)
+        throw ConfigError("MultigridHierarchy: coarsest grid n = " + std::to_string(nc) + " needs " +
+                          std::to_string(need) + " B of shared memory for the batched direct solve (device limit " +
+                          std::to_string(optin - (int)static_red) + " B; coarsest_n <= 119)");
+      const int sm = (int)std::max<size_t>(need, 1);
+      CK(cudaFuncSetAttribute(k_coarse_solve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_small_cycle<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_small_solve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    }
+    CK(cudaMalloc(&d_ainv, sizeof(double2) * hinv.size()));
+    CK(cudaMemcpyAsync(d_ainv, hinv.data(), sizeof(double2) * hinv.size(), cudaMemcpyHostToDevice, stream));
+    // solve state
+    int maxtiles = 1;
+    for (size_t l = 0; l < lv.size(); ++l) {
+      maxtiles = std::max(maxtiles, lv[l].ntiles);
+      for (int post : {POST_NONE, POST_NORM, POST_RESTRICT}) {
+        maxtiles = std::max(maxtiles, march_tasks((int)l, post));
+        for (int two = 0; two < 2; ++two)
+          for (int pr = 0; pr < 2; ++pr) maxtiles = std::max(maxtiles, march2_tasks(lv[l].n, post, two != 0, pr != 0));
+      }
+      maxtiles = std::max(maxtiles, (lv[l].n - 1 + RN_ROWS - 1) / RN_ROWS);  // k_resid_norm
+    }
+    CK(cudaMalloc(&d_active, sizeof(int) * S));
+    CK(cudaMalloc(&d_iters, sizeof(int) * S));
+    CK(cudaMalloc(&d_conv, sizeof(int) * S));
+    CK(cudaMalloc(&d_nactive, 6 * sizeof(int)));  // [n_active slot 0, 1][pred slot 0, 1 (8 B each)]
+    CK(cudaMalloc(&d_parity, sizeof(int) * (cfg.max_iter + 1)));
+    CK(cudaMalloc(&d_ones, sizeof(int) * S));
+    CK(cudaMalloc(&d_r0, sizeof(double) * S));
+    CK(cudaMalloc(&d_hist, sizeof(double) * S * (size_t)(cfg.max_iter + 1)));
+    CK(cudaMalloc(&d_partial, sizeof(double) * S * (size_t)maxtiles));
+    CK(cudaMalloc(&d_norms, sizeof(double) * S));
+    std::vector<int> ones(S, 1);
+    CK(cudaMemcpyAsync(d_ones, ones.data(), sizeof(int) * S, cudaMemcpyHostToDevice, stream));
+    CK(cudaHostAlloc((void**)&h_map, map_nact() + 6 * sizeof(int), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&d_map, h_map, 0));
+    CK(cudaEventCreateWithFlags(&ev_nactive[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_nactive[1], cudaEventDisableTiming));
+    for (auto& kv : table->e)
+      if (kv.fn) CK(cudaFuncSetAttribute(kv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.smem));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // ---- kernel launch ------------------------------------------------------------------------
+  void level_pass(int l, const Variant& v, const V* uin, V* uout, const V* b, const V* ec, V* bc, const int* active,
+                  int n_act, bool norm_in = false) {
+    const Level& Lv = lv[l];
+    LevelArgs<T> a{};
+    a.u_in = uin;
+    a.u_out = uout;
+    a.b = b;
+    a.ec = ec;
+    a.bc = bc;
+    a.partial = d_partial;
+    a.coef = Lv.coef;
+    a.active = active;
+    a.n = Lv.n;
+    a.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
+    a.ss = Lv.ss;
+    a.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
+    a.ntx = Lv.ntx;
+    a.ntiles = Lv.ntiles;
+    a.H = Lv.H;
+    const double pts = (double)n_act * Lv.m * Lv.m, S_ = sizeof(V);
+    double bpp = 0;  // algorithmic DRAM bytes per point
+    if (v.loadu) bpp += S_;
+    if (v.sweep || v.post != POST_NONE) bpp += S_;  // b
+    if (v.prolong) bpp += S_ / 4;
+    if (v.store || v.post == POST_RESID) bpp += S_;
+    if (v.post == POST_RESTRICT) bpp += S_ / 4;
+    const std::string cls = "L" + std::to_string(l) + ":" + v.name() + (norm_in ? "+norm_in" : "");
+    // a smoother update is 3 S (u in, b in, u out) whatever the pass actually moves
+    const double ubpp = v.sweep ? 3 * S_ + (v.prolong ? S_ / 4 : 0) + (v.post == POST_RESTRICT ? S_ / 4 : 0) : -1.0;
+    const double ub = ubpp < 0 ? -1.0 : pts * ubpp, nupd = v.sweep ? pts : 0.0;
+    if (resid_norm_kernel && v.loadu && !v.prolong && !v.sweep && !v.store && v.post == POST_NORM && !norm_in) {
+      const int ntiles = (Lv.m + RN_ROWS - 1) / RN_ROWS;
+      dim3 grid(ntiles, S);
+      timed(cls, pts * bpp, [&] {
+        k_resid_norm<T><<<grid, RN_THREADS, 0, stream>>>(uin, b, Lv.coef, active, Lv.n, Lv.ss, d_partial);
+      }, ub, nupd);
+      last_partials = ntiles;
+      return;
+    }
+    if (use_march1(l, v)) {
+      level_pass2(l, v.loadu, v.prolong, v.post, uin, uout, b, ec, bc, active, n_act, norm_in, false);
+      return;
+    }
+    if (norm_in && !use_march(l, v)) throw std::logic_error("pdmg_b200: norm_in needs the marching kernel");
+    if (use_march(l, v)) {
+      MarchArgs<T> ma{};
+      ma.u_in = uin, ma.u_out = uout, ma.b = b, ma.ec = ec, ma.bc = bc, ma.partial = d_partial;
+      ma.coef = Lv.coef, ma.active = active, ma.n = a.n, ma.nc = a.nc, ma.ss = a.ss, ma.ssc = a.ssc;
+      const int hA = (v.post == POST_RESTRICT ? 4 : v.post == POST_NORM ? 3 : 2);
+      const int wout = 32 * march_lc - 2 * hA;
+      ma.Hs = march_hs_for(Lv.n);
+      ma.ntx = (Lv.n + wout - 1) / wout;
+      ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
+      auto fn = marches().e[MarchTable<T>::key(v.loadu, v.prolong, v.post, v.jacobi, march_lc, norm_in)];
+      if (!fn) throw std::logic_error("pdmg_b200: no march kernel for variant " + v.name());
+      dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, S);
+      timed(cls, pts * bpp, [&] { fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma); }, ub, nupd);
+      last_partials = ma.ntasks;
+      return;
+    }
+    const KernelEntry<T>& k = table->get(v);
+    dim3 grid(Lv.ntiles, S);
+    timed(cls, pts * bpp, [&] { k.fn<<<grid, NTHREADS, k.smem, stream>>>(a); }, ub, nupd);
+    last_partials = Lv.ntiles;
+  }
+
+  void coarse_solve(const V* b, V* u, const int* active) {
+    const Level& Lv = lv.back();
+    const int thr = std::min(1024, std::max(32, ((coarse_N + 31) / 32) * 32));
+    const double bytes = (double)S * coarse_N * (coarse_N + 2) * sizeof(V);
+    timed("coarse_solve", bytes, [&] {
+      k_coarse_solve<T><<<S, thr, coarse_N * sizeof(double2), stream>>>(b, u, d_ainv, active, Lv.n, Lv.ss);
+    });
+  }
+
+  // ---- one cycle on level l (multigrid.cpp:63-77) -------------------------------------------
+  // zero: u on this level is known to be zero on entry (ec = 0 before recursing, multigrid.cpp:72;
+  // u = 0 before the first fine cycle, multigrid.cpp:90).  fuse_norm: leave ||b - L u||^2 partials of
+  // the updated fine iterate in d_partial (returns whether it did).
+  // first level of the coarse tail (levels with n <= tail_max_n below the finest), or -1
+  int tail_level() const {
+    if (tail_max_n <= 0 || (int)lv.size() > MAX_LEVELS) return -1;
+    for (int l = 1; l < (int)lv.size(); ++l)
+      if (lv[l].n <= tail_max_n) return l;
+    return -1;
+  }
+  // Block size of the one-CTA-per-shift kernels (64 registers/thread: 1024 threads fill an SM's register
+  // file).  Smaller blocks once S exceeds the SM count keep every shift resident in a single wave.
+  int small_threads_env = 0;
+  int small_threads() const {
+    if (small_threads_env > 0) return small_threads_env;
+    int sms = 148;
+    return S <= sms ? SMALL_THREADS : S <= 2 * sms ? SMALL_THREADS / 2 : SMALL_THREADS / 4;
+  }
+  void tail_cycle(int l, const int* active, bool zero) {
+    SmallArgs<T> sa{};
+    for (size_t q = l; q < lv.size(); ++q)
+      sa.lv[q - l] = SmallLevel<T>{lv[q].u[0], lv[q].u[1], lv[q].b, lv[q].coef, lv[q].n, lv[q].ss};
+    sa.L = (int)lv.size() - l;
+    sa.nu1 = cfg.nu1, sa.nu2 = cfg.nu2, sa.gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+    sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
+    sa.ainv = d_ainv, sa.coarse_N = coarse_N, sa.active = active, sa.tail_zero = zero ? 1 : 0;
+    timed("coarse_tail", 0.0,
+          [&] { k_small_cycle<T><<<S, small_threads(), coarse_N * sizeof(double2), stream>>>(sa); });
+    for (size_t q = l; q < lv.size(); ++q) lv[q].cur = 0, lv[q].uzero = false;
+  }
+
+  bool cycle_level(int l, bool zero, const int* active, int n_act, bool want_norm) {
+    Level& Lv = lv[l];
+    const int L = (int)lv.size();
+    const bool jac = cfg.smoother == PDMG_SMOOTHER_JACOBI;
+    if (l > 0 && l == tail_level()) {  // the whole coarse tail in one launch (each visit of a W-cycle)
+      tail_cycle(l, active, zero);
+      return false;
+    }
+    if (l + 1 == L) {
+      coarse_solve(Lv.b, Lv.u[Lv.cur], active);
+      Lv.uzero = false;
+      return false;
+    }
+    Level& Lc = lv[l + 1];
+    if (zero) Lv.uzero = true;
+    const bool pair = use_march2(l) && march2_pre;
+    for (int k = 0; k < cfg.nu1; ++k) {
+      const bool last = k == cfg.nu1 - 1;
+      if (pair && (cfg.nu1 - k) % 2 == 0) {  // sweeps k, k+1 as one pass (the pairs end at the last sweep)
+        const bool nin = l == 0 && k == 0 && nin_k >= 0;
+        level_pass2(l, !Lv.uzero, false, k + 2 == cfg.nu1 ? POST_RESTRICT : POST_NONE, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1],
+                    Lv.b, nullptr, Lc.b, active, n_act, nin);
+        if (nin) {  // convergence bookkeeping of the previous iterate (still in u[cur]) before the rest runs
+          finalize(nin_k, last_partials, false, Lv.cur);
+          nin_k = -1;
+        }
+        Lv.cur ^= 1;
+        Lv.uzero = false;
+        ++k;
+        continue;
+      }
+      Variant v{!Lv.uzero, false, true, last ? POST_RESTRICT : POST_NONE, true, jac};
+      const bool nin = l == 0 && k == 0 && nin_k >= 0;  // (only with nu1 == 1: see use_norm_next)
+      level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, nullptr, Lc.b, active, n_act, nin);
+      if (nin) {
+        finalize(nin_k, last_partials, false, Lv.cur);
+        nin_k = -1;
+      }
+      Lv.cur ^= 1;
+      Lv.uzero = false;
+    }
+    if (cfg.nu1 == 0) {
+      Variant v{!Lv.uzero, false, false, POST_RESTRICT, false, false};
+      level_pass(l, v, Lv.u[Lv.cur], nullptr, Lv.b, nullptr, Lc.b, active, n_act);
+    }
+    const int gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+    for (int g = 0; g < gamma; ++g) cycle_level(l + 1, g == 0, active, n_act, false);
+    const V* ec = Lc.u[Lc.cur];
+    bool normed = false;
+    if (cfg.nu2 > 0) {
+      for (int k = 0; k < cfg.nu2; ++k) {
+        const bool last = k == cfg.nu2 - 1;
+        if (use_march2(l) && march2_post && k + 1 < cfg.nu2) {  // sweeps k, k+1 as one pass (pairs from the first, prolongating, sweep)
+          const int post2 = (k + 2 == cfg.nu2 && want_norm) ? POST_NORM : POST_NONE;
+          level_pass2(l, k == 0 ? !Lv.uzero : true, k == 0, post2, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b,
+                      k == 0 ? ec : nullptr, nullptr, active, n_act);
+          Lv.cur ^= 1;
+          Lv.uzero = false;
+          normed = post2 == POST_NORM;
+          ++k;
+          continue;
+        }
+        const int post = (last && want_norm) ? POST_NORM : POST_NONE;
+        Variant v{k == 0 ? !Lv.uzero : true, k == 0, true, post, true, jac};
+        level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, k == 0 ? ec : nullptr, nullptr, active, n_act);
+        Lv.cur ^= 1;
+        Lv.uzero = false;
+        normed = post == POST_NORM;
+      }
+    } else {
+      Variant v{!Lv.uzero, true, false, want_norm ? POST_NORM : POST_NONE, true, false};
+      level_pass(l, v, Lv.u[Lv.cur], Lv.u[Lv.cur ^ 1], Lv.b, ec, nullptr, active, n_act);
+      Lv.cur ^= 1;
+      Lv.uzero = false;
+      normed = want_norm;
+    }
+    return normed;
+  }
+
+  // Convergence bookkeeping of cycle k (k_finalize); the active count lands in pinned slot k % 2.  With
+  // wait = false the host does not block: the solve loop enqueues cycle k+1 before reading cycle k's count
+  // (converged shifts are frozen on the device, so a speculative extra cycle leaves them untouched).
+  void finalize(int k, int ntiles, bool wait = true, int cur = 0) {
+    const int slot = k & 1;
+    unsigned long long* d_pred = reinterpret_cast<unsigned long long*>(d_nactive + 2) + slot;
+    CK(cudaMemsetAsync(d_nactive + slot, 0, sizeof(int), stream));
+    CK(cudaMemsetAsync(d_pred, 0, sizeof(unsigned long long), stream));
+    SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol, d_parity, cur,
+                  d_pred};
+    const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
+    timed("finalize", 0.0, [&] { k_finalize<<<blocks, threads, 0, stream>>>(d_partial, ntiles, k, st); });
+    to_host(d_nactive, map_nact(), 6 * sizeof(int));  // both slots' counts and predictions (24 B, one launch)
+    CK(cudaEventRecord(ev_nactive[slot], stream));
+    if (wait) n_active_host = read_nactive(k);
+  }
+  int read_nactive(int k) {
+    CK(cudaEventSynchronize(ev_nactive[k & 1]));
+    return ((volatile int*)(h_map + map_nact()))[k & 1];
+  }
+  // after read_nactive(k): max over the still-active shifts of the predicted r_{k+1} / (tol r0)
+  double read_pred(int k) {
+    const unsigned long long v = ((volatile unsigned long long*)(h_map + map_nact() + 2 * sizeof(int)))[k & 1];
+    double q;
+    std::memcpy(&q, &v, sizeof(q));
+    return q;
+  }
+
+  void unpack(const double2* src, V* dst, int l) {
+    const Level& Lv = lv[l];
+    const int64_t total = (int64_t)S * Lv.m * Lv.m;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    timed("unpack", (double)total * 2 * sizeof(V),
+          [&] { k_unpack<T><<<blocks, 256, 0, stream>>>(src, dst, Lv.n, Lv.ss, total); });
+  }
+  void pack(const V* b0, const V* b1, const int* iters, const int* parity, double2* dst, int l) {
+    const Level& Lv = lv[l];
+    const int64_t total = (int64_t)S * Lv.m * Lv.m;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    timed("pack", (double)total * 2 * sizeof(V),
+          [&] { k_pack<T><<<blocks, 256, 0, stream>>>(b0, b1, iters, parity, dst, Lv.n, Lv.ss, total); });
+  }
+
+  // ---- MultigridHierarchy::solve for all shifts (multigrid.cpp:85-110) -----------------------
+  void solve_device(const double2* d_b, double2* d_u, pdmg_solve_report* rep) override {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(device));
+    Level& F = lv[0];
+    const int H = cfg.max_iter + 1;
+    unpack(d_b, F.b, 0);
+    CK(cudaMemsetAsync(F.u[0], 0, F.elems * sizeof(V), stream));
+    F.cur = 0;
+    CK(cudaMemcpyAsync(d_active, d_ones, sizeof(int) * S, cudaMemcpyDeviceToDevice, stream));
+    CK(cudaMemsetAsync(d_iters, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_conv, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_hist, 0, sizeof(double) * S * (size_t)H, stream));
+    if (use_small_path()) {
+      if (any_singular) {
+        // the reference throws at the first coarse solve, i.e. only for shifts that run a cycle
+        std::vector<double> nb(S);
+        level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
+                   nullptr, S);
+        finalize(0, last_partials);
+        std::vector<int> act(S);
+        CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
+        for (int s = 0; s < S; ++s)
+          if (act[s] && coarse_singular[s_base + s])
+            throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " +
+                                        std::to_string(lv.back().n));
+      }
+      SmallArgs<T> sa{};
+      for (size_t l = 0; l < lv.size(); ++l)
+        sa.lv[l] = SmallLevel<T>{lv[l].u[0], lv[l].u[1], lv[l].b, lv[l].coef, lv[l].n, lv[l].ss};
+      sa.L = (int)lv.size();
+      sa.nu1 = cfg.nu1, sa.nu2 = cfg.nu2, sa.gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
+      sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
+      sa.ainv = d_ainv, sa.coarse_N = coarse_N;
+      sa.iterations = d_iters, sa.converged = d_conv, sa.r0 = d_r0, sa.hist = d_hist, sa.n_active = d_nactive;  // unused
+      const double per_shift_bytes = 0.0;
+      (void)per_shift_bytes;
+      timed("small_solve", 0.0, [&] {
+        k_small_solve<T><<<S, small_threads(), coarse_N * sizeof(double2), stream>>>(sa);
+      });
+      CK(cudaGetLastError());
+      CK(cudaMemsetAsync(d_parity, 0, sizeof(int) * H, stream));
+      pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+      finish_report(rep, t0, H);
+      return;
+    }
+    if (use_norm_next() && !any_singular) {
+      // The residual norm of iterate k-1 (multigrid.cpp:91, 96-105) is the first fine sweep's residual in
+      // cycle k: that pass leaves its partials, k_finalize(k-1) runs right after it (freezing converged
+      // shifts, whose iterate stays in the other buffer) and the rest of cycle k runs for the active ones.
+      // The host reads count(k-1) once cycle k is enqueued, so it enqueues cycle k+1 while the GPU is
+      // still in cycle k.  After max_iter cycles one norm pass closes the history.
+      // Predicted last norm: when every active shift's predicted r_{k-1} (from finalize(k-2): the last
+      // ratio times the last contraction) is below pred_final * tol * r0, iterate k-1's norm is formed by
+      // a residual-only pass instead of cycle k's first (fused, two-sweep) pass, which would otherwise be
+      // spent only to find that every shift has converged.  Mispredicted, cycle k runs without norm_in.
+      int n_act = S, k = 1;
+      double pred = 1e300;
+      for (; k <= cfg.max_iter; ++k) {
+        if (pred_final > 0 && k >= 4 && pred <= pred_final) {
+          level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr,
+                     nullptr, d_active, n_act);
+          finalize(k - 1, last_partials, true, F.cur);
+          n_act = n_active_host;
+          if (n_act == 0) break;
+          pred = read_pred(k - 1);
+          nin_k = -1;
+          cycle_level(0, false, d_active, n_act, false);
+          continue;
+        }
+        nin_k = k - 1;
+        const bool normed = cycle_level(0, k == 1, d_active, n_act, false);
+        (void)normed;
+        n_act = read_nactive(k - 1);
+        if (n_act == 0) break;
+        pred = read_pred(k - 1);
+      }
+      if (k > cfg.max_iter) {
+        level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr,
+                   nullptr, d_active, n_act);
+        finalize(cfg.max_iter, last_partials, true, F.cur);
+      }
+      pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+      finish_report(rep, t0, H);
+      return;
+    }
+    // r0 = ||b|| (multigrid.cpp:91): residual of the zero guess
+    level_pass(0, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, F.b, nullptr, nullptr,
+               nullptr, S);
+    finalize(0, last_partials);
+    if (any_singular && n_active_host > 0) {
+      std::vector<int> act(S);
+      CK(cudaMemcpy(act.data(), d_active, sizeof(int) * S, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < S; ++s)
+        if (act[s] && coarse_singular[s_base + s])
+          throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
+    }
+    // cycles are enqueued one ahead of the host's convergence check (pipelined: the GPU never idles on it)
+    int n_act = n_active_host;
+    for (int k = 1; k <= cfg.max_iter && n_act > 0; ++k) {
+      const bool normed = cycle_level(0, k == 1, d_active, n_act, true);
+      if (!normed)
+        level_pass(0, Variant{true, false, false, POST_NORM, false, false}, F.u[F.cur], nullptr, F.b, nullptr, nullptr,
+                   d_active, n_act);
+      finalize(k, last_partials, false, F.cur);  // records parity[k] = F.cur on the device
+      if (k >= 2 || k == cfg.max_iter) n_act = read_nactive(k == cfg.max_iter ? k : k - 1);
+      if (k == 1 && cfg.max_iter > 1) continue;  // cycle 2 is enqueued before cycle 1's count is read
+    }
+    pack(F.u[0], F.u[1], d_iters, d_parity, d_u, 0);
+    finish_report(rep, t0, H);
+  }
+
+  // Copy the per-shift report back; counts the smoother updates performed (sum over shifts of cycles).
+  void finish_report(pdmg_solve_report* rep, std::chrono::steady_clock::time_point t0, int H) {
+    to_host(d_iters, map_iters(), sizeof(int) * S);
+    to_host(d_conv, map_conv(), sizeof(int) * S);
+    const bool need_hist = rep && (rep->residual_history || rep->rate);
+    if (need_hist) to_host(d_hist, map_hist(), sizeof(double) * S * (size_t)H);
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    const int* it = (const int*)(h_map + map_iters());
+    const int* cv = (const int*)(h_map + map_conv());
+    const double* hist = (const double*)(h_map + map_hist());
+    drain_stats();
+    // updates per cycle per shift: (nu1+nu2) * sum_l m_l^2 * gamma^l over non-coarsest levels
+    double per_cycle = 0.0, visits = 1.0;
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+      per_cycle += (cfg.nu1 + cfg.nu2) * (double)lv[l].m * lv[l].m * visits;
+      if (cfg.cycle == PDMG_CYCLE_W) visits *= 2;
+    }
+    double cycles_done = 0.0;
+    for (int s = 0; s < S; ++s) cycles_done += it[s];
+    last_updates = per_cycle * cycles_done;
+    if (rep) {
+      for (int s = 0; s < S; ++s) {
+        if (rep->iterations) rep->iterations[s] = it[s];
+        if (rep->converged) rep->converged[s] = (uint8_t)cv[s];
+        if (rep->residual_history)
+          std::memcpy(rep->residual_history + (size_t)s * H, hist + (size_t)s * H, sizeof(double) * H);
+        if (rep->rate) rep->rate[s] = measured_rate(hist + (size_t)s * H, it[s]);
+      }
+      rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  }
+
+  static double measured_rate(const double* hist, int iters) {  // multigrid.cpp:9-21
+    if (iters <= 0) return 0.0;
+    int count = std::min(5, iters - 1);
+    if (count == 0) count = 1;
+    double log_sum = 0.0;
+    for (int k = iters - count + 1; k <= iters; ++k) {
+      if (hist[k] == 0.0) return 0.0;
+      if (hist[k - 1] == 0.0) return 0.0;
+      log_sum += std::log(hist[k] / hist[k - 1]);
+    }
+    return std::exp(log_sum / count);
+  }
+
+  // ---- host I/O staging --------------------------------------------------------------------
+  double2* stage(size_t elems) {
+    if (elems > stage_elems) {
+      cudaFree(d_stage);
+      d_stage = nullptr;
+      CK(cudaMalloc(&d_stage, elems * sizeof(double2)));
+      stage_elems = elems;
+    }
+    return d_stage;
+  }
+  size_t compact_elems(int l) const { return (size_t)S * lv[l].m * lv[l].m; }
+  void h2d(const pdmg_c128* src, double2* dst, size_t elems) {
+    CK(cudaMemcpyAsync(dst, src, elems * sizeof(double2), cudaMemcpyHostToDevice, stream));
+  }
+  void d2h(const double2* src, pdmg_c128* dst, size_t elems) {
+    CK(cudaMemcpyAsync(dst, src, elems * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+  }
+  void check_level(int l, int need_coarser) const {
+    if (l < 0 || l + need_coarser >= (int)lv.size())
+      throw ConfigError("level index " + std::to_string(l) + " out of range for a " + std::to_string(lv.size()) +
+                        "-level hierarchy");
+  }
+
+  // ---- shift sub-range view: the engine's per-shift arrays offset to shifts [s0, s0 + cnt) ---------------
+  int s_base = 0;  // offset of the current view into coarse_singular
+  struct RangeView {
+    Engine& e;
+    int S0;
+    std::vector<std::array<V*, 3>> saved_lv;
+    std::vector<LevelCoef*> saved_coef;
+    std::vector<size_t> saved_elems;
+    double2* ainv;
+    int *act, *it, *cv, *ones;
+    double *r0, *hist;
+    RangeView(Engine& en, int s0, int cnt) : e(en), S0(en.S) {
+      for (auto& L : e.lv) {
+        saved_lv.push_back({L.u[0], L.u[1], L.b});
+        saved_coef.push_back(L.coef);
+        saved_elems.push_back(L.elems);
+        L.u[0] += s0 * L.ss, L.u[1] += s0 * L.ss, L.b += s0 * L.ss, L.coef += s0;
+        L.elems = (size_t)L.ss * cnt + (s0 + cnt == en.S ? L.n + 2 : 0);
+      }
+      ainv = e.d_ainv, act = e.d_active, it = e.d_iters, cv = e.d_conv, ones = e.d_ones, r0 = e.d_r0, hist = e.d_hist;
+      e.d_ainv += (int64_t)s0 * e.coarse_N * e.coarse_N;
+      e.d_active += s0, e.d_iters += s0, e.d_conv += s0, e.d_ones += s0, e.d_r0 += s0;
+      e.d_hist += (int64_t)s0 * (e.cfg.max_iter + 1);
+      e.S = cnt;
+      e.s_base = s0;
+    }
+    ~RangeView() {
+      for (size_t l = 0; l < e.lv.size(); ++l) {
+        e.lv[l].u[0] = saved_lv[l][0], e.lv[l].u[1] = saved_lv[l][1], e.lv[l].b = saved_lv[l][2];
+        e.lv[l].coef = saved_coef[l], e.lv[l].elems = saved_elems[l];
+      }
+      e.d_ainv = ainv, e.d_active = act, e.d_iters = it, e.d_conv = cv, e.d_ones = ones, e.d_r0 = r0, e.d_hist = hist;
+      e.S = S0;
+      e.s_base = 0;
+    }
+  };
+
+  cudaStream_t copy_stream = nullptr;
+  int io_chunks = 0;  // 0 = automatic
+  int io_mode = 1;    // 1: chunks solve concurrently on sub-engines (own streams, priorities); 0: one stream
+  int stream_priority = 0;
+  // sub-engine of a concurrent host solve: its level arrays are the shift range [borrow_s0, borrow_s0 + S)
+  // of the parent engine's (a contiguous block of the shift-major storage), not allocations of its own
+  Engine* borrow = nullptr;
+  int borrow_s0 = 0;
+  // Sub-engines of the concurrent host-buffer pipeline: shifts [sub_lo[c], sub_lo[c+1]) on their own stream,
+  // chunk c at stream priority greatest + c, so chunks finish in order while later chunks fill the SMs the
+  // earlier ones leave idle (coarse levels, convergence bookkeeping, tails of the large passes).
+  std::vector<std::unique_ptr<Engine<T>>> subs;
+  std::vector<int> sub_lo;
+  pdmg_batch_desc desc_{};
+  bool build_subs(const std::vector<int>& lo) {
+    if (subs.size() + 1 == lo.size() && sub_lo == lo) {
+      for (auto& e : subs) e->solve_path = solve_path, e->profiling = profiling;
+      return true;
+    }
+    subs.clear();
+    sub_lo.clear();
+    // memory: each sub-engine works in its shift range of this engine's level arrays (borrow); it only
+    // allocates its coefficient tables, coarse factors and bookkeeping
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    for (size_t c = 0; c + 1 < lo.size(); ++c) {
+      auto e = std::make_unique<Engine<T>>();
+      pdmg_batch_desc d = desc_;
+      std::vector<pdmg_c128> lam(lo[c + 1] - lo[c]);
+      for (int s = lo[c]; s < lo[c + 1]; ++s) lam[s - lo[c]] = pdmg_c128{lambdas[s].real(), lambdas[s].imag()};
+      d.n_shifts = lo[c + 1] - lo[c];
+      d.lambdas = lam.data();
+      e->device = -1;
+      e->setup_host(d);
+      e->stream_priority = std::min(greatest + (int)c, least);
+      e->borrow = this;
+      e->borrow_s0 = lo[c];
+      e->setup_device(device);
+      e->io_chunks = 1;
+      e->solve_path = solve_path;
+      e->profiling = profiling;
+      subs.push_back(std::move(e));
+    }
+    sub_lo = lo;
+    return true;
+  }
+
+  // Host-buffer solve.  Large batches are pipelined over chunks of shifts: H2D of later chunks and D2H of
+  // earlier ones run on a copy stream while the current chunk solves (results are identical: every shift's
+  // solve is independent and its kernels see the same data).
+  void solve_host(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep) override {
+    CK(cudaSetDevice(device));
+    const size_t N = compact_elems(0);
+    const int64_t per = (int64_t)lv[0].m * lv[0].m;
+    double2* st = stage(2 * N);
+    // automatic: three chunks of S/4, S/2, S/4 shifts.  Each chunk solve carries a fixed ~3 ms of
+    // coarse-level latency (C3 on B200: t(S) ~ 2.9 ms + 0.148 ms * S), so few chunks with short end
+    // chunks minimise exposed copy + overhead: 62 ms (4 equal) -> ~55 ms for C3 (serial: 78 ms).
+    const bool auto_split = io_chunks <= 0;
+    int nch = io_chunks > 0 ? io_chunks : (N * sizeof(double2) >= ((size_t)256 << 20) && S >= 8 ? 3 : 1);
+    nch = std::max(1, std::min(nch, S));
+    auto pinned = [](const void* p) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) return (cudaGetLastError(), false);
+      return a.type == cudaMemoryTypeHost;
+    };
+    if (nch > 1 && !(pinned(b) && pinned(u))) nch = 1;  // pageable copies are host-synchronous: no overlap
+    if (nch == 1) {
+      h2d(b, st, N);
+      solve_device(st, st + N, rep);
+      d2h(st + N, u, N);
+      CK(cudaStreamSynchronize(stream));
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    if (io_mode == 1 && solve_concurrent(b, u, rep, st, N, per)) {
+      if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return;
+    }
+    std::vector<cudaEvent_t> in(nch), done(nch);
+    for (int c = 0; c < nch; ++c) {
+      CK(cudaEventCreateWithFlags(&in[c], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming));
+    }
+    auto bound = [&](int c) {
+      if (auto_split && nch == 3) return c == 0 ? 0 : c == 1 ? S / 4 : c == 2 ? S - S / 4 : S;
+      return (int)((int64_t)S * c / nch);
+    };
+    auto range = [&](int c) { return std::make_pair(bound(c), bound(c + 1)); };
+    for (int c = 0; c < nch; ++c) {
+      const auto [s0, s1] = range(c);
+      CK(cudaMemcpyAsync(st + s0 * per, b + s0 * per, sizeof(double2) * per * (s1 - s0), cudaMemcpyHostToDevice,
+                         copy_stream));
+      CK(cudaEventRecord(in[c], copy_stream));
+    }
+    const int H = cfg.max_iter + 1;
+    double upd = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      const auto [s0, s1] = range(c);
+      CK(cudaStreamWaitEvent(stream, in[c], 0));
+      pdmg_solve_report rc{};
+      if (rep) {
+        rc.iterations = rep->iterations ? rep->iterations + s0 : nullptr;
+        rc.converged = rep->converged ? rep->converged + s0 : nullptr;
+        rc.residual_history = rep->residual_history ? rep->residual_history + (int64_t)s0 * H : nullptr;
+        rc.rate = rep->rate ? rep->rate + s0 : nullptr;
+      }
+      {
+        RangeView view(*this, s0, s1 - s0);
+        solve_device(st + s0 * per, st + N + s0 * per, rep ? &rc : nullptr);
+      }
+      upd += last_updates;
+      CK(cudaEventRecord(done[c], stream));
+      CK(cudaStreamWaitEvent(copy_stream, done[c], 0));
+      CK(cudaMemcpyAsync(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * (s1 - s0), cudaMemcpyDeviceToHost,
+                         copy_stream));
+    }
+    CK(cudaStreamSynchronize(copy_stream));
+    for (int c = 0; c < nch; ++c) cudaEventDestroy(in[c]), cudaEventDestroy(done[c]);
+    last_updates = upd;
+    if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  // Concurrent host pipeline: all H2D copies queue on the copy stream in chunk order; chunk c's host thread
+  // waits for its copy, solves on its sub-engine's stream and queues its own D2H there.  Every shift's solve
+  // is independent, so the results are bitwise those of one batch (test_chunked_host_solve_matches).
+  bool solve_concurrent(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep, double2* st, size_t N, int64_t per) {
+    // automatic: six chunks weighted 1,2,2,2,2,1 -- half-size first and last chunks shorten the exposed fill
+    // (first H2D) and drain (last D2H); measured on B200 (C3): 45.9 ms vs 47.4 (1,2,2,2,1), 48.1 (8 equal),
+    // 49.4 (1,3,3,1) and 51.4 for the one-stream three-chunk pipeline (io_mode 0)
+    int nch = io_chunks > 0 ? io_chunks : 6;
+    nch = std::max(2, std::min(nch, S));
+    std::vector<int> lo(nch + 1);
+    if (io_chunks <= 0 && nch == 6) {
+      static const int wt[6] = {1, 2, 2, 2, 2, 1};
+      int acc = 0;
+      for (int c = 0; c < 6; ++c) acc += wt[c], lo[c + 1] = (int)((int64_t)S * acc / 10);
+    } else {
+      for (int c = 0; c <= nch; ++c) lo[c] = (int)((int64_t)S * c / nch);
+    }
+    if (const char* e = std::getenv("PDMG_IO_LAYOUT")) {  // chunk sizes in parts, e.g. "1,2,2,2,1" (tuning)
+      std::vector<double> w;
+      for (const char* q = e; *q;) {
+        char* end = nullptr;
+        w.push_back(std::strtod(q, &end));
+        q = (*end == ',') ? end + 1 : end;
+        if (end == q && *q) break;
+      }
+      double tw = 0;
+      for (double x : w) tw += x;
+      lo.assign(w.size() + 1, 0);
+      double acc = 0;
+      for (size_t c = 0; c < w.size(); ++c) acc += w[c], lo[c + 1] = (int)std::lround(S * acc / tw);
+      lo.back() = S;
+      nch = (int)w.size();
+    }
+    for (int c = 0; c < nch; ++c)
+      if (lo[c + 1] <= lo[c]) return false;
+    if (!build_subs(lo)) return false;
+    std::vector<cudaEvent_t> in(nch);
+    static const bool dbg = std::getenv("PDMG_IO_DEBUG") != nullptr;
+    auto tevent = [&](cudaStream_t st_) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, st_));
+      return e;
+    };
+    std::vector<cudaEvent_t> t_in(nch), t_sol(nch), t_out(nch);
+    cudaEvent_t t_start = dbg ? tevent(copy_stream) : nullptr;
+    for (int c = 0; c < nch; ++c) {
+      CK(cudaEventCreateWithFlags(&in[c], dbg ? 0 : cudaEventDisableTiming));
+      CK(cudaMemcpyAsync(st + lo[c] * per, b + lo[c] * per, sizeof(double2) * per * (lo[c + 1] - lo[c]),
+                         cudaMemcpyHostToDevice, copy_stream));
+      CK(cudaEventRecord(in[c], copy_stream));
+    }
+    const int H = cfg.max_iter + 1;
+    std::vector<std::exception_ptr> err(nch);
+    std::vector<std::thread> th;
+    for (int c = 0; c < nch; ++c) {
+      th.emplace_back([&, c] {
+        try {
+          Engine<T>& e = *subs[c];
+          CK(cudaSetDevice(device));
+          const int s0 = lo[c], cnt = lo[c + 1] - lo[c];
+          CK(cudaStreamWaitEvent(e.stream, in[c], 0));
+          pdmg_solve_report rc{};
+          if (rep) {
+            rc.iterations = rep->iterations ? rep->iterations + s0 : nullptr;
+            rc.converged = rep->converged ? rep->converged + s0 : nullptr;
+            rc.residual_history = rep->residual_history ? rep->residual_history + (int64_t)s0 * H : nullptr;
+            rc.rate = rep->rate ? rep->rate + s0 : nullptr;
+          }
+          e.solve_device(st + s0 * per, st + N + s0 * per, rep ? &rc : nullptr);
+          if (dbg) t_sol[c] = tevent(e.stream);
+          CK(cudaMemcpyAsync(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * cnt, cudaMemcpyDeviceToHost,
+                             e.stream));
+          if (dbg) t_out[c] = tevent(e.stream);
+          CK(cudaStreamSynchronize(e.stream));
+        } catch (...) {
+          err[c] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    if (dbg) {
+      for (int c = 0; c < nch; ++c) {
+        float a = 0, b2 = 0, c2 = 0;
+        cudaEventElapsedTime(&a, t_start, in[c]);
+        if (t_sol[c]) cudaEventElapsedTime(&b2, t_start, t_sol[c]);
+        if (t_out[c]) cudaEventElapsedTime(&c2, t_start, t_out[c]);
+        std::fprintf(stderr, "pdmg io chunk %d [%d,%d): in %.2f solved %.2f out %.2f ms\n", c, lo[c], lo[c + 1], a, b2, c2);
+        if (t_sol[c]) cudaEventDestroy(t_sol[c]);
+        if (t_out[c]) cudaEventDestroy(t_out[c]);
+      }
+      cudaEventDestroy(t_start);
+    }
+    for (int c = 0; c < nch; ++c) cudaEventDestroy(in[c]);
+    for (auto& x : err)
+      if (x) std::rethrow_exception(x);
+    double upd = 0.0;
+    for (auto& e : subs) {
+      upd += e->last_updates, launches += e->launches, e->launches = 0;
+      for (auto& kv : e->stats) {  // (each sub-engine drained its own events at the end of its solve)
+        Stat& st = stats[kv.first];
+        st.launches += kv.second.launches, st.ms += kv.second.ms, st.bytes += kv.second.bytes;
+        st.ubytes += kv.second.ubytes, st.updates += kv.second.updates;
+      }
+      e->stats.clear();
+    }
+    last_updates = upd;
+    return true;
+  }
+
+  void cycle_host(pdmg_c128* u, const pdmg_c128* b) override {
+    CK(cudaSetDevice(device));
+    if (any_singular)
+      throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
+    Level& F = lv[0];
+    const size_t N = compact_elems(0);
+    double2* st = stage(2 * N);
+    h2d(b, st, N);
+    h2d(u, st + N, N);
+    unpack(st, F.b, 0);
+    F.cur = 0;
+    unpack(st + N, F.u[0], 0);
+    cycle_level(0, false, nullptr, S, false);
+    pack(F.u[F.cur], F.u[F.cur], nullptr, nullptr, st + N, 0);
+    d2h(st + N, u, N);
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    drain_stats();
+  }
+
+  // level operators ----------------------------------------------------------------------------
+  void op_smooth(int l, const pdmg_c128* u, const pdmg_c128* b, pdmg_c128* out) override {
+    check_level(l, 1);
+    CK(cudaSetDevice(device));
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    double2* st = stage(2 * N);
+    h2d(u, st, N);
+    h2d(b, st + N, N);
+    unpack(st, Lv.u[0], l);
+    unpack(st + N, Lv.b, l);
+    level_pass(l, Variant{true, false, true, POST_NONE, true, cfg.smoother == PDMG_SMOOTHER_JACOBI}, Lv.u[0], Lv.u[1],
+               Lv.b, nullptr, nullptr, nullptr, S);
+    pack(Lv.u[1], Lv.u[1], nullptr, nullptr, st, l);
+    d2h(st, out, N);
+    finish();
+  }
+  void op_residual(int l, const pdmg_c128* b, const pdmg_c128* u, pdmg_c128* r) override {
+    check_level(l, 0);
+    CK(cudaSetDevice(device));
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    double2* st = stage(2 * N);
+    h2d(u, st, N);
+    h2d(b, st + N, N);
+    unpack(st, Lv.u[0], l);
+    unpack(st + N, Lv.b, l);
+    level_pass(l, Variant{true, false, false, POST_RESID, false, false}, Lv.u[0], Lv.u[1], Lv.b, nullptr, nullptr,
+               nullptr, S);
+    pack(Lv.u[1], Lv.u[1], nullptr, nullptr, st, l);
+    d2h(st, r, N);
+    finish();
+  }
+  void op_restrict(int l, const pdmg_c128* fine, pdmg_c128* coarse) override {
+    check_level(l, 1);
+    CK(cudaSetDevice(device));
+    Level &Lv = lv[l], &Lc = lv[l + 1];
+    const size_t N = compact_elems(l), Nc = compact_elems(l + 1);
+    double2* st = stage(N + Nc);
+    h2d(fine, st, N);
+    unpack(st, Lv.b, l);
+    level_pass(l, Variant{false, false, false, POST_RESTRICT, false, false}, nullptr, nullptr, Lv.b, nullptr, Lc.b,
+               nullptr, S);
+    pack(Lc.b, Lc.b, nullptr, nullptr, st + N, l + 1);
+    d2h(st + N, coarse, Nc);
+    finish();
+  }
+  void op_prolong(int l, const pdmg_c128* coarse, pdmg_c128* fine) override {
+    check_level(l, 1);
+    CK(cudaSetDevice(device));
+    Level &Lv = lv[l], &Lc = lv[l + 1];
+    const size_t N = compact_elems(l), Nc = compact_elems(l + 1);
+    double2* st = stage(N + Nc);
+    h2d(coarse, st + N, Nc);
+    unpack(st + N, Lc.u[0], l + 1);
+    level_pass(l, Variant{false, true, false, POST_NONE, true, false}, nullptr, Lv.u[1], Lv.b, Lc.u[0], nullptr,
+               nullptr, S);
+    pack(Lv.u[1], Lv.u[1], nullptr, nullptr, st, l);
+    d2h(st, fine, N);
+    finish();
+  }
+  void op_norm(int l, const pdmg_c128* v, double* norms) override {
+    check_level(l, 0);
+    CK(cudaSetDevice(device));
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    double2* st = stage(N);
+    h2d(v, st, N);
+    unpack(st, Lv.b, l);
+    level_pass(l, Variant{false, false, false, POST_NORM, false, false}, nullptr, nullptr, Lv.b, nullptr, nullptr,
+               nullptr, S);
+    const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
+    timed("sum_partials", 0.0,
+          [&] { k_sum_partials<<<blocks, threads, 0, stream>>>(d_partial, last_partials, S, d_norms); });
+    CK(cudaMemcpyAsync(norms, d_norms, sizeof(double) * S, cudaMemcpyDeviceToHost, stream));
+    finish();
+  }
+  void op_coarse_solve(const pdmg_c128* b, pdmg_c128* u) override {
+    CK(cudaSetDevice(device));
+    if (any_singular)
+      throw SingularOperatorError("DenseShiftedSolver: operator is singular on grid n = " + std::to_string(lv.back().n));
+    const int l = (int)lv.size() - 1;
+    Level& Lv = lv[l];
+    const size_t N = compact_elems(l);
+    double2* st = stage(2 * N);
+    h2d(b, st, N);
+    unpack(st, Lv.b, l);
+    coarse_solve(Lv.b, Lv.u[0], nullptr);
+    pack(Lv.u[0], Lv.u[0], nullptr, nullptr, st + N, l);
+    d2h(st + N, u, N);
+    finish();
+  }
+  void finish() {
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    drain_stats();
+  }
+};
+
+
+}  // namespace pdmg_b200

@@ -670,7 +670,7 @@ struct SolveState {
   unsigned long long* pred;
 };
 
-__global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k, SolveState st) {
+static __global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k, SolveState st) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0 && st.parity) st.parity[k] = st.cur;
   if (warp >= st.S) return;
@@ -711,7 +711,7 @@ __global__ void k_finalize(const double* __restrict__ partial, int ntiles, int k
 
 // Device -> mapped pinned host words, written by SMs over PCIe: small result copies that never queue
 // behind bulk transfers on the copy engines (the chunked host solve keeps those busy).
-__global__ void k_copy_words(const uint32_t* __restrict__ src, volatile uint32_t* dst, int64_t n) {
+static __global__ void k_copy_words(const uint32_t* __restrict__ src, volatile uint32_t* dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(RN_THREADS) k_resid_norm(const typename vec2<T
 }
 
 // Per-shift norms (op-level pdmg_norm): sum partials -> sqrt.
-__global__ void k_sum_partials(const double* __restrict__ partial, int ntiles, int S, double* out) {
+static __global__ void k_sum_partials(const double* __restrict__ partial, int ntiles, int S, double* out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= S) return;
   double acc = 0.0;
@@ -800,11 +800,10 @@ __global__ void k_unpack(const double2* __restrict__ src, typename vec2<T>::type
   }
 }
 
-// Gather u out of the buffer each shift finished in (level 0 has two, three with the V(1,1) cross-cycle
-// fusion): sel = parity[iterations[s]].
+// Gather u out of the buffer each shift finished in: sel = parity[iterations[s]].
 template <class T>
 __global__ void k_pack(const typename vec2<T>::type* __restrict__ buf0, const typename vec2<T>::type* __restrict__ buf1,
-                       const typename vec2<T>::type* __restrict__ buf2, const int* __restrict__ iters,
+                       const int* __restrict__ iters,
                        const int* __restrict__ parity, double2* __restrict__ dst, int n, int64_t ss, int64_t total) {
   const int m = n - 1;
   const int64_t N = (int64_t)m * m;
@@ -812,132 +811,13 @@ __global__ void k_pack(const typename vec2<T>::type* __restrict__ buf0, const ty
     const int64_t s = q / N, p = q % N;
     const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
     const int sel = (iters == nullptr) ? 0 : parity[iters[s]];
-    const typename vec2<T>::type* src = sel == 0 ? buf0 : sel == 1 ? buf1 : buf2;
+    const typename vec2<T>::type* src = sel == 0 ? buf0 : buf1;
     dst[q] = ld2(src[s * ss + (int64_t)j * n + i]);
   }
 }
 
 }  // namespace pdmg_b200
 
-// ===================================================================================================
-// ParaDIAG time direction (alpha-circulant backward Euler; restated, see DESIGN.md section 1 row P3).
-//   step 1:  g_k = (1/nt) sum_t alpha^(t/nt) f_t e^{+2 pi i t k / nt}      (dir = +1, pre-scale, 1/nt)
-//   step 3:  u_t = alpha^(-t/nt) sum_k w_k e^{-2 pi i t k / nt}           (dir = -1, post-scale)
-// Layout: [nt][npts] compact (time slices of the reference layout).  A CTA transforms DFT_P spatial
-// points: loads rows t (DFT_P contiguous complex each), runs an in-place radix-2 DIT FFT in shared
-// memory when nt is a power of two (direct O(nt^2) DFT otherwise), writes rows k.
-// ===================================================================================================
-namespace pdmg_b200 {
-
-constexpr int DFT_THREADS = 256;
-
-// tw[q] = e^{dir 2 pi i q / nt}; pre[t] multiplies the input, post[k] the output (complex fp64 host tables:
-// alpha^(t/nt) is complex for the QBV scheme's alpha < 0).
-__global__ void k_time_dft(const double2* __restrict__ in, double2* __restrict__ out, int nt, int log2nt, int npts,
-                           int P, const double2* __restrict__ tw, const double2* __restrict__ pre,
-                           const double2* __restrict__ post) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* buf = reinterpret_cast<double2*>(smem_raw);  // [nt][P]
-  const int p0 = blockIdx.x * P;
-  const int np = min(P, npts - p0);
-  const int tid = threadIdx.x;
-  // load (bit-reversed time order for the radix-2 path), with the pre-scaling
-  for (int q = tid; q < nt * P; q += blockDim.x) {
-    const int t = q / P, pl = q - t * P;
-    double2 v = make_double2(0.0, 0.0);
-    if (pl < np) v = cmul(pre[t], in[(int64_t)t * npts + p0 + pl]);
-    const int dst = log2nt >= 0 ? (int)(__brev((unsigned)t) >> (32 - log2nt)) : t;
-    buf[dst * P + pl] = v;
-  }
-  __syncthreads();
-  if (log2nt >= 0) {
-    for (int len = 2; len <= nt; len <<= 1) {
-      const int half = len >> 1, tstep = nt / len;
-      for (int q = tid; q < (nt >> 1) * P; q += blockDim.x) {
-        const int bf = q / P, pl = q - bf * P;
-        const int grp = bf / half, j = bf - grp * half;
-        const int i0 = grp * len + j, i1 = i0 + half;
-        const double2 w = tw[j * tstep];
-        const double2 a = buf[i0 * P + pl], b = buf[i1 * P + pl];
-        const double2 wb = make_double2(w.x * b.x - w.y * b.y, w.x * b.y + w.y * b.x);
-        buf[i0 * P + pl] = make_double2(a.x + wb.x, a.y + wb.y);
-        buf[i1 * P + pl] = make_double2(a.x - wb.x, a.y - wb.y);
-      }
-      __syncthreads();
-    }
-    for (int q = tid; q < nt * P; q += blockDim.x) {
-      const int k = q / P, pl = q - k * P;
-      if (pl < np) out[(int64_t)k * npts + p0 + pl] = cmul(post[k], buf[k * P + pl]);
-    }
-  } else {
-    for (int q = tid; q < nt * P; q += blockDim.x) {
-      const int k = q / P, pl = q - k * P;
-      if (pl >= np) continue;
-      double2 acc = make_double2(0.0, 0.0);
-      int idx = 0;  // (t * k) mod nt
-      for (int t = 0; t < nt; ++t) {
-        const double2 w = tw[idx], v = buf[t * P + pl];
-        acc.x += w.x * v.x - w.y * v.y;
-        acc.y += w.x * v.y + w.y * v.x;
-        idx += k;
-        if (idx >= nt) idx -= nt;
-      }
-      out[(int64_t)k * npts + p0 + pl] = cmul(post[k], acc);
-    }
-  }
-}
-
-// All-at-once residual r_t = f_t - ((C_alpha (x) I + I (x) A) u)_t over the local time slices
-// [t0, t0+ntl) of a global nt (paradiag.cpp:141-183 with B = C_alpha): C_alpha row t couples u_t and
-// u_{t-1} (-1/dt, 1/dt), row 0 couples u_0 and alpha u_{nt-1}.  u_prev is the slice before t0 (u_{nt-1}
-// when t0 == 0).  Per-block partial sums of |r|^2 and |f|^2 (fixed-order, deterministic).
-__global__ void k_aao_residual(const double2* __restrict__ u, const double2* __restrict__ u_prev,
-                               const double2* __restrict__ f, int n, int ntl, int t0, double alpha, double dt,
-                               double* __restrict__ partial) {
-  const int m = n - 1, npts = m * m;
-  const double h = 1.0 / n, inv_h2 = 1.0 / (h * h), idt = 1.0 / dt;
-  double rr = 0.0, ff = 0.0;
-  const int64_t total = (int64_t)ntl * npts;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int tl = (int)(q / npts), p = (int)(q - (int64_t)tl * npts);
-    const int j = p / m, i = p - j * m;  // 0-based interior coords
-    const double2* ut = u + (int64_t)tl * npts;
-    const double2 c = ut[p];
-    double ax = 4.0 * c.x, ay = 4.0 * c.y;  // A u (unshifted 5-point, grid.cpp:69-90)
-    if (i > 0) ax -= ut[p - 1].x, ay -= ut[p - 1].y;
-    if (i < m - 1) ax -= ut[p + 1].x, ay -= ut[p + 1].y;
-    if (j > 0) ax -= ut[p - m].x, ay -= ut[p - m].y;
-    if (j < m - 1) ax -= ut[p + m].x, ay -= ut[p + m].y;
-    ax *= inv_h2, ay *= inv_h2;
-    const double2 pv = tl > 0 ? u[(int64_t)(tl - 1) * npts + p] : u_prev[p];
-    const double wp = (t0 + tl == 0) ? -alpha * idt : -idt;
-    ax += idt * c.x + wp * pv.x;
-    ay += idt * c.y + wp * pv.y;
-    const double2 fv = f[(int64_t)tl * npts + p];
-    const double rx = fv.x - ax, ry = fv.y - ay;
-    rr += rx * rx + ry * ry;
-    ff += fv.x * fv.x + fv.y * fv.y;
-  }
-  __shared__ double red[2][32];
-  for (int o = 16; o > 0; o >>= 1) {
-    rr += __shfl_xor_sync(0xffffffffu, rr, o);
-    ff += __shfl_xor_sync(0xffffffffu, ff, o);
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[0][w] = rr, red[1][w] = ff;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    double a = l < nw ? red[0][l] : 0.0, b = l < nw ? red[1][l] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
-    if (l == 0) partial[2 * blockIdx.x] = a, partial[2 * blockIdx.x + 1] = b;
-  }
-}
-
-}  // namespace pdmg_b200
 
 // ===================================================================================================
 // Small-grid path: one CTA runs the WHOLE solve of one shift (multigrid.cpp:85-110 loop, V or W cycles,
@@ -1246,7 +1126,6 @@ struct MarchArgs {
   const V* b;
   const V* ec;
   V* bc;
-  V* u_mid;  // k_march2<MID>: the first sweep's iterate (the previous cycle's final iterate) is stored here
   double* partial;
   const LevelCoef* coef;
   const int* active;
@@ -1531,22 +1410,16 @@ struct IC {
 #define PDMG_MARCH2_MINB 2
 #endif
 // (measured and removed, DESIGN 3.2b: input rows through a TMA ring in shared memory, L2 bulk prefetch,
-// register prefetch two rows ahead -- all slower than the one-row register prefetch)
-template <class T>
-constexpr size_t march2_smem(bool) {
-  return 0;
-}
+// register prefetch two rows ahead, warp-specialised sweep pairs, V(1,1) cross-cycle fusion -- all slower
+// than or as fast as this one-row register prefetch)
 // NORM_IN: also leave the partial sums of ||b - L u_in||^2 (the first sweep's residual, i.e. the residual of
 // the previous cycle's iterate) in a.partial -- the fine-level convergence norm, read one pass later.
-// MID (V(1,1) cross-cycle fusion): the pass is cycle k's prolongate-and-correct + post-sweep followed by
-// cycle k+1's pre-sweep + restriction; the first sweep's iterate u1 (= cycle k's result) is also stored to
-// a.u_mid and the partials hold ||b - L u1||^2 (the second sweep's residual), i.e. cycle k's residual norm.
 // TWO = false: ONE Vanka sweep per pass with the same machinery (the single-sweep passes of V(1,1) and odd
 // nu): u1 at row j-2 is the stored iterate and the post stage reads r2 = b - L u1 at row j-3.
 #ifndef PDMG_MARCH1_MINB
 #define PDMG_MARCH1_MINB 3
 #endif
-template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool MID = false, bool TWO = true>
+template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool TWO = true>
 __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB)
     k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
@@ -1554,35 +1427,19 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   constexpr int LC = 2;
   constexpr bool EVEN = sizeof(V) == 8;
   constexpr bool HASD = POST != POST_NONE;
-  static_assert(TWO || !MID, "the cross-cycle pass is a two-sweep pass");
+  static_assert(!(PROLONG && POST == POST_RESTRICT), "prolongation and restriction never share a pass");
   constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
   constexpr int hC = HASD ? hD + 1 : 0;
   // 2 halo columns/rows per sweep (residual + Vanka patch) + the post stage, rounded up to even (strips
   // start at even columns)
   constexpr int hA = (hC + (TWO ? 4 : 2) + 1) & ~1;
   constexpr int WOUT = 32 * LC - 2 * hA;
-  // the largest variant (prolongation + restriction + mid store) loads b rows j-3 / j-5 inside the step
-  // instead of holding them in prefetch registers (otherwise it spills)
-#ifndef PDMG_M2_BINSTEP
-#define PDMG_M2_BINSTEP 0
-#endif
-  constexpr bool B_INSTEP = MID || (PDMG_M2_BINSTEP && TWO);
   // L2 prefetch distance in rows (0 = none).  Measured at C3 (DESIGN 3.2b): 2 rows ahead speeds up every
-  // marching pass (the prolongating pairs only since their coarse values are loaded directly, PRO_DIRECT)
+  // marching pass
 #ifndef PDMG_M2_PF
 #define PDMG_M2_PF 2
 #endif
   constexpr int M2_PF = PDMG_M2_PF;
-  // NO_EX: lane 31 skips the coarse column beyond its strip, so the prolongation at the strip's last
-  // column (cA + 63, odd) is wrong.  With the restriction's halo (hA = 6) that error reaches u1/u2 at
-  // columns >= cA + 59 and r2 at >= cA + 58 only, outside the stored columns (<= cA + 57) and the stored
-  // coarse points (fine column <= cA + 56): the results are unchanged and 12 registers are saved.
-  constexpr bool NO_EX = PROLONG && POST == POST_RESTRICT;
-#ifndef PDMG_M2_PRO_DIRECT
-#define PDMG_M2_PRO_DIRECT 1
-#endif
-  constexpr bool PRO_DIRECT = PDMG_M2_PRO_DIRECT && !MID;
-  static_assert(!NO_EX || hA >= 6, "NO_EX needs the restriction halo");
   const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
   const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
@@ -1594,7 +1451,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   const int64_t sbase = (int64_t)shift * a.ss;
   const int cA = x0 - hA + LC * lane;
   V* __restrict__ uout = a.u_out + sbase + cA;  // per-lane column pointer (row 0)
-  V* __restrict__ umid = MID ? a.u_mid + sbase + cA : nullptr;
   const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
   const LevelCoef cf = coef_of(cp);
 
@@ -1619,28 +1475,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   // (one sweep: the b rows read are j-1 and j-3 only)
   constexpr bool NEED_B3 = TWO || HASD, NEED_B5 = TWO && HASD;
 
-  // prolongation window: coarse rows J, J+1 (in use) and J+2 (prefetched) at this lane's coarse column Ie;
-  // the column Ie+1 comes from the next lane (lane 31 loads it itself)
-  D2 Eo0 = cz<D2>(), Eo1 = cz<D2>(), Eo2 = cz<D2>(), Ex0 = cz<D2>(), Ex1 = cz<D2>(), Ex2 = cz<D2>();
-  int wJ = -1000;
   const int Ie = cA >> 1;
   const bool codd = (cA & 1) != 0;  // warp-uniform (strips start at x0 - hA, lanes step by 2)
-  auto load_crow = [&](int J, D2& o, D2& x, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
-#ifdef PDMG_DBG_NOPROLOAD
-    o = make_double2((double)J, (double)Ie);
-    x = o;
-#else
-    const bool jok = (unsigned)J <= (unsigned)nc;
-    if constexpr (MASK)
-      o = (jok && (unsigned)Ie <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie]) : cz<D2>();
-    else
-      o = ld2(ecs[(int64_t)J * nc + Ie]);
-    if (!NO_EX && lane == 31) x = (jok && (unsigned)(Ie + 1) <= (unsigned)nc) ? ld2(ecs[(int64_t)J * nc + Ie + 1]) : cz<D2>();
-#endif
-  };
-  // u_in row `row`, and the prolongation of e_c onto fine row `row` (register window E0/E1, rows visited
-  // in increasing order; computed a step ahead so the coarse loads are not waited on)
   auto gread_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value;
 #pragma unroll
@@ -1680,27 +1516,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
 #pragma unroll
     for (int k = 0; k < LC; ++k) pout[k] = MASK ? csel(rin && cin[k], p[k]) : p[k];
   };
-  auto prolong_row = [&](int row, D2* pout, auto MK) __attribute__((always_inline)) {
-    const int J = row >> 1;
-    if (J == wJ + 1) {
-      Eo0 = Eo1, Eo1 = Eo2, Ex0 = Ex1, Ex1 = Ex2;
-      load_crow(J + 2, Eo2, Ex2, MK);
-      wJ = J;
-    } else if (J != wJ) {
-      load_crow(J, Eo0, Ex0, IC<1>{});
-      load_crow(J + 1, Eo1, Ex1, IC<1>{});
-      load_crow(J + 2, Eo2, Ex2, IC<1>{});
-      wJ = J;
-    }
-    const D2 a0 = Eo0, b0 = Eo1;
-    D2 a1 = shfl_dn2(Eo0), b1 = shfl_dn2(Eo1);
-    if (!NO_EX && lane == 31) a1 = Ex0, b1 = Ex1;
-    prolong_of(row, a0, a1, b0, b1, pout, MK);
-  };
-  // PRO_DIRECT: the four coarse values of fine row `row` -- e(J, Ie), e(J, Ie+1), e(J+1, Ie), e(J+1, Ie+1),
-  // J = row >> 1 -- are loaded unconditionally (indices clamped into the array; out-of-domain points are
-  // masked when the prolongation is formed) one step before the row is consumed: no window rotation, no
-  // branch around the loads, so no register copy waits on a load that was just issued
+  // the four coarse values of fine row `row` -- e(J, Ie), e(J, Ie+1), e(J+1, Ie), e(J+1, Ie+1), J = row >> 1 --
+  // are loaded unconditionally (indices clamped into the array; out-of-domain points are masked when the
+  // prolongation is formed) one step before the row is consumed: no window rotation, no branch around the
+  // loads, so no register copy waits on a load that was just issued (DESIGN 3.2b)
   D2 Cq[4];
   auto load_coarse = [&](int row, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value;
@@ -1708,9 +1527,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     if constexpr (MASK) J = min(max(J, 0), nc - 1), I = min(max(I, 0), nc - 1);
     const V* p0 = ecs + (int64_t)J * nc + I;
     Cq[0] = ld2(p0[0]), Cq[1] = ld2(p0[1]), Cq[2] = ld2(p0[nc]), Cq[3] = ld2(p0[nc + 1]);
-  };
-  auto prolong_direct = [&](int row, D2* pout, auto MK) __attribute__((always_inline)) {
-    prolong_of(row, Cq[0], Cq[1], Cq[2], Cq[3], pout, MK);
   };
   auto west = [&](const D2* x, int k, const D2& wl) __attribute__((always_inline)) { return k == 0 ? wl : x[k - 1]; };
   auto east = [&](const D2* x, int k, const D2& er) __attribute__((always_inline)) { return k == LC - 1 ? er : x[k + 1]; };
@@ -1744,7 +1560,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   D2 P1[LC], C1[LC], P2[LC], C2[LC], Vp[LC];
   // rows prefetched one step ahead (indexing these by window phase, so a step reads one slot and loads the
   // next, was measured to make ptxas keep three copies live and spill)
-  D2 Pn[LC], Unx[LC], Bn[LC], B3n[LC], B5n[LC];
+  D2 Unx[LC], Bn[LC], B3n[LC], B5n[LC];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -1754,14 +1570,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   double nacc = 0.0;
   gread_u(rlo, Unx, IC<1>{});
   gload_b(rlo - 1, Bn, IC<1>{});
-  if constexpr (!B_INSTEP) {
-    if constexpr (NEED_B3) gload_b(rlo - 3, B3n, IC<1>{});
-    if constexpr (NEED_B5) gload_b(rlo - 5, B5n, IC<1>{});
-  }
-  if constexpr (PROLONG) {
-    if constexpr (PRO_DIRECT) load_coarse(rlo, IC<1>{});
-    else prolong_row(rlo, Pn, IC<1>{});
-  }
+  if constexpr (NEED_B3) gload_b(rlo - 3, B3n, IC<1>{});
+  if constexpr (NEED_B5) gload_b(rlo - 5, B5n, IC<1>{});
+  if constexpr (PROLONG) load_coarse(rlo, IC<1>{});
 
   // one step at row j; window slot of (oldest, middle, newest) row = ((PH + 0, 1, 2) % 3)
   auto step = [&](int j, auto PH, auto MK) __attribute__((always_inline)) {
@@ -1771,23 +1582,16 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     D2 B3[LC], B5[LC], Bc[LC], Un[LC];
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
-      if constexpr (PRO_DIRECT) Un[k] = Unx[k];
-      else Un[k] = PROLONG ? cadd(Unx[k], Pn[k]) : Unx[k];
+      Un[k] = Unx[k];
       Bc[k] = Bn[k];
-      if constexpr (!B_INSTEP) {
-        if constexpr (NEED_B3) B3[k] = B3n[k];
-        if constexpr (NEED_B5) B5[k] = B5n[k];
-      }
+      if constexpr (NEED_B3) B3[k] = B3n[k];
+      if constexpr (NEED_B5) B5[k] = B5n[k];
     }
-    if constexpr (PROLONG && PRO_DIRECT) {  // u row j += P e_c (coarse values loaded last step)
+    if constexpr (PROLONG) {  // u row j += P e_c (coarse values loaded last step)
       D2 Pc[LC];
-      prolong_direct(j, Pc, MK);
+      prolong_of(j, Cq[0], Cq[1], Cq[2], Cq[3], Pc, MK);
 #pragma unroll
       for (int k = 0; k < LC; ++k) Un[k] = cadd(Un[k], Pc[k]);
-    }
-    if constexpr (B_INSTEP) {  // (L1 hits: b rows j-3 and j-5 were loaded 2 and 4 steps ago)
-      gload_b(j - 3, B3, MK);
-      if constexpr (HASD) gload_b(j - 5, B5, MK);
     }
     if (j + 1 < rhi) {
       if constexpr (M2_PF > 0) {  // L2 prefetch of the rows M2_PF steps ahead (one hint per lane)
@@ -1796,12 +1600,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
       }
       gread_u(j + 1, Unx, MK);
       gload_b(j, Bn, MK);
-      if constexpr (PROLONG && !PRO_DIRECT) prolong_row(j + 1, Pn, MK);
-      if constexpr (PROLONG && PRO_DIRECT) load_coarse(j + 1, MK);
-      if constexpr (!B_INSTEP) {
-        if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
-        if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
-      }
+      if constexpr (PROLONG) load_coarse(j + 1, MK);
+      if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
+      if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
     }
 #pragma unroll
     for (int k = 0; k < LC; ++k) U0[sn][k] = Un[k];
@@ -1817,15 +1618,12 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
         }
       }
       vanka_row(r, P1, C1, row_in(j - 2), dl, MK);
-      const bool rst1 = (MID || !TWO) && j - 2 >= olo && j - 2 < ohi;
+      const bool rst1 = !TWO && j - 2 >= olo && j - 2 < ohi;
 #pragma unroll
       for (int k = 0; k < LC; ++k) {
         D2 u1 = cadd(U0[so][k], dl[k]);
         if constexpr (EVEN) u1 = ld2(st2<V>(u1));  // the iterate the unfused sweep would have stored
         U1[sn][k] = u1;
-        if constexpr (MID) {
-          if (rst1 && cst[k]) umid[(int64_t)(j - 2) * n + k] = st2<V>(u1);
-        }
         if constexpr (!TWO) {
           if (rst1 && cst[k]) uout[(int64_t)(j - 2) * n + k] = st2<V>(u1);
         }
@@ -1835,13 +1633,6 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     if constexpr (TWO) {
       D2 r[LC], dl[LC];
       resid(U1[so], U1[sm], U1[sn], B3, row_in(j - 3), r, MK);
-      if constexpr (MID) {  // ||b - L u1||^2 over the owned rows/columns: the residual of cycle k's iterate
-        if (j - 3 >= olo && j - 3 < ohi) {
-#pragma unroll
-          for (int k = 0; k < LC; ++k)
-            if (cst[k]) nacc += r[k].x * r[k].x + r[k].y * r[k].y;
-        }
-      }
       const int row = j - 4;
       vanka_row(r, P2, C2, row_in(row), dl, MK);
       const bool rst = row >= olo && row < ohi;
@@ -1900,9 +1691,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   //  (a) every step unrolled by 3 over the window phases, each with a masked and an unmasked copy;
   //  (b) boundary steps one at a time in window phase 0 followed by a register rotation, interior steps
   //      unmasked and unrolled by 3 -- only unmasked copies in the hot loop (smaller code).
-  // (MID: shape (b) only -- one loop shape keeps it under 255 registers; prolongating passes with a
-  //  post stage: shape (a) only -- both shapes in one function spill)
-  if (!MID && (a.loop_a || (PROLONG && POST != POST_NONE))) {
+  // (prolongating passes with a post stage: shape (a) only -- both shapes in one function spill)
+  if (a.loop_a || (PROLONG && POST != POST_NONE)) {
     auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
       if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
       else step(j, PH, IC<1>{});
@@ -1945,58 +1735,9 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
       rotate();
     }
   }
-  if constexpr (POST == POST_NORM || NORM_IN || MID) {
+  if constexpr (POST == POST_NORM || NORM_IN) {
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
     if (lane == 0) a.partial[(int64_t)shift * a.ntasks + task] = nacc;
-  }
-}
-
-}  // namespace pdmg_b200
-
-// ===================================================================================================
-// General (dense) time matrix B for ParaDIAG (HeatBVM, paradiag.cpp:46-82): the time transforms are dense
-// complex GEMMs over the time index (cuBLAS ZGEMM, see pdmg_capi.cu); this kernel forms the all-at-once
-// residual r = f - Y - (I (x) A) u with Y = (B (x) I) u precomputed, and its per-block partial norms.
-// ===================================================================================================
-namespace pdmg_b200 {
-
-__global__ void k_aao_residual_dense(const double2* __restrict__ u, const double2* __restrict__ y,
-                                     const double2* __restrict__ f, int n, int nt, double* __restrict__ partial) {
-  const int m = n - 1, npts = m * m;
-  const double h = 1.0 / n, inv_h2 = 1.0 / (h * h);
-  double rr = 0.0, ff = 0.0;
-  const int64_t total = (int64_t)nt * npts;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(q / npts), p = (int)(q - (int64_t)t * npts);
-    const int j = p / m, i = p - j * m;
-    const double2* ut = u + (int64_t)t * npts;
-    const double2 c = ut[p];
-    double ax = 4.0 * c.x, ay = 4.0 * c.y;  // A u (unshifted 5-point, grid.cpp:69-90)
-    if (i > 0) ax -= ut[p - 1].x, ay -= ut[p - 1].y;
-    if (i < m - 1) ax -= ut[p + 1].x, ay -= ut[p + 1].y;
-    if (j > 0) ax -= ut[p - m].x, ay -= ut[p - m].y;
-    if (j < m - 1) ax -= ut[p + m].x, ay -= ut[p + m].y;
-    const double2 yv = y[q], fv = f[q];
-    const double rx = fv.x - (inv_h2 * ax + yv.x), ry = fv.y - (inv_h2 * ay + yv.y);
-    rr += rx * rx + ry * ry;
-    ff += fv.x * fv.x + fv.y * fv.y;
-  }
-  __shared__ double red[2][32];
-  for (int o = 16; o > 0; o >>= 1) {
-    rr += __shfl_xor_sync(0xffffffffu, rr, o);
-    ff += __shfl_xor_sync(0xffffffffu, ff, o);
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[0][w] = rr, red[1][w] = ff;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    double a = l < nw ? red[0][l] : 0.0, b = l < nw ? red[1][l] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
-    if (l == 0) partial[2 * blockIdx.x] = a, partial[2 * blockIdx.x + 1] = b;
   }
 }
 

@@ -175,9 +175,10 @@ class BatchedMultigridHierarchy:
     """
 
     def __init__(self, fine: Grid2D, shifts: Sequence[Shift | complex], cfg: MultigridConfig, device: int = 0,
-                 precision: str = "c128"):
+                 precision: str = "c128", devices: Sequence[int] | None = None):
         """precision: "c128" (the reference's std::complex<double>) or "c64" (fp32 storage, fp64 arithmetic;
-        host arrays stay complex128)."""
+        host arrays stay complex128).  devices: shard the shifts over these devices (contiguous chunks of
+        ceil(S / len(devices)), paradiag.cpp:217-236), one engine and host thread per shard."""
         if isinstance(fine, int):
             fine = Grid2D(fine)
         if precision not in ("c128", "c64"):
@@ -189,7 +190,10 @@ class BatchedMultigridHierarchy:
         self.device = device
         lam = np.array([complex(s.lam) for s in self.shifts], dtype=np.complex128)
         self._lam = lam
-        desc = N.BatchDesc(fine.n, len(lam), lam.ctypes.data, cfg._c(), 0 if precision == "c128" else 1, device)
+        self.devices = list(devices) if devices else None
+        self._devs = np.ascontiguousarray(self.devices or [], np.int32)
+        desc = N.BatchDesc(fine.n, len(lam), lam.ctypes.data, cfg._c(), 0 if precision == "c128" else 1, device,
+                           self._devs.ctypes.data if self.devices else None, len(self._devs))
         h = C.c_void_p()
         _check(N.lib().pdmg_create(C.byref(desc), C.byref(h)))
         self._h = h
@@ -263,6 +267,26 @@ class BatchedMultigridHierarchy:
             _check(N.lib().pdmg_solve_device(self._h, d_b, d_u, C.byref(rep)))
             return self._reports(rep, it, cv, hist, rate)
         _check(N.lib().pdmg_solve_device(self._h, d_b, d_u, None))
+        return None
+
+    def parts(self) -> list[tuple[int, int, int]]:
+        """Device shards: (first shift, shift count, device) per shard."""
+        out = []
+        for p in range(N.lib().pdmg_num_parts(self._h)):
+            s0, cnt, dev = C.c_int32(), C.c_int32(), C.c_int32()
+            _check(N.lib().pdmg_part_range(self._h, p, C.byref(s0), C.byref(cnt), C.byref(dev)))
+            out.append((s0.value, cnt.value, dev.value))
+        return out
+
+    def solve_device_shards(self, d_b: Sequence[int], d_u: Sequence[int], want_reports: bool = True):
+        """Solve with each shard's b and u already in its device's memory (pdmg_solve_device_shards)."""
+        P_ = len(d_b)
+        arr_b, arr_u = (C.c_void_p * P_)(*d_b), (C.c_void_p * P_)(*d_u)
+        if want_reports:
+            rep, it, cv, hist, rate = self._report_bufs()
+            _check(N.lib().pdmg_solve_device_shards(self._h, arr_b, arr_u, C.byref(rep)))
+            return self._reports(rep, it, cv, hist, rate)
+        _check(N.lib().pdmg_solve_device_shards(self._h, arr_b, arr_u, None))
         return None
 
     def cycle(self, u, b) -> np.ndarray:

@@ -21,16 +21,13 @@ from . import _native as N
 from .multigrid import ConfigError, Grid2D, MultigridConfig, SolveReport, _check
 
 
-class ParadiagCirculant:
-    """GPU ParaDIAG solver for one (n, nt, alpha, dt, cfg) on one device."""
+class _ParadiagBase:
+    """A GPU ParaDIAG solver object (pdmg_paradiag_*): one device, or the time slices sharded over `devices`
+    (the reference's `threads` argument of paradiag_solve, paradiag.cpp:207-236), with the time transforms
+    gathering / scattering across the shards through NVLink peer pointers inside the transform kernels."""
 
-    def __init__(self, grid: Grid2D | int, nt: int, alpha: float, dt: float, cfg: MultigridConfig, device: int = 0):
-        self.grid = grid if isinstance(grid, Grid2D) else Grid2D(int(grid))
-        self.nt, self.alpha, self.dt, self.cfg, self.device = nt, alpha, dt, cfg, device
-        h = C.c_void_p()
-        c = cfg._c()
-        _check(N.lib().pdmg_paradiag_create(self.grid.n, nt, alpha, dt, C.byref(c), device, C.byref(h)))
-        self._h = h
+    nt: int
+    cfg: MultigridConfig
 
     def close(self):
         if getattr(self, "_h", None):
@@ -52,6 +49,15 @@ class ParadiagCirculant:
     @property
     def solver_handle(self):
         return N.lib().pdmg_paradiag_solver(self._h)
+
+    def parts(self) -> list[tuple[int, int, int]]:
+        """Time-slice shards: (first slice, slice count, device)."""
+        out = []
+        for p in range(N.lib().pdmg_paradiag_num_parts(self._h)):
+            t0, cnt, dev = C.c_int32(), C.c_int32(), C.c_int32()
+            _check(N.lib().pdmg_paradiag_part_range(self._h, p, C.byref(t0), C.byref(cnt), C.byref(dev)))
+            out.append((t0.value, cnt.value, dev.value))
+        return out
 
     def _reports(self):
         S, H = self.nt, self.cfg.max_iter + 1
@@ -78,6 +84,56 @@ class ParadiagCirculant:
         rr = C.c_double()
         _check(N.lib().pdmg_paradiag_run_device(self._h, d_f, d_u, None, C.byref(rr)))
         return rr.value
+
+    def run_shards(self, d_f, d_u, want_reports: bool = False):
+        """Device-resident run of a sharded solver: d_f[p], d_u[p] = shard p's slices on its device."""
+        P_ = len(d_f)
+        af, au = (C.c_void_p * P_)(*d_f), (C.c_void_p * P_)(*d_u)
+        rr = C.c_double()
+        if want_reports:
+            rep, it, cv, hist, rate = self._reports()
+            _check(N.lib().pdmg_paradiag_run_shards(self._h, af, au, C.byref(rep), C.byref(rr)))
+            reps = [SolveReport(bool(cv[s]), int(it[s]), hist[s, : it[s] + 1].copy(), float(rate[s]), rep.seconds)
+                    for s in range(self.nt)]
+            return reps, rr.value
+        _check(N.lib().pdmg_paradiag_run_shards(self._h, af, au, None, C.byref(rr)))
+        return None, rr.value
+
+
+class ParadiagCirculant(_ParadiagBase):
+    """GPU ParaDIAG for the alpha-circulant time matrix (alpha > 0: the BASELINE preconditioner; alpha = -1/beta: the
+    reference's BackwardHeatQBV)."""
+
+    def __init__(self, grid: Grid2D | int, nt: int, alpha: float, dt: float, cfg: MultigridConfig, device: int = 0,
+                 devices=None):
+        self.grid = grid if isinstance(grid, Grid2D) else Grid2D(int(grid))
+        self.nt, self.alpha, self.dt, self.cfg, self.device = nt, alpha, dt, cfg, device
+        self._devs = np.ascontiguousarray(list(devices) if devices else [device], np.int32)
+        h = C.c_void_p()
+        c = cfg._c()
+        _check(N.lib().pdmg_paradiag_create_multi(self.grid.n, nt, alpha, dt, C.byref(c), self._devs.ctypes.data,
+                                                  len(self._devs), C.byref(h)))
+        self._h = h
+
+
+class ParadiagGeneral(_ParadiagBase):
+    """GPU ParaDIAG for a general diagonalizable time matrix B = V diag(lambdas) V^{-1} (HeatBVM,
+    diagonalize_time_matrix, paradiag.cpp:71-82); the time transforms are hand-written complex GEMM kernels."""
+
+    def __init__(self, grid: Grid2D | int, B: np.ndarray, dg: "TimeDiagonalization", cfg: MultigridConfig,
+                 device: int = 0, devices=None):
+        self.grid = grid if isinstance(grid, Grid2D) else Grid2D(int(grid))
+        self.nt, self.cfg, self.device = B.shape[0], cfg, device
+        self._B = np.ascontiguousarray(B, np.float64)
+        self._lam = np.ascontiguousarray(dg.eigenvalues, np.complex128)
+        self._V, self._Vi = np.ascontiguousarray(dg.V, np.complex128), np.ascontiguousarray(dg.Vinv, np.complex128)
+        self._devs = np.ascontiguousarray(list(devices) if devices else [device], np.int32)
+        h = C.c_void_p()
+        c = cfg._c()
+        _check(N.lib().pdmg_paradiag_create_general(self.grid.n, self.nt, self._lam.ctypes.data, self._V.ctypes.data,
+                                                    self._Vi.ctypes.data, self._B.ctypes.data, C.byref(c),
+                                                    self._devs.ctypes.data, len(self._devs), C.byref(h)))
+        self._h = h
 
 
 def heat_initial_rhs(n: int, nt: int, dt: float, seed: int = 4) -> np.ndarray:
@@ -191,36 +247,50 @@ def diagonalize_time_matrix(B: np.ndarray) -> TimeDiagonalization:
     return TimeDiagonalization(lam.astype(np.complex128), V, np.linalg.inv(V), cond, not cond <= 1e12)
 
 
-def paradiag_solve(f: np.ndarray, td: TimeDiscretization, cfg: MultigridConfig, device: int = 0):
+def diagonalize_qbv_closed_form(td: TimeDiscretization) -> TimeDiagonalization:
+    """diagonalize_qbv_closed_form (paradiag.cpp:84-108): eigenvalue k = (1 - gamma zeta^{-k}) / tau with
+    gamma = |alpha|^{1/m} e^{i pi/m}, alpha = -1/beta, zeta = e^{2 pi i/m}; column k of V is
+    V(j, k) = gamma^{-j} zeta^{jk} / m, normalized.  cond_estimate is the 1-norm condition number of V (the
+    reference's Eigen rcond() estimates the same quantity)."""
+    td.validate()
+    if td.kind != TimeSchemeKind.BackwardHeatQBV:
+        raise ConfigError("diagonalize_qbv_closed_form: scheme is not BackwardHeatQBV")
+    m = td.n + 1
+    gr, ga, wa = (1.0 / td.beta) ** (1.0 / m), np.pi / m, 2.0 * np.pi / m
+    k = np.arange(m)
+    lam = (1.0 - gr * np.exp(1j * (ga - wa * k))) / td.tau
+    j = np.arange(m)[:, None]
+    V = (gr ** (-j.astype(np.float64))) * np.exp(1j * j * (wa * k[None, :] - ga)) / m
+    V = V / np.linalg.norm(V, axis=0, keepdims=True)
+    cond = float(np.linalg.cond(V, 1))
+    return TimeDiagonalization(lam.astype(np.complex128), V, np.linalg.inv(V), cond, not cond <= 1e12)
+
+
+def qbv_slot_of_reference_index(m: int) -> np.ndarray:
+    """The circulant engine's slot q holds lambda_q = (1 - gamma e^{+2 pi i q/m})/tau; the reference's eigenvalue
+    k is (1 - gamma zeta^{-k})/tau (paradiag.cpp:100), so reference index k is slot (m - k) mod m."""
+    return (m - np.arange(m)) % m
+
+
+def paradiag_solve(f: np.ndarray, td: TimeDiscretization, cfg: MultigridConfig, device: int = 0, devices=None):
     """paradiag_solve (paradiag.cpp:185-248): returns (u, reports, relres).  The circulant schemes
-    (BackwardHeatQBV, CirculantAlpha) transform time with an alpha-scaled FFT; HeatBVM with dense GEMMs
-    against the eigenvector matrix."""
+    (BackwardHeatQBV, CirculantAlpha) transform time with an alpha-scaled FFT; HeatBVM with dense GEMM kernels
+    against the eigenvector matrix.  devices: shard the time slices over these devices (the reference's `threads`)."""
     td.validate()
     f = np.ascontiguousarray(f, np.complex128)
     if f.shape[0] != td.dim():
         raise ConfigError(f"paradiag_solve: expected {td.dim()} time slices, got {f.shape[0]}")
     n = f.shape[-1] + 1
     if td.kind != TimeSchemeKind.HeatBVM:
-        with ParadiagCirculant(n, td.dim(), td.circulant_alpha(), td.tau, cfg, device) as pd:
-            return pd.run(f)
+        with ParadiagCirculant(n, td.dim(), td.circulant_alpha(), td.tau, cfg, device, devices) as pd:
+            u, reps, rr = pd.run(f)
+        if td.kind == TimeSchemeKind.BackwardHeatQBV:  # reports in the reference's eigenvalue order
+            reps = [reps[q] for q in qbv_slot_of_reference_index(td.dim())]
+        return u, reps, rr
     B = np.ascontiguousarray(time_stepping_matrix(td), np.float64)
     dg = diagonalize_time_matrix(B)
-    nt = td.dim()
-    u = np.empty_like(f)
-    H = cfg.max_iter + 1
-    it, cv = np.zeros(nt, np.int32), np.zeros(nt, np.uint8)
-    hist, rate = np.zeros((nt, H)), np.zeros(nt)
-    rep = N.SolveReport(it.ctypes.data, cv.ctypes.data, hist.ctypes.data, rate.ctypes.data, 0.0)
-    rr = C.c_double()
-    lam = np.ascontiguousarray(dg.eigenvalues)
-    V, Vi = np.ascontiguousarray(dg.V), np.ascontiguousarray(dg.Vinv)
-    c = cfg._c()
-    _check(N.lib().pdmg_paradiag_general(n, nt, lam.ctypes.data, V.ctypes.data, Vi.ctypes.data, B.ctypes.data,
-                                         C.byref(c), device, f.ctypes.data, u.ctypes.data, C.byref(rep),
-                                         C.byref(rr)))
-    reps = [SolveReport(bool(cv[s]), int(it[s]), hist[s, : it[s] + 1].copy(), float(rate[s]), rep.seconds)
-            for s in range(nt)]
-    return u, reps, rr.value
+    with ParadiagGeneral(n, B, dg, cfg, device, devices) as pd:
+        return pd.run(f)
 
 
 def helmholtz_shifts(h: float) -> np.ndarray:

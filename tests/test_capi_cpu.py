@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 25
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.pdmg_abi_version() == 1
+    assert lib.pdmg_abi_version() == 2
 
 
 def test_library_is_sm100a_fatbin():

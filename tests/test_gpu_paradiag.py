@@ -90,7 +90,11 @@ def test_qbv_matches_oracle(oracle):
     cfg = P.MultigridConfig(P.CycleKind.V, 1, 1, 4, 1e-10, 200, P.SmootherConfig.vanka())
     u, reps, relres = P.paradiag_solve(f, td, cfg)
     ref = oracle.paradiag(n, nt, td.circulant_alpha(), td.tau, Cfg(), f, threads=8)
-    assert [r.iterations for r in reps] == ref["iterations"].tolist()
+    # paradiag_solve reports in the reference's eigenvalue order (paradiag.cpp:100): index k is circulant slot -k
+    slots = P.paradiag.qbv_slot_of_reference_index(nt)
+    assert [r.iterations for r in reps] == ref["iterations"][slots].tolist()
+    lam_ref = P.diagonalize_qbv_closed_form(td).eigenvalues
+    np.testing.assert_allclose(lam_ref, P.circulant_shifts(td.circulant_alpha(), nt, td.tau)[slots], rtol=1e-13)
     assert rel(u, ref["u"]) < 1e-10
     assert abs(relres - ref["relres"]) <= 1e-3 * ref["relres"] + 1e-14
 
@@ -136,3 +140,81 @@ def test_heat_bvm_manufactured_run():
     assert relres <= 1e-6
     err = max(np.linalg.norm(u[i] - ustar[i]) / np.linalg.norm(ustar[i]) for i in range(td.dim()))
     assert err <= 1e-5
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_paradiag_device_list_matches_single(oracle, devices):
+    """ParaDIAG with the time slices sharded over a device list (here shards sharing GPU 0, each with its own
+    engine and stream): both time transforms gather their columns from every shard and scatter the rows to
+    their owners inside the kernel; the result is bitwise the single-device one (the per-point transform
+    arithmetic does not depend on the sharding) and relres agrees to summation order."""
+    n, nt = 32, 10  # 10 slices over 3 shards: 4, 4, 2 (paradiag.cpp:222 chunking); not a power of two
+    m = n - 1
+    alpha, dt = 0.01, 1.0 / nt
+    f = oracle.random_complex(9, nt * m * m).reshape(nt, m, m)
+    cfg = P.MultigridConfig(P.CycleKind.V, 1, 1, 4, 1e-10, 200, P.SmootherConfig.vanka())
+    with ParadiagCirculant(n, nt, alpha, dt, cfg) as pd:
+        u1, reps1, rr1 = pd.run(f)
+    with ParadiagCirculant(n, nt, alpha, dt, cfg, devices=devices) as pd:
+        parts = pd.parts()
+        u2, reps2, rr2 = pd.run(f)
+    chunk = -(-nt // len(devices))
+    assert parts[0] == (0, chunk, 0) and sum(p[1] for p in parts) == nt
+    assert np.array_equal(u1, u2)
+    assert [r.iterations for r in reps1] == [r.iterations for r in reps2]
+    assert abs(rr1 - rr2) <= 1e-12 * rr1
+
+
+def test_paradiag_shards_device_resident(oracle):
+    """pdmg_paradiag_run_shards: per-shard device buffers."""
+    n, nt = 32, 8
+    m = n - 1
+    f = oracle.random_complex(10, nt * m * m).reshape(nt, m, m)
+    cfg = P.MultigridConfig(P.CycleKind.V, 1, 1, 4, 1e-10, 200, P.SmootherConfig.vanka())
+    with ParadiagCirculant(n, nt, 0.01, 1.0 / nt, cfg) as pd:
+        u1, _, rr1 = pd.run(f)
+    with ParadiagCirculant(n, nt, 0.01, 1.0 / nt, cfg, devices=[0, 0]) as pd:
+        d_f = [torch.from_numpy(np.ascontiguousarray(f[t0:t0 + c]).view(np.float64)).cuda() for t0, c, _ in pd.parts()]
+        d_u = [torch.empty_like(x) for x in d_f]
+        reps, rr2 = pd.run_shards([x.data_ptr() for x in d_f], [x.data_ptr() for x in d_u], want_reports=True)
+        torch.cuda.synchronize()
+        u2 = np.concatenate([x.cpu().numpy().view(np.complex128).reshape(-1, m, m) for x in d_u])
+    assert np.array_equal(u1, u2) and abs(rr1 - rr2) <= 1e-12 * rr1
+    assert all(r.converged for r in reps)
+
+
+@pytest.mark.parametrize("nt,npts", [(1, 7), (5, 1000), (33, 4099), (64, 20000)])
+def test_time_transform_kernel_matches_numpy(nt, npts):
+    """The hand-written complex fp64 GEMM over the time index (k_time_gemm; kron_time_apply, paradiag.cpp:129-133)
+    against numpy, ragged in both the time and the point dimensions."""
+    rng = np.random.default_rng(nt)
+    M = rng.standard_normal((nt, nt)) + 1j * rng.standard_normal((nt, nt))
+    x = rng.standard_normal((nt, npts)) + 1j * rng.standard_normal((nt, npts))
+    dx = torch.from_numpy(x.view(np.float64)).cuda()
+    dy = torch.empty_like(dx)
+    Mc = np.ascontiguousarray(M)
+    assert N.lib().pdmg_time_transform(0, nt, npts, Mc.ctypes.data, dx.data_ptr(), dy.data_ptr(), None) == 0
+    y = dy.cpu().numpy().view(np.complex128)
+    np.testing.assert_allclose(y, M @ x, rtol=0, atol=1e-12 * max(1.0, np.abs(M @ x).max()))
+
+
+@pytest.mark.parametrize("devices", [None, [0, 0]])
+def test_heat_bvm_general_scheme_matches_oracle_solves(oracle, devices):
+    """HeatBVM through the general scheme (hand-written time GEMMs), one device and sharded: every slot's
+    shifted solve matches the oracle's batched solve of the same transformed right-hand side, and the
+    all-at-once residual is at the multigrid tolerance."""
+    n = 32
+    td = P.TimeDiscretization(P.TimeSchemeKind.HeatBVM, 8, 1.0 / 8, 0.01)
+    m, nt = n - 1, td.dim()
+    f = oracle.random_complex(12, nt * m * m).reshape(nt, m, m)
+    cfg = P.MultigridConfig(P.CycleKind.V, 1, 1, 4, 1e-10, 200, P.SmootherConfig.vanka())
+    B = P.time_stepping_matrix(td)
+    dg = P.diagonalize_time_matrix(B)
+    with P.ParadiagGeneral(n, B, dg, cfg, devices=devices) as pd:
+        u, reps, relres = pd.run(f)
+    g = (dg.Vinv @ f.reshape(nt, -1)).reshape(nt, m, m)
+    ref = oracle.solve_batch(n, dg.eigenvalues, Cfg(), g, threads=8)
+    assert [r.iterations for r in reps] == ref["iterations"].tolist()
+    u_ref = (dg.V @ ref["u"].reshape(nt, -1)).reshape(nt, m, m)
+    assert rel(u, u_ref) < 1e-10
+    assert relres < 1e-8

@@ -108,8 +108,9 @@ def _check_solve(oracle, n, lams, b, cfg: Cfg, tol_rel=1e-10, path="auto", expec
             continue
         assert np.max(np.abs(reps[s].residual_history - hist_ref) / hist_ref[0]) < tol_rel
         assert rel(u[s], ref["u"][s]) < tol_rel
-        # rate is a geometric mean of ratios of residuals ~1e-10 r0, so it inherits their relative error
-        assert abs(reps[s].rate - ref["rates"][s]) <= 1e-6 * ref["rates"][s]
+        # rate is a geometric mean of ratios of residuals ~1e-10 r0: their roundoff differences (~1e-16 r0,
+        # i.e. ~1e-6 of the last entries) carry into it
+        assert abs(reps[s].rate - ref["rates"][s]) <= 1e-5 * ref["rates"][s]
     return u, reps, ref
 
 
@@ -318,15 +319,121 @@ def test_predicted_last_norm(oracle, monkeypatch, cyc, pred):
     assert reps[1].iterations == 0 and np.all(u[1] == 0)
 
 
-@pytest.mark.parametrize("cyc", [Cfg(nu1=1, nu2=1), Cfg(nu1=1, nu2=1, cycle="W"), Cfg(nu1=1, nu2=1, tol=1e-14, max_iter=3)])
-def test_xfuse_matches_oracle(oracle, monkeypatch, cyc):
-    """V(1,1) cross-cycle fusion (PDMG_XFUSE=1): cycle k's fine post-sweep and cycle k+1's pre-sweep run as
-    one k_march2<MID> pass that also stores u_k and forms ||b - L u_k||; mixed convergence (b = 0, an easy
-    and a hard shift) and max_iter exhaustion must reproduce the oracle's counts, histories and iterates."""
-    monkeypatch.setenv("PDMG_XFUSE", "1")
-    n, m = 128, 127
-    lams = [5000 + 0j, 0.0, 0.0, 8.959263353215057 - 15.395328029306036j]
-    b = oracle.random_complex(43, 4 * m * m).reshape(4, m, m)
-    b[1] = 0
-    u, reps, ref = _check_solve(oracle, n, lams, b, cyc, path="batched", expect_kernel="+mid")
-    assert reps[1].iterations == 0 and np.all(u[1] == 0)
+def test_batch_beyond_coef_max(oracle):
+    """A 600-shift batch on the batched path (n = 128): the marching passes take their per-shift coefficients
+    as kernel parameters, COEF_MAX = 256 shifts per launch, so shifts 256..599 run in launches with
+    shift0 = 256 and 512.  Every shift is checked against the oracle."""
+    n, m, S = 128, 127, 600
+    lams = oracle.circulant_shifts(0.01, S, 1 / 32, 0, S)
+    b = oracle.random_complex(17, S * m * m).reshape(S, m, m)
+    _check_solve(oracle, n, lams, b, Cfg(), path="batched")
+
+
+def test_config3_sample_golden_on_gpu(oracle):
+    """The reference-generated C3 sample (tests/golden/reference_golden.json, produced by the reference's own
+    grid.cpp/smoother.cpp): cycle counts and residual histories within 1e-10 on the GPU path."""
+    import json
+    import os
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))["solves"]["C3_sample"]
+    n, m = g["n"], g["n"] - 1
+    lams = [complex(*x) for x in g["lambdas"]]
+    b = oracle.random_complex(g["seed"], 2 * m * m).reshape(2, m, m)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, mgcfg(Cfg(**g["cfg"]))) as H:
+        _, reps = H.solve(b)
+    for j in range(2):
+        h = np.array(g["hist"][j])
+        assert reps[j].iterations == g["iterations"][j]
+        assert np.max(np.abs(reps[j].residual_history - h) / h[0]) < 1e-10
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_large_coarsest_grid(oracle, path):
+    """coarsest_n = 58 (57 x 57 = 3249 coarse unknowns): the batched direct solve stages 52 KB of coarse
+    right-hand side in shared memory, above the 48 KB default (the kernels opt in at setup)."""
+    n, m = 116, 115
+    lams = [0.0, 300 - 40j]
+    b = oracle.random_complex(23, 2 * m * m).reshape(2, m, m)
+    _check_solve(oracle, n, lams, b, Cfg(coarsest_n=58), path=path)
+
+
+def test_coarsest_too_large_is_config_error():
+    """coarsest_n = 128 needs 258 KB of shared memory for the coarse right-hand side: rejected up front."""
+    with pytest.raises(P.ConfigError, match="shared memory"):
+        P.BatchedMultigridHierarchy(P.Grid2D(128), [0.0], P.MultigridConfig(coarsest_n=128))
+
+
+@pytest.mark.parametrize("chunks", [3, 5])
+def test_chunked_host_solve_marching_passes(oracle, monkeypatch, chunks):
+    """The concurrent chunked host solve at n = 256 (the k_march2 / L2-prefetch passes, whose halo reads reach
+    past a chunk's last shift into the next chunk's storage): bitwise the one-chunk result."""
+    import ctypes
+
+    from paper_2203_11154_b200 import _native as N
+
+    n, m, S = 256, 255, 7
+    lams = oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, 256)[[0, 3, 40, 77, 128, 200, 255]]
+    cfg = mgcfg(Cfg(nu1=2, nu2=2))
+    b = P.random_rhs(n, 6, count=S)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        u_ref, reps_ref = H.solve(b)
+    monkeypatch.setenv("PDMG_IO_CHUNKS", str(chunks))
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        nbytes = b.nbytes
+        hb, hu = N.lib().pdmg_host_alloc(nbytes), N.lib().pdmg_host_alloc(nbytes)
+        try:
+            ctypes.memmove(hb, b.ctypes.data, nbytes)
+            rep, it, cv, hist, rate = H._report_bufs()
+            assert N.lib().pdmg_solve(H._h, hb, hu, ctypes.byref(rep)) == 0, N.lib().pdmg_last_error()
+            u = np.empty_like(b)
+            ctypes.memmove(u.ctypes.data, hu, nbytes)
+            reps = H._reports(rep, it, cv, hist, rate)
+        finally:
+            N.lib().pdmg_host_free(hb)
+            N.lib().pdmg_host_free(hu)
+    assert np.array_equal(u, u_ref)
+    for r, q in zip(reps, reps_ref):
+        assert r.iterations == q.iterations and list(r.residual_history) == list(q.residual_history)
+
+
+def test_device_list_matches_single_device(oracle):
+    """One context sharded over a device list (three shards sharing GPU 0, chunks of ceil(S / 3),
+    paradiag.cpp:222): host solve, device-resident shard solve, cycle and level operators are bitwise the
+    single-device context's."""
+    import torch
+
+    n, m, S = 64, 63, 7
+    lams = oracle.circulant_shifts(0.01, 32, 1 / 32, 0, S)
+    cfg = mgcfg(Cfg())
+    b = oracle.random_complex(3, S * m * m).reshape(S, m, m)
+    u0 = oracle.random_complex(4, S * m * m).reshape(S, m, m)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        H.set_solve_path("batched")
+        u1, r1 = H.solve(b)
+        c1 = H.cycle(u0, b)
+        s1 = H.apply_smoother(1, u0[:, ::2, ::2][:, :31, :31].copy(), b[:, ::2, ::2][:, :31, :31].copy())
+        n1 = H.norm(0, b)
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg, devices=[0, 0, 0]) as H:
+        H.set_solve_path("batched")
+        assert H.parts() == [(0, 3, 0), (3, 3, 0), (6, 1, 0)]
+        u2, r2 = H.solve(b)
+        c2 = H.cycle(u0, b)
+        s2 = H.apply_smoother(1, u0[:, ::2, ::2][:, :31, :31].copy(), b[:, ::2, ::2][:, :31, :31].copy())
+        n2 = H.norm(0, b)
+        d_b = [torch.from_numpy(np.ascontiguousarray(b[s0:s0 + c]).view(np.float64)).cuda() for s0, c, _ in H.parts()]
+        d_u = [torch.empty_like(x) for x in d_b]
+        r3 = H.solve_device_shards([x.data_ptr() for x in d_b], [x.data_ptr() for x in d_u])
+        torch.cuda.synchronize()
+        u3 = np.concatenate([x.cpu().numpy().view(np.complex128).reshape(-1, m, m) for x in d_u])
+        with pytest.raises(P.ConfigError, match="pdmg_solve_device_shards"):
+            H.solve_device(d_b[0].data_ptr(), d_u[0].data_ptr())
+    assert np.array_equal(u1, u2) and np.array_equal(u1, u3)
+    assert np.array_equal(c1, c2) and np.array_equal(s1, s2) and np.array_equal(n1, n2)
+    for a, q, w in zip(r1, r2, r3):
+        assert a.iterations == q.iterations == w.iterations
+        assert list(a.residual_history) == list(q.residual_history) == list(w.residual_history)
+
+
+def test_device_list_bad_device_is_device_error():
+    with pytest.raises(P.DeviceError, match="not available"):
+        P.BatchedMultigridHierarchy(P.Grid2D(16), [0.0, 1.0], P.MultigridConfig(), devices=[0, 97])

@@ -87,6 +87,34 @@ def test_config2_batch_matches_reference(oracle):
         assert np.array_equal(s["u"][j].ravel()[:4], l2c(g["u"][j]["first"]))
 
 
+def test_config3_sample_matches_reference(oracle):
+    """BASELINE config 3 shape (h=1/512, V(2,2), alpha=1e-3): the reference-generated C3 sample (slots 0 and 128
+    with the first two seed-2 right-hand sides, tests/golden/make_golden.py) -- cycle counts and residual
+    histories bit for bit."""
+    g = GOLD["solves"]["C3_sample"]
+    n, m = g["n"], g["n"] - 1
+    lams = l2c(g["lambdas"])
+    b = oracle.random_complex(g["seed"], 2 * m * m).reshape(2, m, m)
+    s = oracle.solve_batch(n, lams, _cfg(g["cfg"]), b, threads=2)
+    for j in range(2):
+        it = g["iterations"][j]
+        assert s["iterations"][j] == it
+        assert np.array_equal(s["hist"][j, : it + 1], np.array(g["hist"][j]))
+
+
+def test_banded_coarse_factor_large_coarsest(oracle):
+    """The coarsest-level LU (dense.cpp:82-100) exploits the band of A + lambda I (skipping exact zeros only):
+    a 57 x 57 coarsest grid (3249 unknowns) factors quickly and solves to roundoff."""
+    n = 58
+    m = n - 1
+    for lam in (0.0, 300 - 40j):
+        b = oracle.random_complex(9, m * m).reshape(m, m)
+        s = oracle.solve(n, lam, Cfg(coarsest_n=n, nu1=1, nu2=1), b)  # single level: a direct solve
+        assert s["iterations"] == 1 and s["converged"]
+        r = oracle.residual(n, lam, b, s["u"])
+        assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(b)
+
+
 def test_threads_bitwise_identical(oracle):
     """paradiag test 'multi-threaded result is bitwise identical' (test_paradiag.cpp:250-259)."""
     lams = oracle.circulant_shifts(0.01, 32, 1 / 32)[:6]
