@@ -134,6 +134,62 @@ class ClockSampler:
                 "samples": len(self.samples), "source": self.src}
 
 
+def roofline_of(stats: dict, config: str, upd_per_step: float, nu_sum: int) -> dict:
+    """Roofline entry of the dominant kernel class (by CUDA-event time in the profiled pass).  `achieved` = SURVEY
+    8(d) algorithmic bytes (48 B per c128 grid-point smoother update, 24 B c64, plus S/4 per point for a fused
+    restriction / prolongation; a transform or residual pass: the bytes it must move) / the class's average launch
+    time, against MEASURED_PEAKS.json hbm_gbs."""
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md 6650 GB/s)"
+    peak = peak or 6650.0
+    top_name, top = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    total_ms = sum(v["ms"] for v in stats.values())
+    all_bytes = sum(v.get("unit_bytes", v["bytes"]) for v in stats.values())
+    moved = None
+    if top["bytes"] > 0:
+        ub = top.get("unit_bytes") or top["bytes"]
+        achieved = ub / (top["ms"] / 1e3) / 1e9
+        mv = top["bytes"] / (top["ms"] / 1e3) / 1e9
+        moved = {"moved_bytes_per_launch": top["bytes"] / top["launches"], "moved_GBps": round(mv, 1),
+                 "moved_frac": round(mv / peak, 4), "updates_per_launch": top.get("updates", 0.0) / top["launches"]}
+        bound = "hbm"
+    else:
+        # one-CTA-per-shift solve (small grids): its working set is L2/L1-resident, so report the
+        # operator-level algorithmic bytes (SURVEY 8(d): 96 B/update V(1,1), 72 B/update V(2,2), c128)
+        bpu = {2: 96.0, 4: 72.0}.get(nu_sum, 96.0)
+        achieved = upd_per_step * bpu / (top["ms"] / top["launches"] / 1e3) / 1e9
+        bound = "latency (L2-resident working set; operator-level bytes)"
+    roofline = {"bound": bound, "kernel": top_name, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "kernel_share_of_step": round(top["ms"] / total_ms, 4),
+                "timing": "per-kernel CUDA events on the library stream, profiled pass right after the timed region",
+                "launch_avg_ms": round(top["ms"] / top["launches"], 4),
+                "algo_bytes_per_launch": (top.get("unit_bytes") or top["bytes"]) / top["launches"],
+                "algo_bytes_def": "SURVEY 8(d): 48 B (c128) / 24 B (c64) per grid-point smoother update, plus "
+                                  "S/4 per point for a fused restriction or prolongation",
+                "all_kernels_algorithmic_GBps": round(all_bytes / (total_ms / 1e3) / 1e9, 1),
+                "frac_note": "a two-sweep pass performs two smoother updates per point while streaming the level "
+                             "once (temporal blocking), so its SURVEY 8(d) algorithmic rate can exceed the HBM "
+                             "peak; moved_GBps / moved_frac are the bytes the pass physically moves"}
+    if moved:
+        roofline.update(moved)
+    roofline.update(traffic_for(config, top_name))
+    return roofline
+
+
+def kernels_summary(stats: dict, top: int = 12) -> dict:
+    return {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                "GBps": round(v.get("unit_bytes", v["bytes"]) / v["ms"] / 1e6, 1) if v["ms"] > 0 else None,
+                "moved_GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] > 0 else None}
+            for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])[:top]}
+
+
 def so_sha16() -> str:
     import hashlib
 
@@ -153,7 +209,7 @@ def traffic_for(config: str, kernel: str) -> dict:
     except Exception:
         return {"traffic": None, "traffic_note": "no ncu capture in profiles/traffic.json"}
     ent = tj.get(config, {}).get(kernel)
-    if not ent:
+    if not isinstance(ent, dict):
         return {"traffic": None, "traffic_note": f"no ncu capture of {kernel} for {config}"}
     cur = so_sha16()
     if ent.get("so_sha16") != cur:
@@ -317,6 +373,8 @@ def run_paradiag(args):
     sh = N.lib().pdmg_stream(pd.solver_handle) if world == 1 else None
     stream = torch.cuda.ExternalStream(sh) if sh else torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world == 1:
+        N.lib().pdmg_reset_stats(pd.solver_handle)
     t0 = time.perf_counter()
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -331,6 +389,21 @@ def run_paradiag(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     relres = out[2]
+    launches = int(N.lib().pdmg_launch_count(pd.solver_handle)) if world == 1 else None
+    roofline, kern = None, None
+    if world == 1:  # per-kernel CUDA events in a separate profiled pass (the timed region carries no events)
+        from paper_2203_11154_b200.multigrid import kernel_stats
+
+        hs = pd.solver_handle
+        N.lib().pdmg_reset_stats(hs)
+        N.lib().pdmg_set_profiling(hs, 1)
+        for _ in range(max(1, min(args.steps, 3))):
+            step()
+        torch.cuda.synchronize()
+        kst = kernel_stats(hs)
+        N.lib().pdmg_set_profiling(hs, 0)
+        roofline = roofline_of(kst, "c5", 0.0, nu1 + nu2)
+        kern = kernels_summary(kst)
     # total V-cycles over all slots (for the updates count), from one reported run
     if world == 1:
         u, reps, rr = pd.run(f)
@@ -363,14 +436,35 @@ def run_paradiag(args):
         N.lib().pdmg_host_free(hu)
         e2e = {"value": e_steps * iters_total * upc / e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": e_steps, "ms_per_step": 1e3 * e_s / e_steps}
+    cpu = parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:  # the oracle's ParaDIAG (C restatement of paradiag.cpp:185-248 with the alpha-circulant transforms)
+            from oracle_lib import Cfg, Oracle
+
+            thr = os.cpu_count() or 1
+            t_c = time.perf_counter()
+            ref = Oracle().paradiag(n, nt, alpha, dt, Cfg(nu1=nu1, nu2=nu2), f, threads=thr)
+            t_c = time.perf_counter() - t_c
+            iters_ref = int(np.sum(ref["iterations"]))
+            cpu = {"value": iters_ref * upc / t_c, "unit": UNIT, "cores": thr, "kind": "port", "cpu_model": cpu_model(),
+                   "sample": f"the whole C5 step (time transforms + {nt} shifted solves + residual), {thr} threads, "
+                             f"{t_c:.2f} s wall", "seconds": t_c}
+            it_gpu = np.array([r.iterations for r in reps])
+            parity = {"slots_compared": nt, "iters_equal": bool(np.array_equal(it_gpu, ref["iterations"])),
+                      "max_rel_err_u": float(np.linalg.norm((u - ref["u"]).ravel()) / np.linalg.norm(ref["u"].ravel())),
+                      "relres_gpu": relres, "relres_oracle": ref["relres"],
+                      "reference": "oracle/liboracle.so (orc_paradiag_circulant) on the box's host"}
+        except Exception as e:
+            cpu = {"error": str(e)}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "gpu_launches": launches, "cpu_baseline": cpu, "parity": parity,
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": desc, "parallelism": f"time-sharded x{world} + NCCL all-to-all"},
             "paradiag_steps_per_s": 1e3 / ms, "relres": relres, "cycles_total": iters_total,
-            "host_wall_ms_per_step": wall_ms, "e2e": e2e,
+            "host_wall_ms_per_step": wall_ms, "e2e": e2e, "roofline": roofline, "kernels": kern,
             "clocks": clk.summary()}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -500,52 +594,23 @@ def main():
     e_value = sum_over_ranks(e_upd) / e_s_max
     N.lib().pdmg_host_free(hb)
     N.lib().pdmg_host_free(hu)
+    # the same through pageable host buffers (numpy arrays; what a std::vector through the C++ facade passes):
+    # the library page-locks them for the call (cudaHostRegister) and runs the same chunked pipeline
+    u_np = np.empty_like(b_host)
+    st = N.lib().pdmg_solve(H._h, b_host.ctypes.data, u_np.ctypes.data, ctypes.byref(rep))
+    assert st == 0, N.lib().pdmg_last_error()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        st = N.lib().pdmg_solve(H._h, b_host.ctypes.data, u_np.ctypes.data, ctypes.byref(rep))
+        assert st == 0, N.lib().pdmg_last_error()
+    barrier()
+    e_pg = max_over_ranks(time.perf_counter() - t0)
+    e2e_pageable = {"value": sum_over_ranks(e_upd) / e_pg, "unit": UNIT, "ms_per_step": 1e3 * e_pg / e_steps,
+                    "buffers": "pageable numpy arrays (page-locked by the library for the call)"}
+    del u_np
 
-    # ---- roofline of the dominant kernel ------------------------------------------------------
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs")
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md 6650 GB/s)"
-    peak = peak or 6650.0
-    top_name, top = max(stats.items(), key=lambda kv: kv[1]["ms"])
-    total_ms = sum(v["ms"] for v in stats.values())
-    all_bytes = sum(v.get("unit_bytes", v["bytes"]) for v in stats.values())
-    moved = None
-    if top["bytes"] > 0:
-        # SURVEY 8(d) algorithmic bytes: 48 B (c128) / 24 B (c64) per grid-point smoother update + the fused
-        # transfers; a two-sweep pass performs two updates per point.  `moved_*` is what the pass must move.
-        ub = top.get("unit_bytes") or top["bytes"]
-        achieved = ub / (top["ms"] / 1e3) / 1e9
-        mv = top["bytes"] / (top["ms"] / 1e3) / 1e9
-        moved = {"moved_bytes_per_launch": top["bytes"] / top["launches"], "moved_GBps": round(mv, 1),
-                 "moved_frac": round(mv / (peaks.get("hbm_gbs") or 6650.0), 4),
-                 "updates_per_launch": top.get("updates", 0.0) / top["launches"]}
-        bound = "hbm"
-    else:
-        # one-CTA-per-shift solve (small grids): its working set is L2/L1-resident, so report the
-        # operator-level algorithmic bytes (96 B/update V(1,1), 72 B/update V(2,2), c128)
-        bpu = {2: 96.0, 4: 72.0}.get(nu1 + nu2, 96.0)
-        achieved = upd / args.steps * bpu / (top["ms"] / top["launches"] / 1e3) / 1e9
-        bound = "latency (L2-resident working set; operator-level bytes)"
-    roofline = {"bound": bound, "kernel": top_name, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                "kernel_share_of_step": round(top["ms"] / total_ms, 4),
-                "timing": "per-kernel CUDA events on the library stream, profiled pass right after the timed region",
-                "launch_avg_ms": round(top["ms"] / top["launches"], 4),
-                "algo_bytes_per_launch": (top.get("unit_bytes") or top["bytes"]) / top["launches"],
-                "algo_bytes_def": "SURVEY 8(d): 48 B (c128) / 24 B (c64) per grid-point smoother update, plus "
-                                  "S/4 per point for a fused restriction or prolongation",
-                "all_kernels_algorithmic_GBps": round(all_bytes / (total_ms / 1e3) / 1e9, 1),
-                "frac_note": "a two-sweep pass performs two smoother updates per point while streaming the level "
-                             "once (temporal blocking), so its SURVEY 8(d) algorithmic rate can exceed the HBM "
-                             "peak; moved_GBps / moved_frac are the bytes the pass physically moves"}
-    if moved:
-        roofline.update(moved)
-    roofline.update(traffic_for(args.config, top_name))
+    roofline = roofline_of(stats, args.config, upd / args.steps, nu1 + nu2)
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -574,16 +639,15 @@ def main():
                        if S * (n + 1) * n * 16 > 126e6 else "working set fits in L2 (latency-bound config)"},
             "shifts_per_s": shifts_per_s, "cycles_per_shift": sorted(set(iters)), "all_converged": conv,
             "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                    "steps": e_steps, "ms_per_step": 1e3 * e_s_max / e_steps},
+                    "steps": e_steps, "ms_per_step": 1e3 * e_s_max / e_steps,
+                    "buffers": "pinned (pdmg_host_alloc)"},
+            "e2e_pageable": e2e_pageable,
             "gpu_launches": int(launches),
             "roofline": roofline,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "parity": parity,
-            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                            "GBps": round(v.get("unit_bytes", v["bytes"]) / v["ms"] / 1e6, 1) if v["ms"] > 0 else None,
-                            "moved_GBps": round(v["bytes"] / v["ms"] / 1e6, 1) if v["ms"] > 0 else None}
-                        for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])[:12]},
+            "kernels": kernels_summary(stats),
         }
         print(json.dumps(line), flush=True)
     H.close()

@@ -189,6 +189,46 @@ int pdmg_time_dft(int32_t device, int32_t nt, int64_t npts, double alpha, int32_
 int pdmg_aao_residual(int32_t device, int32_t n, int32_t ntl, int32_t t0, double alpha, double dt, const void* d_u,
                       const void* d_u_prev, const void* d_f, double* sums, void* stream);
 
+/* ---- Local Fourier analysis (proj/include/pdmg/lfa.hpp, proj/src/lfa.cpp) ----------------------------------------
+ * Symbols of the shifted operator, the Vanka / Jacobi preconditioner, the smoother error and the transfer operators;
+ * smoothing factors over the sampled high-frequency region (first maximizer in the reference's sampling order);
+ * the shift-splitting bound; the two-grid model rho(omega, nu); the damping optimization (coarse scan of
+ * [0.1, 1.9] by 0.01, golden-section refinement to 1e-4).  The per-frequency work runs on `device`: one thread per
+ * (omega, base frequency) for the 4 x 4 two-grid spectral radii. */
+typedef struct {
+  int32_t samples_per_dim; /* even, >= 16 (LFAConfig, lfa.hpp:21-31)          */
+  double coarse_skip_tol;  /* two-grid bases with |coarse symbol| <= this skipped */
+} pdmg_lfa_config;
+enum { PDMG_LFA_OPERATOR = 0, PDMG_LFA_VANKA = 1, PDMG_LFA_PRECONDITIONER = 2, PDMG_LFA_SMOOTHER_ERROR = 3,
+       PDMG_LFA_TRANSFER = 4 };
+enum { PDMG_LFA_TWO_GRID_RHO = 0, PDMG_LFA_SMOOTHING_MU = 1 }; /* OmegaObjective (lfa.hpp:100-103) */
+void pdmg_lfa_config_default(pdmg_lfa_config* cfg); /* {64, 1e-8} */
+/* symbol_shifted_laplacian / symbol_vanka / symbol_preconditioner / symbol_smoother_error / symbol_transfer
+ * (lfa.hpp:33-53) at (t1, t2) for Shift{lambda} on mesh width h; `smoother` and `omega` where they apply. */
+int pdmg_lfa_symbol(int32_t which, double t1, double t2, pdmg_c128 lambda, double h, int32_t smoother, double omega,
+                    pdmg_c128* out);
+/* smoothing_factor (lfa.hpp:62-63): mu and its first sampled maximizer argmax[2] (may be NULL). */
+int pdmg_lfa_smoothing_factor(pdmg_c128 lambda, double h, int32_t smoother, double omega, const pdmg_lfa_config* lfa,
+                              int32_t device, double* mu, double* argmax);
+/* smoothing_factor_bound (lfa.hpp:69-75): phi[0] = phi_base, phi[1] = phi_shift (Vanka). */
+int pdmg_lfa_smoothing_bound(pdmg_c128 lambda, double h, double omega, const pdmg_lfa_config* lfa, int32_t device,
+                             double* phi);
+/* TwoGridModel (lfa.hpp:77-96), symbol caches in device memory. */
+typedef struct pdmg_lfa_model pdmg_lfa_model;
+int pdmg_lfa_model_create(pdmg_c128 lambda, double h, int32_t smoother, const pdmg_lfa_config* lfa, int32_t device,
+                          pdmg_lfa_model** out);
+void pdmg_lfa_model_destroy(pdmg_lfa_model* model);
+int pdmg_lfa_model_skipped(const pdmg_lfa_model* model);
+/* rho[k] = TwoGridModel::rho(omegas[k], nu) for k < count (one launch for the whole batch). */
+int pdmg_lfa_model_rho(pdmg_lfa_model* model, int32_t count, const double* omegas, int32_t nu, double* rho);
+/* TwoGridModel::smoothing(omega): mu and argmax[2] (may be NULL). */
+int pdmg_lfa_model_smoothing(pdmg_lfa_model* model, double omega, double* mu, double* argmax);
+/* optimize_omega(model, objective, nu) (lfa.hpp:112-113). */
+int pdmg_lfa_optimize_omega(pdmg_lfa_model* model, int32_t objective, int32_t nu, double* omega, double* value);
+/* optimize_omega(shift, h, kind, SmoothingMu) without a two-grid model (lfa.cpp:231-246). */
+int pdmg_lfa_optimize_omega_smoothing(pdmg_c128 lambda, double h, int32_t smoother, const pdmg_lfa_config* lfa,
+                                      int32_t device, double* omega, double* value);
+
 /* Host helpers (no GPU needed). */
 /* tools/pdmg.cpp:137-147 random_rhs: std::mt19937(seed), uniform_real_distribution<double>(lo,hi),
  * re then im per node; `count` complex values. */

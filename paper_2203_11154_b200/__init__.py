@@ -12,7 +12,10 @@ from .paradiag import (ParadiagCirculant, ParadiagGeneral, TimeDiagonalization, 
                        manufactured_field,
                        paradiag_solve, time_stepping_matrix)
 
+from . import lfa  # noqa: E402
+
 __all__ = [
+    "lfa",
     "ParadiagCirculant", "ParadiagGeneral", "diagonalize_qbv_closed_form", "TimeDiagonalization", "TimeDiscretization", "TimeSchemeKind", "all_at_once_apply",
     "diagonalize_time_matrix", "helmholtz_shifts", "manufactured_field", "paradiag_solve", "time_stepping_matrix",
     "BatchedMultigridHierarchy", "ConfigError", "CycleKind", "DeviceError", "Grid2D", "MultigridConfig",

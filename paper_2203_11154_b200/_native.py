@@ -30,6 +30,16 @@ class BatchDesc(C.Structure):
                 ("precision", C.c_int32), ("device", C.c_int32), ("devices", C.c_void_p), ("n_devices", C.c_int32)]
 
 
+class C128(C.Structure):
+    """pdmg_c128 (layout of std::complex<double>); passed by value in two SSE registers like the C struct."""
+
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+class LfaConfig(C.Structure):
+    _fields_ = [("samples_per_dim", C.c_int32), ("coarse_skip_tol", C.c_double)]
+
+
 class SolveReport(C.Structure):
     _fields_ = [("iterations", C.c_void_p), ("converged", C.c_void_p), ("residual_history", C.c_void_p),
                 ("rate", C.c_void_p), ("seconds", C.c_double)]
@@ -89,6 +99,19 @@ def lib() -> C.CDLL:
                                             C.POINTER(SolveReport), C.POINTER(f64)]),
         "pdmg_time_transform": (C.c_int, [i32, i32, i64, vp, vp, vp, vp]),
         "pdmg_aao_residual": (C.c_int, [i32, i32, i32, i32, f64, f64, vp, vp, vp, C.POINTER(f64), vp]),
+        "pdmg_lfa_config_default": (None, [C.POINTER(LfaConfig)]),
+        "pdmg_lfa_symbol": (C.c_int, [i32, f64, f64, C128, f64, i32, f64, C.POINTER(C128)]),
+        "pdmg_lfa_smoothing_factor": (C.c_int, [C128, f64, i32, f64, C.POINTER(LfaConfig), i32, C.POINTER(f64),
+                                                C.POINTER(f64)]),
+        "pdmg_lfa_smoothing_bound": (C.c_int, [C128, f64, f64, C.POINTER(LfaConfig), i32, C.POINTER(f64)]),
+        "pdmg_lfa_model_create": (C.c_int, [C128, f64, i32, C.POINTER(LfaConfig), i32, C.POINTER(vp)]),
+        "pdmg_lfa_model_destroy": (None, [vp]),
+        "pdmg_lfa_model_skipped": (C.c_int, [vp]),
+        "pdmg_lfa_model_rho": (C.c_int, [vp, i32, C.POINTER(f64), i32, C.POINTER(f64)]),
+        "pdmg_lfa_model_smoothing": (C.c_int, [vp, f64, C.POINTER(f64), C.POINTER(f64)]),
+        "pdmg_lfa_optimize_omega": (C.c_int, [vp, i32, i32, C.POINTER(f64), C.POINTER(f64)]),
+        "pdmg_lfa_optimize_omega_smoothing": (C.c_int, [C128, f64, i32, C.POINTER(LfaConfig), i32, C.POINTER(f64),
+                                                        C.POINTER(f64)]),
         "pdmg_random_rhs": (None, [C.c_uint32, f64, f64, i64, vp]),
         "pdmg_circulant_shifts": (None, [f64, i32, f64, i32, i32, vp]),
         "pdmg_host_alloc": (vp, [C.c_size_t]),

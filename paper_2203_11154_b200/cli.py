@@ -141,10 +141,9 @@ def open_out(path):
 
 
 def qbv_eigenvalues(n: int, tau: float, beta: float) -> np.ndarray:
-    """diagonalize_qbv_closed_form eigenvalue order (paradiag.cpp:204-228): (1 - gamma zeta^{-k}) / tau."""
-    m = n + 1
-    gr, ga, wa = (1.0 / beta) ** (1.0 / m), math.pi / m, 2.0 * math.pi / m
-    return np.array([(1.0 - gr * np.exp(1j * (ga - wa * k))) / tau for k in range(m)])
+    """diagonalize_qbv_closed_form eigenvalue order (paradiag.cpp:84-108): (1 - gamma zeta^{-k}) / tau."""
+    return PD.diagonalize_qbv_closed_form(PD.TimeDiscretization(PD.TimeSchemeKind.BackwardHeatQBV, n, tau,
+                                                                beta)).eigenvalues
 
 
 def scheme_shifts(scheme: str, n: int, beta: float) -> np.ndarray:
@@ -196,6 +195,45 @@ def cmd_solve(a) -> int:
         os.close()
     sys.stderr.write(f"solve: converged={bool_str(rep.converged)} iterations={rep.iterations} "
                      f"rate={format_sig(rep.rate)} seconds={format_sig(rep.seconds)}\n")
+    return EXIT_OK
+
+
+def cmd_lfa_table(a) -> int:
+    """lfa-table (pdmg.cpp:153-220): optimized damping, smoothing factor and two-grid factors rho(1..nu_max) per
+    smoother for the first eigenvalue shift of the time scheme, from the GPU LFA kernels."""
+    from . import lfa as LFA
+
+    N_ = parse_reciprocal(a.h)
+    n = parse_reciprocal(a.tau or a.h)
+    shift = complex(scheme_shifts(a.scheme, n, a.beta)[0])
+    if a.nu_max < 1:
+        raise M.ConfigError("--nu-max must be positive")
+    kinds = [parse_smoother(s) for s in a.smoothers.split(",") if s]
+    if not kinds:
+        raise M.ConfigError("--smoothers: empty list")
+    cfg = LFA.LFAConfig(a.samples, 1e-8)
+    cfg.validate()
+    m = RunManifest("lfa-table")
+    m.add("h", f"1/{N_}")
+    m.add("tau", f"1/{n}")
+    m.add("scheme", a.scheme)
+    if a.scheme == "backward-heat":
+        m.add("beta", format_sig(a.beta))
+    m.add("lambda_re", format_sig(shift.real))
+    m.add("lambda_im", format_sig(shift.imag))
+    m.add("samples", str(a.samples))
+    m.add("nu_max", str(a.nu_max))
+    os = open_out(a.out)
+    csv = CsvWriter(os, m, ["smoother", "omega_opt", "mu"] + [f"rho_nu{nu}" for nu in range(1, a.nu_max + 1)])
+    for kind in kinds:
+        model = LFA.TwoGridModel(shift, 1.0 / N_, kind, cfg, a.device)
+        opt = LFA.optimize_omega(model, LFA.OmegaObjective.TwoGridRho, 1)
+        name = "vanka" if kind == M.SmootherKind.Vanka else "jacobi"
+        csv.row([name, format_sig(opt.omega), format_sig(model.smoothing(opt.omega).mu)]
+                + [format_sig(model.rho(opt.omega, nu)) for nu in range(1, a.nu_max + 1)])
+        sys.stderr.write(f"lfa-table: {name} omega_opt={format_sig(opt.omega)} rho1={format_sig(opt.value)}\n")
+    if os is not sys.stdout:
+        os.close()
     return EXIT_OK
 
 
@@ -308,6 +346,17 @@ def build_parser():
     s.add_argument("--seed", type=int, default=1234)
     add_cycle_opts(s)
     s.set_defaults(fn=cmd_solve)
+    t = sub.add_parser("lfa-table", help="Predicted smoothing/two-grid factors with optimized damping")
+    t.add_argument("--h", default="1/256")
+    t.add_argument("--tau")
+    t.add_argument("--scheme", default="heat-bvm", choices=["heat-bvm", "backward-heat"])
+    t.add_argument("--beta", type=float, default=0.01)
+    t.add_argument("--smoothers", default="vanka,jacobi")
+    t.add_argument("--nu-max", type=int, default=4)
+    t.add_argument("--samples", type=int, default=64)
+    t.add_argument("-o", "--out", default="-")
+    t.add_argument("--device", type=int, default=0, help="CUDA device (B200 extension)")
+    t.set_defaults(fn=cmd_lfa_table)
     w = sub.add_parser("sweep", help="Solve across a family of shifts and tabulate iterations/rates")
     w.add_argument("--example", required=True, choices=["heat", "backward-heat", "helmholtz"])
     w.add_argument("--h", required=True)

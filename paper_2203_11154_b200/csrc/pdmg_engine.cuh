@@ -1046,7 +1046,37 @@ struct Engine : EngineBase {
       if (cudaPointerGetAttributes(&a, p) != cudaSuccess) return (cudaGetLastError(), false);
       return a.type == cudaMemoryTypeHost;
     };
-    if (nch > 1 && !(pinned(b) && pinned(u))) nch = 1;  // pageable copies are host-synchronous: no overlap
+    if (nch > 1 && !(pinned(b) && pinned(u))) {
+      // Pageable caller buffers (a std::vector through the C++ facade): page-lock them for the duration of the
+      // call so the copies run as DMA and overlap the chunked solves (cudaHostRegister / Unregister); a
+      // pageable copy is host-synchronous and would serialize the pipeline.  PDMG_PAGEABLE=0: plain copies.
+      static const bool reg_on = [] {
+        const char* e = std::getenv("PDMG_PAGEABLE");
+        return !(e && std::atoi(e) == 0);
+      }();
+      const size_t bytes = N * sizeof(double2);
+      if (reg_on) {
+        struct Reg {
+          const void* p = nullptr;
+          ~Reg() {
+            if (p) cudaHostUnregister(const_cast<void*>(p));
+          }
+        } rb, ru;
+        if (!pinned(b) && cudaHostRegister(const_cast<pdmg_c128*>(b), bytes, cudaHostRegisterReadOnly) == cudaSuccess)
+          rb.p = b;
+        else
+          (void)cudaGetLastError();
+        if (!pinned(u) && cudaHostRegister(u, bytes, cudaHostRegisterDefault) == cudaSuccess)
+          ru.p = u;
+        else
+          (void)cudaGetLastError();
+        if (pinned(b) && pinned(u)) {
+          solve_host(b, u, rep);
+          return;
+        }
+      }
+      nch = 1;
+    }
     if (nch == 1) {
       h2d(b, st, N);
       solve_device(st, st + N, rep);

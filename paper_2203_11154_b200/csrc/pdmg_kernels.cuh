@@ -86,15 +86,26 @@ __device__ __forceinline__ float2 st2<float2>(double2 v) {
 
 __device__ __forceinline__ double2 csel(bool c, double2 a) { return c ? a : make_double2(0.0, 0.0); }
 // b - (1/h^2)((4+eta) u_c - (u_w + u_e + u_s + u_n)) with dd = (4+eta)/h^2 folded into FMAs
+#ifndef PDMG_RES5_TREE
+#define PDMG_RES5_TREE 0
+#endif
 __device__ __forceinline__ double2 res5(double2 b, double ih2, double2 dd, double2 uc, double2 uw, double2 ue,
                                         double2 us, double2 un) {
   const double sx = (uw.x + ue.x) + (us.x + un.x), sy = (uw.y + ue.y) + (us.y + un.y);
+#if PDMG_RES5_TREE
+  // the centre term and the neighbour sum as independent chains (dependency depth 3 instead of 5)
+  double tx = fma(-dd.x, uc.x, b.x), ty = fma(-dd.x, uc.y, b.y);
+  tx = fma(dd.y, uc.y, tx);
+  ty = fma(-dd.y, uc.x, ty);
+  return make_double2(fma(ih2, sx, tx), fma(ih2, sy, ty));
+#else
   double rx = fma(ih2, sx, b.x), ry = fma(ih2, sy, b.y);
   rx = fma(-dd.x, uc.x, rx);
   rx = fma(dd.y, uc.y, rx);
   ry = fma(-dd.x, uc.y, ry);
   ry = fma(-dd.y, uc.x, ry);
   return make_double2(rx, ry);
+#endif
 }
 // k0 rc + k1 e1 + k2 e2 (complex), as one FMA chain per component
 __device__ __forceinline__ double2 cdot3(double2 k0, double2 rc, double2 k1, double2 e1, double2 k2, double2 e2) {
@@ -113,8 +124,16 @@ __device__ __forceinline__ double2 cdot3(double2 k0, double2 rc, double2 k1, dou
   return make_double2(x, y);
 }
 
-// k0 x + k1 y (complex), one FMA chain per component
+// k0 x + k1 y (complex), one FMA chain per component (PDMG_CMAD_TREE: two chains of two per component)
+#ifndef PDMG_CMAD_TREE
+#define PDMG_CMAD_TREE 0
+#endif
 __device__ __forceinline__ double2 cmad2(double2 k0, double2 x, double2 k1, double2 y) {
+#if PDMG_CMAD_TREE
+  const double ra = fma(-k0.y, x.y, k0.x * x.x), rb = fma(-k1.y, y.y, k1.x * y.x);
+  const double ia = fma(k0.y, x.x, k0.x * x.y), ib = fma(k1.y, y.x, k1.x * y.y);
+  return make_double2(ra + rb, ia + ib);
+#endif
   double re = k0.x * x.x;
   re = fma(-k0.y, x.y, re);
   re = fma(k1.x, y.x, re);
@@ -1440,6 +1459,11 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
 #define PDMG_M2_PF 2
 #endif
   constexpr int M2_PF = PDMG_M2_PF;
+  // L2 prefetch of the coarse-correction row M2_CPF coarse rows ahead (prolongating passes; 0 = none)
+#ifndef PDMG_M2_CPF
+#define PDMG_M2_CPF 2
+#endif
+  constexpr int M2_CPF = PDMG_M2_CPF;
   const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
   const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
@@ -1600,7 +1624,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
       }
       gread_u(j + 1, Unx, MK);
       gload_b(j, Bn, MK);
-      if constexpr (PROLONG) load_coarse(j + 1, MK);
+      if constexpr (PROLONG) {
+        if constexpr (M2_CPF > 0) l2_prefetch(ecs + (int64_t)min((j + 1 + 2 * M2_CPF) >> 1, nc) * nc + Ie);
+        load_coarse(j + 1, MK);
+      }
       if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
       if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
     }

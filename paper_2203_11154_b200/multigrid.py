@@ -364,19 +364,24 @@ class BatchedMultigridHierarchy:
         return float(N.lib().pdmg_last_updates(self._h))
 
     def kernel_stats(self) -> dict[str, dict]:
-        out = {}
-        i = 0
-        name = C.create_string_buffer(128)
-        while True:
-            la, ms, by = C.c_int64(), C.c_double(), C.c_double()
-            if N.lib().pdmg_kernel_stats(self._h, i, name, 128, C.byref(la), C.byref(ms), C.byref(by)):
-                break
-            ub, nu = C.c_double(), C.c_double()
-            N.lib().pdmg_kernel_updates(self._h, i, C.byref(ub), C.byref(nu))
-            out[name.value.decode()] = dict(launches=la.value, ms=ms.value, bytes=by.value, unit_bytes=ub.value,
-                                            updates=nu.value)
-            i += 1
-        return out
+        return kernel_stats(self._h)
+
+
+def kernel_stats(handle) -> dict[str, dict]:
+    """Per-kernel-class CUDA-event stats of a pdmg_ctx (pdmg_kernel_stats / pdmg_kernel_updates)."""
+    out = {}
+    i = 0
+    name = C.create_string_buffer(128)
+    while True:
+        la, ms, by = C.c_int64(), C.c_double(), C.c_double()
+        if N.lib().pdmg_kernel_stats(handle, i, name, 128, C.byref(la), C.byref(ms), C.byref(by)):
+            break
+        ub, nu = C.c_double(), C.c_double()
+        N.lib().pdmg_kernel_updates(handle, i, C.byref(ub), C.byref(nu))
+        out[name.value.decode()] = dict(launches=la.value, ms=ms.value, bytes=by.value, unit_bytes=ub.value,
+                                        updates=nu.value)
+        i += 1
+    return out
 
 
 class MultigridHierarchy:
