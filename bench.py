@@ -607,7 +607,7 @@ def main():
     barrier()
     e_pg = max_over_ranks(time.perf_counter() - t0)
     e2e_pageable = {"value": sum_over_ranks(e_upd) / e_pg, "unit": UNIT, "ms_per_step": 1e3 * e_pg / e_steps,
-                    "buffers": "pageable numpy arrays (page-locked by the library for the call)"}
+                    "buffers": "pageable numpy arrays (through the library's pinned bounce buffers)"}
     del u_np
 
     roofline = roofline_of(stats, args.config, upd / args.steps, nu1 + nu2)

@@ -8,6 +8,9 @@
 // match the reference.
 #pragma once
 #include <array>
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 
 #include "pdmg_host.h"
@@ -1046,36 +1049,17 @@ struct Engine : EngineBase {
       if (cudaPointerGetAttributes(&a, p) != cudaSuccess) return (cudaGetLastError(), false);
       return a.type == cudaMemoryTypeHost;
     };
+    // pageable caller buffers (a std::vector through the C++ facade): the chunked pipeline through the library's
+    // pinned bounce buffers (a pageable cudaMemcpy is host-synchronous and would serialize it; page-locking the
+    // caller's 2 GB per call measured 2.7x slower than this at C3).  PDMG_PAGEABLE=0: plain copies.
+    bool staged = false;
     if (nch > 1 && !(pinned(b) && pinned(u))) {
-      // Pageable caller buffers (a std::vector through the C++ facade): page-lock them for the duration of the
-      // call so the copies run as DMA and overlap the chunked solves (cudaHostRegister / Unregister); a
-      // pageable copy is host-synchronous and would serialize the pipeline.  PDMG_PAGEABLE=0: plain copies.
-      static const bool reg_on = [] {
+      static const bool stage_on = [] {
         const char* e = std::getenv("PDMG_PAGEABLE");
         return !(e && std::atoi(e) == 0);
       }();
-      const size_t bytes = N * sizeof(double2);
-      if (reg_on) {
-        struct Reg {
-          const void* p = nullptr;
-          ~Reg() {
-            if (p) cudaHostUnregister(const_cast<void*>(p));
-          }
-        } rb, ru;
-        if (!pinned(b) && cudaHostRegister(const_cast<pdmg_c128*>(b), bytes, cudaHostRegisterReadOnly) == cudaSuccess)
-          rb.p = b;
-        else
-          (void)cudaGetLastError();
-        if (!pinned(u) && cudaHostRegister(u, bytes, cudaHostRegisterDefault) == cudaSuccess)
-          ru.p = u;
-        else
-          (void)cudaGetLastError();
-        if (pinned(b) && pinned(u)) {
-          solve_host(b, u, rep);
-          return;
-        }
-      }
-      nch = 1;
+      if (stage_on && io_mode == 1) staged = true;
+      else nch = 1;
     }
     if (nch == 1) {
       h2d(b, st, N);
@@ -1086,7 +1070,7 @@ struct Engine : EngineBase {
     }
     const auto t0 = std::chrono::steady_clock::now();
     if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-    if (io_mode == 1 && solve_concurrent(b, u, rep, st, N, per)) {
+    if (io_mode == 1 && solve_concurrent(b, u, rep, st, N, per, staged)) {
       if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       return;
     }
@@ -1137,7 +1121,124 @@ struct Engine : EngineBase {
   // Concurrent host pipeline: all H2D copies queue on the copy stream in chunk order; chunk c's host thread
   // waits for its copy, solves on its sub-engine's stream and queues its own D2H there.  Every shift's solve
   // is independent, so the results are bitwise those of one batch (test_chunked_host_solve_matches).
-  bool solve_concurrent(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep, double2* st, size_t N, int64_t per) {
+  // Pageable host buffers go through pinned bounce buffers (the library's own): multi-threaded host copies into
+  // a ring of pinned pieces, each piece's DMA queued as soon as it is filled; the output the same way back.
+  static constexpr size_t kStagePiece = (size_t)32 << 20;  // bytes per bounce piece
+  static constexpr int kStageRing = 4;                      // input pieces in flight
+  struct Bounce {
+    void* buf[kStageRing] = {};
+    cudaEvent_t ev[kStageRing] = {};
+    int n = 0;
+    void ensure(int count) {
+      for (; n < count; ++n) {
+        CK(cudaMallocHost(&buf[n], kStagePiece));
+        CK(cudaEventCreateWithFlags(&ev[n], cudaEventDisableTiming));
+      }
+    }
+    ~Bounce() {
+      for (int i = 0; i < n; ++i) cudaFreeHost(buf[i]), cudaEventDestroy(ev[i]);
+    }
+  };
+  std::unique_ptr<Bounce> bounce_in, bounce_out;
+  // Host copies of the bounce pipeline run on one persistent pool of worker threads shared by the input and all
+  // output streams (no per-piece thread creation, no oversubscription of the host cores).
+  struct CopyPool {
+    std::mutex mu;
+    std::condition_variable cv;
+    struct Task {
+      void* dst;
+      const void* src;
+      size_t len;
+      std::atomic<int>* left;
+    };
+    std::vector<Task> q;
+    std::vector<std::thread> th;
+    bool stop = false;
+    explicit CopyPool(int n) {
+      for (int i = 0; i < n; ++i)
+        th.emplace_back([this] {
+          for (;;) {
+            Task t;
+            {
+              std::unique_lock<std::mutex> lk(mu);
+              cv.wait(lk, [&] { return stop || !q.empty(); });
+              if (stop && q.empty()) return;
+              t = q.back();
+              q.pop_back();
+            }
+            std::memcpy(t.dst, t.src, t.len);
+            t.left->fetch_sub(1, std::memory_order_acq_rel);
+          }
+        });
+    }
+    ~CopyPool() {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+      }
+      cv.notify_all();
+      for (auto& x : th) x.join();
+    }
+    static CopyPool& get() {
+      static CopyPool pool(std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2)));
+      return pool;
+    }
+  };
+  static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t slice = (size_t)2 << 20;
+    if (bytes <= slice) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    CopyPool& P = CopyPool::get();
+    std::atomic<int> left{0};
+    {
+      std::lock_guard<std::mutex> lk(P.mu);
+      for (size_t o = 0; o < bytes; o += slice) {
+        P.q.push_back({(char*)dst + o, (const char*)src + o, std::min(slice, bytes - o), &left});
+        left.fetch_add(1, std::memory_order_relaxed);
+      }
+    }
+    P.cv.notify_all();
+    while (left.load(std::memory_order_acquire) > 0) std::this_thread::yield();
+  }
+  // host -> device through the input ring (on `st_`); returns after the last piece's DMA is queued
+  void staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st_) {
+    Bounce& B = *bounce_in;
+    static thread_local int slot = 0;
+    for (size_t o = 0; o < bytes; o += kStagePiece) {
+      const size_t len = std::min(kStagePiece, bytes - o);
+      const int k = slot++ % kStageRing;
+      CK(cudaEventSynchronize(B.ev[k]));  // the piece's previous DMA has drained
+      parallel_memcpy(B.buf[k], (const char*)src + o, len);
+      CK(cudaMemcpyAsync((char*)dst + o, B.buf[k], len, cudaMemcpyHostToDevice, st_));
+      CK(cudaEventRecord(B.ev[k], st_));
+    }
+  }
+  // device -> host through two pinned pieces owned by the calling sub-engine (double-buffered)
+  void staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st_, Bounce& B) {
+    int k = 0;
+    size_t pend_o = 0, pend_len = 0;
+    int pend_k = -1;
+    for (size_t o = 0; o < bytes; o += kStagePiece) {
+      const size_t len = std::min(kStagePiece, bytes - o);
+      CK(cudaMemcpyAsync(B.buf[k], (const char*)src + o, len, cudaMemcpyDeviceToHost, st_));
+      CK(cudaEventRecord(B.ev[k], st_));
+      if (pend_k >= 0) {  // drain the previous piece while this one transfers
+        CK(cudaEventSynchronize(B.ev[pend_k]));
+        parallel_memcpy((char*)dst + pend_o, B.buf[pend_k], pend_len);
+      }
+      pend_k = k, pend_o = o, pend_len = len;
+      k ^= 1;
+    }
+    if (pend_k >= 0) {
+      CK(cudaEventSynchronize(B.ev[pend_k]));
+      parallel_memcpy((char*)dst + pend_o, B.buf[pend_k], pend_len);
+    }
+  }
+
+  bool solve_concurrent(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep, double2* st, size_t N, int64_t per,
+                        bool staged = false) {
     // automatic: six chunks weighted 1,2,2,2,2,1 -- half-size first and last chunks shorten the exposed fill
     // (first H2D) and drain (last D2H); measured on B200 (C3): 45.9 ms vs 47.4 (1,2,2,2,1), 48.1 (8 equal),
     // 49.4 (1,3,3,1) and 51.4 for the one-stream three-chunk pipeline (io_mode 0)
@@ -1180,11 +1281,45 @@ struct Engine : EngineBase {
     };
     std::vector<cudaEvent_t> t_in(nch), t_sol(nch), t_out(nch);
     cudaEvent_t t_start = dbg ? tevent(copy_stream) : nullptr;
-    for (int c = 0; c < nch; ++c) {
-      CK(cudaEventCreateWithFlags(&in[c], dbg ? 0 : cudaEventDisableTiming));
-      CK(cudaMemcpyAsync(st + lo[c] * per, b + lo[c] * per, sizeof(double2) * per * (lo[c + 1] - lo[c]),
-                         cudaMemcpyHostToDevice, copy_stream));
-      CK(cudaEventRecord(in[c], copy_stream));
+    for (int c = 0; c < nch; ++c) CK(cudaEventCreateWithFlags(&in[c], dbg ? 0 : cudaEventDisableTiming));
+    // staged input: an input thread fills the bounce ring chunk by chunk; chunk c's solve waits (on the host) until
+    // in[c] is recorded, then (on its stream) for the copy itself
+    std::mutex in_mu;
+    std::condition_variable in_cv;
+    int in_ready = 0;
+    std::exception_ptr in_err;
+    std::thread in_thread;
+    if (staged) {
+      if (!bounce_in) bounce_in = std::make_unique<Bounce>();
+      bounce_in->ensure(kStageRing);
+      for (auto& e : subs) {
+        if (!e->bounce_out) e->bounce_out = std::make_unique<Bounce>();
+        e->bounce_out->ensure(2);
+      }
+      in_thread = std::thread([&] {
+        try {
+          CK(cudaSetDevice(device));
+          for (int c = 0; c < nch; ++c) {
+            staged_h2d(st + lo[c] * per, b + lo[c] * per, sizeof(double2) * per * (lo[c + 1] - lo[c]), copy_stream);
+            CK(cudaEventRecord(in[c], copy_stream));
+            std::lock_guard<std::mutex> lk(in_mu);
+            in_ready = c + 1;
+            in_cv.notify_all();
+          }
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(in_mu);
+          in_err = std::current_exception();
+          in_ready = nch;
+          in_cv.notify_all();
+        }
+      });
+    } else {
+      for (int c = 0; c < nch; ++c) {
+        CK(cudaMemcpyAsync(st + lo[c] * per, b + lo[c] * per, sizeof(double2) * per * (lo[c + 1] - lo[c]),
+                           cudaMemcpyHostToDevice, copy_stream));
+        CK(cudaEventRecord(in[c], copy_stream));
+      }
+      in_ready = nch;
     }
     const int H = cfg.max_iter + 1;
     std::vector<std::exception_ptr> err(nch);
@@ -1195,6 +1330,11 @@ struct Engine : EngineBase {
           Engine<T>& e = *subs[c];
           CK(cudaSetDevice(device));
           const int s0 = lo[c], cnt = lo[c + 1] - lo[c];
+          {
+            std::unique_lock<std::mutex> lk(in_mu);
+            in_cv.wait(lk, [&] { return in_ready > c; });
+            if (in_err) return;
+          }
           CK(cudaStreamWaitEvent(e.stream, in[c], 0));
           pdmg_solve_report rc{};
           if (rep) {
@@ -1205,8 +1345,12 @@ struct Engine : EngineBase {
           }
           e.solve_device(st + s0 * per, st + N + s0 * per, rep ? &rc : nullptr);
           if (dbg) t_sol[c] = tevent(e.stream);
-          CK(cudaMemcpyAsync(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * cnt, cudaMemcpyDeviceToHost,
-                             e.stream));
+          if (staged) {
+            staged_d2h(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * cnt, e.stream, *e.bounce_out);
+          } else {
+            CK(cudaMemcpyAsync(u + s0 * per, st + N + s0 * per, sizeof(double2) * per * cnt, cudaMemcpyDeviceToHost,
+                               e.stream));
+          }
           if (dbg) t_out[c] = tevent(e.stream);
           CK(cudaStreamSynchronize(e.stream));
         } catch (...) {
@@ -1215,6 +1359,8 @@ struct Engine : EngineBase {
       });
     }
     for (auto& t : th) t.join();
+    if (in_thread.joinable()) in_thread.join();
+    if (in_err) std::rethrow_exception(in_err);
     if (dbg) {
       for (int c = 0; c < nch; ++c) {
         float a = 0, b2 = 0, c2 = 0;

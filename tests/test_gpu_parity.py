@@ -437,3 +437,31 @@ def test_device_list_matches_single_device(oracle):
 def test_device_list_bad_device_is_device_error():
     with pytest.raises(P.DeviceError, match="not available"):
         P.BatchedMultigridHierarchy(P.Grid2D(16), [0.0, 1.0], P.MultigridConfig(), devices=[0, 97])
+
+
+def test_pageable_host_solve_staged_matches(oracle, monkeypatch):
+    """Pageable host buffers on the chunked pipeline go through the library's pinned bounce buffers (32 MB pieces,
+    multi-threaded host copies, DMA queued per piece): bitwise the plain-copy result.  83 MB per array here, so
+    every direction crosses several pieces and the input ring wraps."""
+    n, m, S = 512, 511, 20
+    lams = oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, S)
+    cfg = mgcfg(Cfg(nu1=2, nu2=2))
+    b = P.random_rhs(n, 7, count=S)
+    monkeypatch.setenv("PDMG_IO_CHUNKS", "3")
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        u1, r1 = H.solve(b)  # pageable numpy arrays -> staged pipeline
+    monkeypatch.setenv("PDMG_PAGEABLE", "0")
+    import subprocess
+    import sys
+    # PDMG_PAGEABLE is read once per process: the plain-copy reference runs in a child process
+    code = ("import numpy as np, sys; sys.path.insert(0, %r); import paper_2203_11154_b200 as P; "
+            "lams = P.circulant_shifts(1e-3, 256, 1/256, 0, 20); "
+            "cfg = P.MultigridConfig(P.CycleKind.V, 2, 2, 4, 1e-10, 200, P.SmootherConfig.vanka()); "
+            "b = P.random_rhs(512, 7, count=20); H = P.BatchedMultigridHierarchy(P.Grid2D(512), lams, cfg); "
+            "u, r = H.solve(b); np.save('/tmp/pdmg_plain_u.npy', u); "
+            "np.save('/tmp/pdmg_plain_it.npy', np.array([x.iterations for x in r]))" % P.__path__[0].rsplit('/', 1)[0])
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=600)
+    assert np.array_equal(u1, np.load("/tmp/pdmg_plain_u.npy"))
+    assert [x.iterations for x in r1] == np.load("/tmp/pdmg_plain_it.npy").tolist()
+    ref = oracle.solve_batch(n, lams[:2], Cfg(nu1=2, nu2=2), b[:2], threads=2)
+    assert rel(u1[:2], ref["u"]) < 1e-10
