@@ -16,6 +16,11 @@
 #include "pdmg_host.h"
 #include "pdmg_kernels.cuh"
 
+// compile the hot marching passes with the level's n as a constant (n = 256, 512, 1024; complex128)
+#ifndef PDMG_MARCH2_NF
+#define PDMG_MARCH2_NF 1
+#endif
+
 namespace pdmg_b200 {
 
 // ---------------------------------------------------------------------------------------------
@@ -142,6 +147,26 @@ struct March2Table {
   using Fn = void (*)(MarchArgs<T>, CoefPack);
   Fn e[32] = {};   // two sweeps per pass
   Fn e1[32] = {};  // one sweep per pass (k_march2<..., TWO = false>)
+  // the hot variants with the level's n compiled in (NF): [n = 256, 512, 1024][key]
+  Fn eN[3][32] = {}, e1N[3][32] = {};
+  static int nf_slot(int n) { return n == 256 ? 0 : n == 512 ? 1 : n == 1024 ? 2 : -1; }
+  template <bool LU, bool PR, int PO, bool NI, bool TWO, int NFV>
+  void regN() {
+    (TWO ? eN : e1N)[nf_slot(NFV)][key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI, TWO, NFV>;
+  }
+  template <int NFV>
+  void reg_hot() {
+#if PDMG_MARCH2_NF
+    regN<true, true, POST_NONE, false, true, NFV>();        // prolong+vanka2
+    regN<true, false, POST_RESTRICT, true, true, NFV>();    // vanka2+restrict+norm_in
+    regN<false, false, POST_RESTRICT, true, true, NFV>();   // zero+vanka2+restrict+norm_in
+    regN<false, false, POST_RESTRICT, false, true, NFV>();  // zero+vanka2+restrict (coarse levels)
+    regN<true, true, POST_NONE, false, false, NFV>();       // prolong+vanka (V(1,1))
+    regN<true, false, POST_RESTRICT, true, false, NFV>();   // vanka+restrict+norm_in (V(1,1))
+    regN<false, false, POST_RESTRICT, true, false, NFV>();  // zero+vanka+restrict+norm_in
+    regN<false, false, POST_RESTRICT, false, false, NFV>(); // zero+vanka+restrict
+#endif
+  }
   static int key(bool lu, bool pr, int post, bool nin = false) {
     return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0);
   }
@@ -163,6 +188,11 @@ struct March2Table {
   March2Table() {
     reg_lu<false>();
     reg_lu<true>();
+    if constexpr (std::is_same<T, double>::value) {
+      reg_hot<256>();
+      reg_hot<512>();
+      reg_hot<1024>();
+    }
   }
 };
 
@@ -284,6 +314,10 @@ struct Engine : EngineBase {
     if (ma.ntasks != march2_tasks(Lv.n, post, two, prolong)) throw std::logic_error("pdmg_b200: march2 task count");
     const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
     auto fn = two ? marches2().e[key2] : marches2().e1[key2];
+    if (const int sl = March2Table<T>::nf_slot(Lv.n); sl >= 0) {
+      auto fnN = two ? marches2().eN[sl][key2] : marches2().e1N[sl][key2];
+      if (fnN) fn = fnN;
+    }
     if (!fn) throw std::logic_error("pdmg_b200: no two-sweep kernel for this variant");
     const double S_ = sizeof(V), pts = (double)n_act * Lv.m * Lv.m;
     const double bpp = (loadu ? S_ : 0) + S_ + (prolong ? S_ / 4 : 0) + S_ + (post == POST_RESTRICT ? S_ / 4 : 0);

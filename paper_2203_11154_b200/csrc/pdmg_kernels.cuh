@@ -1438,7 +1438,8 @@ struct IC {
 #ifndef PDMG_MARCH1_MINB
 #define PDMG_MARCH1_MINB 3
 #endif
-template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool TWO = true>
+// NF > 0: the level's subdivision count n as a compile-time constant (row offsets become immediates)
+template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool TWO = true, int NF = 0>
 __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB)
     k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
@@ -1470,12 +1471,12 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   if (task >= a.ntasks) return;
   const int lane = threadIdx.x & 31;
   const int tx = task % a.ntx, ty = task / a.ntx;
-  const int n = a.n, m = n - 1, Hs = a.Hs, nc = a.nc;
+  const int n = NF ? NF : a.n, m = n - 1, Hs = a.Hs, nc = NF ? NF / 2 : a.nc;
   const int x0 = tx * WOUT, r0 = ty * Hs;
-  const int64_t sbase = (int64_t)shift * a.ss;
+  const int64_t sbase = (int64_t)shift * (NF ? (int64_t)(NF + 1) * NF : a.ss);
   const int cA = x0 - hA + LC * lane;
   V* __restrict__ uout = a.u_out + sbase + cA;  // per-lane column pointer (row 0)
-  const V* __restrict__ ecs = a.ec + (int64_t)shift * a.ssc;
+  const V* __restrict__ ecs = a.ec + (int64_t)shift * (NF ? (int64_t)(NF / 2 + 1) * (NF / 2) : a.ssc);
   const LevelCoef cf = coef_of(cp);
 
   bool cin[LC], cst[LC];
