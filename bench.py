@@ -567,6 +567,33 @@ def main():
     iters = [r.iterations for r in reps]
     conv = all(r.converged for r in reps)
 
+    # ---- N > 1 strong scaling: also the weak-scaled companion (every rank solves its own full batch) ----------
+    weak_extra = None
+    if world > 1 and not weak:
+        bw = P.random_rhs(n, seed + 100 * rank, count=S)
+        Hw = P.BatchedMultigridHierarchy(P.Grid2D(n), lams_all, cfg, device=local, precision=args.precision)
+        d_bw = torch.from_numpy(bw.reshape(S, m, m).view(np.float64)).to(f"cuda:{local}")
+        d_uw = torch.empty_like(d_bw)
+        del bw
+        for _ in range(args.warmup):
+            Hw.solve_device(d_bw.data_ptr(), d_uw.data_ptr(), want_reports=False)
+        sw = torch.cuda.ExternalStream(Hw.stream)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sw)
+        upd_w = 0.0
+        for _ in range(args.steps):
+            Hw.solve_device(d_bw.data_ptr(), d_uw.data_ptr(), want_reports=False)
+            upd_w += Hw.last_updates()
+        e1.record(sw)
+        barrier()
+        ms_w = max_over_ranks(e0.elapsed_time(e1))
+        weak_extra = {"value": sum_over_ranks(upd_w) / (ms_w / 1e3), "unit": UNIT, "ms_per_step": ms_w / args.steps,
+                      "workload": f"every rank solves its own {S}-shift batch (rank r: RHS seed {seed} + 100 r)",
+                      "scaling": "weak"}
+        Hw.close()
+        del d_bw, d_uw
+
     # ---- end to end through the host API: pinned host b -> device -> solve -> host u ----------
     import ctypes
 
@@ -642,6 +669,7 @@ def main():
                     "steps": e_steps, "ms_per_step": 1e3 * e_s_max / e_steps,
                     "buffers": "pinned (pdmg_host_alloc)"},
             "e2e_pageable": e2e_pageable,
+            "weak_scaling": weak_extra,
             "gpu_launches": int(launches),
             "roofline": roofline,
             "clocks": clk.summary(),

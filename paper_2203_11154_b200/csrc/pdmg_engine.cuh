@@ -261,14 +261,34 @@ struct Engine : EngineBase {
     return ((two ? 4 : 2) + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;
   }
   int march2_tasks(int n, int post, bool two, bool prolong) const {  // warp tasks per shift of a k_march2 pass
-    const int wout = 64 - 2 * march2_ha(post, two), hs = march2_hs_for(n, prolong);
+    const int wout = 64 - 2 * march2_ha(post, two), hs = march2_hs_for(n, prolong, post, two);
     return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
   }
-  int march2_hs_for(int n, bool prolong) const {
+  static constexpr int kMinStrip = 16;  // smallest strip height the wave model may pick (partial-buffer sizing)
+  int sm_count = 148;
+  // Strip height of a k_march2 pass.  The measured defaults (128 rows for n >= 512, 64 for n = 256, 32 below;
+  // DESIGN 3.2b, at C3's 256 shifts) unless a wave model of the launch finds a clearly shorter pass: a warp marches
+  // Hs + 2 hA rows, CTAs of MARCH_WARPS strips run in waves of (SMs x resident CTAs), and the pass takes about
+  // waves x (Hs + 2 hA) row steps.  Small batches (strong scaling: 32 shifts per GPU) leave the default's last wave
+  // nearly empty; shorter strips fill it (C3 with 32 shifts: n = 512 passes at Hs = 96 instead of 128).
+  int march2_hs_for(int n, bool prolong, int post = POST_NONE, bool two = true) const {
     if (march2_hs > 0) return march2_hs;
     for (auto& e : prolong ? march2_hs_p : march2_hs_r)
       if (e.first == n) return e.second;
-    return n >= 512 ? 128 : n >= 256 ? 64 : 32;  // measured at C3 (DESIGN 3.2b)
+    const int def = n >= 512 ? 128 : n >= 256 ? 64 : 32;
+    const int ha = march2_ha(post, two), ntx = (n + 63 - 2 * ha) / (64 - 2 * ha);
+    const int64_t slots = (int64_t)sm_count * (two ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB);
+    auto cost = [&](int hs) {
+      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + MARCH_WARPS - 1) / MARCH_WARPS) * S;
+      return (double)((ctas + slots - 1) / slots) * (hs + 2 * ha);
+    };
+    int best = def;
+    double bc = 0.95 * cost(def);  // the default keeps a 5% preference (it is the measured optimum at C3)
+    for (int hs = kMinStrip; hs <= 256 && hs <= n + (n & 1); hs += 8) {
+      const double c = cost(hs);
+      if (c < bc) best = hs, bc = c;
+    }
+    return best;
   }
   bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
   int march2_loopb_min_n = 128;  // (prolongating passes: shape (a), see march2_prolong_b)
@@ -306,7 +326,7 @@ struct Engine : EngineBase {
     ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
     ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
     const int wout = 64 - 2 * march2_ha(post, two);
-    ma.Hs = march2_hs_for(Lv.n, prolong);
+    ma.Hs = march2_hs_for(Lv.n, prolong, post, two);
     // loop shape (a) for prolongating passes unless march2_prolong_b (measured, DESIGN 3.2b)
     ma.loop_a = Lv.n < march2_loopb_min_n || (prolong && !march2_prolong_b);
     ma.ntx = (Lv.n + wout - 1) / wout;
@@ -449,6 +469,7 @@ struct Engine : EngineBase {
     if (dev < 0 || dev >= ndev) throw CudaError("pdmg_create: CUDA device " + std::to_string(dev) + " not available");
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, stream_priority));
+    CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
     table = &kernels();
     const int L = (int)ln.size();
     lv.resize(L);
@@ -543,8 +564,11 @@ struct Engine : EngineBase {
       maxtiles = std::max(maxtiles, lv[l].ntiles);
       for (int post : {POST_NONE, POST_NORM, POST_RESTRICT}) {
         maxtiles = std::max(maxtiles, march_tasks((int)l, post));
-        for (int two = 0; two < 2; ++two)
-          for (int pr = 0; pr < 2; ++pr) maxtiles = std::max(maxtiles, march2_tasks(lv[l].n, post, two != 0, pr != 0));
+        for (int two = 0; two < 2; ++two) {  // (any strip height the wave model may pick, any batch size)
+          const int n = lv[l].n, wout = 64 - 2 * march2_ha(post, two != 0);
+          maxtiles = std::max(maxtiles, ((n + wout - 1) / wout) * ((n + kMinStrip - 1) / kMinStrip));
+          for (int pr = 0; pr < 2; ++pr) maxtiles = std::max(maxtiles, march2_tasks(n, post, two != 0, pr != 0));
+        }
       }
       maxtiles = std::max(maxtiles, (lv[l].n - 1 + RN_ROWS - 1) / RN_ROWS);  // k_resid_norm
     }
