@@ -204,6 +204,7 @@ struct Engine : EngineBase {
     int n = 0, m = 0;
     int64_t ss = 0;  // shift stride (elements)
     size_t elems = 0;
+    int64_t alloc_left = 0;  // elements from this view's start to the end of the allocation (bounds checks)
     V* u[2] = {nullptr, nullptr};
     V* b = nullptr;
     int ntx = 0, nty = 0, ntiles = 0, H = 0;
@@ -279,7 +280,8 @@ struct Engine : EngineBase {
     const int ha = march2_ha(post, two), ntx = (n + 63 - 2 * ha) / (64 - 2 * ha);
     const int64_t slots = (int64_t)sm_count * (two ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB);
     auto cost = [&](int hs) {
-      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + MARCH_WARPS - 1) / MARCH_WARPS) * S;
+      const int wpc = march2_wpc(two);
+      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + wpc - 1) / wpc) * S;
       return (double)((ctas + slots - 1) / slots) * (hs + 2 * ha);
     };
     int best = def;
@@ -325,6 +327,7 @@ struct Engine : EngineBase {
     ma.coef = Lv.coef, ma.active = active, ma.n = Lv.n;
     ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
     ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
+    ma.elems = Lv.alloc_left, ma.elems_c = (l + 1 < (int)lv.size()) ? lv[l + 1].alloc_left : 0;
     const int wout = 64 - 2 * march2_ha(post, two);
     ma.Hs = march2_hs_for(Lv.n, prolong, post, two);
     // loop shape (a) for prolongating passes unless march2_prolong_b (measured, DESIGN 3.2b)
@@ -349,8 +352,9 @@ struct Engine : EngineBase {
       for (int c0 = 0; c0 < S; c0 += COEF_MAX) {  // one launch per COEF_MAX shifts (coefficients as parameters)
         const int cnt = std::min(COEF_MAX, S - c0);
         fill_pack(Lv, c0, cnt);
-        dim3 grid((ma.ntasks + MARCH_WARPS - 1) / MARCH_WARPS, cnt);
-        fn<<<grid, 32 * MARCH_WARPS, 0, stream>>>(ma, *cpack);
+        const int wpc = march2_wpc(two);
+        dim3 grid((ma.ntasks + wpc - 1) / wpc, cnt);
+        fn<<<grid, 32 * wpc, 0, stream>>>(ma, *cpack);
       }
     }, pts * ubpp, (two ? 2 : 1) * pts);
     last_partials = ma.ntasks;
@@ -486,7 +490,9 @@ struct Engine : EngineBase {
         const int64_t off = (int64_t)borrow_s0 * Lv.ss;
         Lv.u[0] = P.u[0] + off, Lv.u[1] = P.u[1] + off, Lv.b = P.b + off;
         if (borrow_s0 + S < borrow->S) Lv.elems = (size_t)Lv.ss * S;
+        Lv.alloc_left = P.alloc_left - off;
       } else {
+        Lv.alloc_left = (int64_t)Lv.elems;
         for (V** p : {&Lv.u[0], &Lv.u[1], &Lv.b}) {
           CK(cudaMalloc(p, Lv.elems * sizeof(V)));
           CK(cudaMemsetAsync(*p, 0, Lv.elems * sizeof(V), stream));
@@ -1012,6 +1018,7 @@ struct Engine : EngineBase {
     std::vector<std::array<V*, 3>> saved_lv;
     std::vector<LevelCoef*> saved_coef;
     std::vector<size_t> saved_elems;
+    std::vector<int64_t> saved_left;
     double2* ainv;
     int *act, *it, *cv, *ones;
     double *r0, *hist;
@@ -1021,6 +1028,8 @@ struct Engine : EngineBase {
         saved_coef.push_back(L.coef);
         saved_elems.push_back(L.elems);
         L.u[0] += s0 * L.ss, L.u[1] += s0 * L.ss, L.b += s0 * L.ss, L.coef += s0;
+        saved_left.push_back(L.alloc_left);
+        L.alloc_left -= (int64_t)s0 * L.ss;
         L.elems = (size_t)L.ss * cnt + (s0 + cnt == en.S ? L.n + 2 : 0);
       }
       ainv = e.d_ainv, act = e.d_active, it = e.d_iters, cv = e.d_conv, ones = e.d_ones, r0 = e.d_r0, hist = e.d_hist;
@@ -1033,7 +1042,7 @@ struct Engine : EngineBase {
     ~RangeView() {
       for (size_t l = 0; l < e.lv.size(); ++l) {
         e.lv[l].u[0] = saved_lv[l][0], e.lv[l].u[1] = saved_lv[l][1], e.lv[l].b = saved_lv[l][2];
-        e.lv[l].coef = saved_coef[l], e.lv[l].elems = saved_elems[l];
+        e.lv[l].coef = saved_coef[l], e.lv[l].elems = saved_elems[l], e.lv[l].alloc_left = saved_left[l];
       }
       e.d_ainv = ainv, e.d_active = act, e.d_iters = it, e.d_conv = cv, e.d_ones = ones, e.d_r0 = r0, e.d_hist = hist;
       e.S = S0;

@@ -1129,6 +1129,13 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
 namespace pdmg_b200 {
 
 constexpr int MARCH_WARPS = 4;  // warps per CTA (independent)
+// warps per CTA of the two-sweep marching passes (k_march2<TWO>); their registers (~236 per thread) allow 8.7 warps
+// per SM, so 3-warp CTAs at 3 per SM would hold 9
+#ifndef PDMG_M2_WPC
+#define PDMG_M2_WPC 4
+#endif
+constexpr int M2_WPC = PDMG_M2_WPC;
+__host__ __device__ constexpr int march2_wpc(bool two) { return two ? M2_WPC : MARCH_WARPS; }
 
 __device__ __forceinline__ double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
@@ -1151,6 +1158,8 @@ struct MarchArgs {
   int n, nc;
   int64_t ss, ssc;
   int ntx, ntasks, Hs;  // strips across, warp tasks per shift, strip height
+  int64_t elems, elems_c;  // elements from u_in / b / u_out (and ec / bc) to the end of their allocations
+                           // (PDMG_BOUNDS_CHECK builds assert every k_march2 access against them)
   int loop_a;           // k_march2 loop shape (see there)
 };
 
@@ -1438,9 +1447,23 @@ struct IC {
 #ifndef PDMG_MARCH1_MINB
 #define PDMG_MARCH1_MINB 3
 #endif
+// Debug builds (-DPDMG_BOUNDS_CHECK=1, compute-sanitizer being closed on this pool): every global access of the
+// marching pass is checked against its allocation and traps with the offending index.
+#ifndef PDMG_BOUNDS_CHECK
+#define PDMG_BOUNDS_CHECK 0
+#endif
+__device__ __forceinline__ void bounds_check(int64_t idx, int64_t lim, int what) {
+#if PDMG_BOUNDS_CHECK
+  if (idx < 0 || idx >= lim) {
+    printf("pdmg bounds check: access %d index %lld outside [0, %lld) block (%d,%d) thread %d\n", what,
+           (long long)idx, (long long)lim, blockIdx.x, blockIdx.y, threadIdx.x);
+    __trap();
+  }
+#endif
+}
 // NF > 0: the level's subdivision count n as a compile-time constant (row offsets become immediates)
 template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool TWO = true, int NF = 0>
-__global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB)
+__global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB)
     k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
   using D2 = double2;
@@ -1467,7 +1490,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
   constexpr int M2_CPF = PDMG_M2_CPF;
   const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
-  const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
+  const int task = blockIdx.x * march2_wpc(TWO) + (threadIdx.x >> 5);
   if (task >= a.ntasks) return;
   const int lane = threadIdx.x & 31;
   const int tx = task % a.ntx, ty = task / a.ntx;
@@ -1508,7 +1531,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     for (int k = 0; k < LC; ++k) {
       out[k] = cz<D2>();
       if constexpr (LOADU) {
-        if (!MASK || (row_ok(row) && cin[k])) out[k] = ld2(uin[(int64_t)row * n + k]);
+        if (!MASK || (row_ok(row) && cin[k])) {
+          bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 0);
+          out[k] = ld2(uin[(int64_t)row * n + k]);
+        }
       }
     }
   };
@@ -1516,10 +1542,16 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     constexpr bool MASK = decltype(MK)::value;
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
-      if constexpr (MASK)
-        out[k] = (row_ok(row) && cin[k]) ? ld2(bb[(int64_t)row * n + k]) : cz<D2>();
-      else
+      if constexpr (MASK) {
+        out[k] = cz<D2>();
+        if (row_ok(row) && cin[k]) {
+          bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 1);
+          out[k] = ld2(bb[(int64_t)row * n + k]);
+        }
+      } else {
+        bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 2);
         out[k] = ld2(bb[(int64_t)row * n + k]);
+      }
     }
   };
   // prolong_bilinear (grid.cpp:123-153) onto fine row `row` from the coarse values a0 = e(J, Ie),
@@ -1551,6 +1583,8 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
     int J = row >> 1, I = Ie;
     if constexpr (MASK) J = min(max(J, 0), nc - 1), I = min(max(I, 0), nc - 1);
     const V* p0 = ecs + (int64_t)J * nc + I;
+    bounds_check((p0 - a.ec) + nc + 1, a.elems_c, 3);
+    bounds_check(p0 - a.ec, a.elems_c, 3);
     Cq[0] = ld2(p0[0]), Cq[1] = ld2(p0[1]), Cq[2] = ld2(p0[nc]), Cq[3] = ld2(p0[nc + 1]);
   };
   auto west = [&](const D2* x, int k, const D2& wl) __attribute__((always_inline)) { return k == 0 ? wl : x[k - 1]; };
@@ -1653,7 +1687,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
         if constexpr (EVEN) u1 = ld2(st2<V>(u1));  // the iterate the unfused sweep would have stored
         U1[sn][k] = u1;
         if constexpr (!TWO) {
-          if (rst1 && cst[k]) uout[(int64_t)(j - 2) * n + k] = st2<V>(u1);
+          if (rst1 && cst[k]) {
+            bounds_check(sbase + cA + (int64_t)(j - 2) * n + k, a.elems, 4);
+            uout[(int64_t)(j - 2) * n + k] = st2<V>(u1);
+          }
         }
       }
     }
@@ -1667,7 +1704,10 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
 #pragma unroll
       for (int k = 0; k < LC; ++k) {
         const V us = st2<V>(cadd(U1[so][k], dl[k]));
-        if (rst && cst[k]) uout[(int64_t)row * n + k] = us;
+        if (rst && cst[k]) {
+          bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 5);
+          uout[(int64_t)row * n + k] = us;
+        }
         U2[sn][k] = ld2(us);
       }
     }
@@ -1703,6 +1743,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, TWO ? PDMG_MARCH2_MINB : PDM
                 const int I = c >> 1;
                 if (I >= 1 && I <= nc - 1) {
                   const D2 s = cadd(cadd(west(v, k, vwl), cscale(2.0, v[k])), east(v, k, ver));
+                  bounds_check((int64_t)shift * a.ssc + (int64_t)J * nc + I, a.elems_c, 6);
                   a.bc[(int64_t)shift * a.ssc + (int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, s));
                 }
               }

@@ -5,6 +5,10 @@
 set -e
 tag=$1; re=$2; skip=$3; shift 3
 python tools/profile_c3.py "$@" > gpurun_out/${tag}_plain.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$re" -s $skip -c 2 \
-    -o gpurun_out/${tag} python tools/profile_c3.py "$@" > gpurun_out/${tag}_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$re" -s $skip -c 1 \
+    -o /tmp/${tag} python tools/profile_c3.py "$@" > gpurun_out/${tag}_ncu.log 2>&1
 echo "ncu rc=$?"
+# the report itself stays on the box (tens of MB); its raw metrics and per-instruction source page come back
+ncu -i /tmp/${tag}.ncu-rep --page raw --csv > gpurun_out/${tag}_raw.csv
+ncu -i /tmp/${tag}.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/${tag}_sass.csv.gz || true
+ncu -i /tmp/${tag}.ncu-rep --page details --csv > gpurun_out/${tag}_details.csv || true
