@@ -330,7 +330,7 @@ def cmd_paradiag(a) -> int:
 
 def build_parser():
     ap = argparse.ArgumentParser(prog="pdmg-b200", description="B200 shifted-Laplacian multigrid driver")
-    ap.add_argument("--version", action="version", version=VERSION)
+    ap.add_argument("--version", action="version", version="pdmg " + VERSION)  # pdmg.cpp:523
     sub = ap.add_subparsers(dest="cmd", required=True)
     s = sub.add_parser("solve", help="Run one shifted multigrid solve and dump residual history")
     s.add_argument("--h", required=True)
