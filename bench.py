@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c5-transport", default="ipc", choices=["ipc", "nccl"],
+                    help="C5 on N>1 ranks: fused peer-memory transforms over CUDA IPC (default) or NCCL all-to-all")
     ap.add_argument("--shifts", type=int, default=0, help="override the number of shifts (0 = config's)")
     ap.add_argument("--nu", default="", help="override the cycle's nu1,nu2 (experiments; not a BASELINE config)")
     ap.add_argument("--precision", default="c128", choices=["c128", "c64"],
@@ -67,10 +69,21 @@ def parse():
     return ap.parse_args()
 
 
+def dist_backend(local: int):
+    """NCCL over NVLink; gloo for the one-GPU script-path tests (NCCL refuses two ranks on one device)."""
+    import torch
+
+    if os.environ.get("PDMG_BENCH_ONE_DEVICE"):
+        return {"backend": "gloo"}
+    return {"backend": "nccl", "device_id": torch.device("cuda", local)}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PDMG_BENCH_ONE_DEVICE"):  # script-path tests on a one-GPU box (never a reported number)
+        local = 0
     return rank, world, local
 
 
@@ -345,17 +358,37 @@ def run_paradiag(args):
     m = n - 1
     f = heat_initial_rhs(n, nt, dt, seed)
     upc = updates_per_cycle(n, nu1, nu2)
+    pdr = None
     if world > 1:
         import torch.distributed as dist
 
         from paper_2203_11154_b200.paradiag_dist import GpuOps, paradiag_step
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        ntl = nt // world
-        f_local = torch.from_numpy(f[rank * ntl:(rank + 1) * ntl].reshape(ntl, m * m).view(np.float64)
-                                   .reshape(ntl, m * m, 2)).to(f"cuda:{local}")
-        ops = GpuOps(n, nt, alpha, dt, cfg, local)
-        step = lambda: paradiag_step(f_local, n, nt, alpha, dt, ops)  # noqa: E731
+        dist.init_process_group(**dist_backend(local))
+        transport = args.c5_transport
+        if transport == "ipc":
+            # each rank owns its time slices in the library; peers' slice buffers are opened over CUDA IPC and the
+            # time transforms gather / scatter across the ranks through NVLink peer memory inside the kernel
+            try:
+                from paper_2203_11154_b200.paradiag_dist import IpcParadiag
+
+                pdr = IpcParadiag(n, nt, alpha, dt, cfg, local)
+                ctype = {"shape": (pdr.ntl * m * m * 2,), "typestr": "<f8", "data": (pdr.f_ptr, False), "version": 3}
+                fv = torch.as_tensor(type("DevView", (), {"__cuda_array_interface__": ctype})(), device=f"cuda:{local}")
+                fv.copy_(torch.from_numpy(np.ascontiguousarray(f[pdr.t0:pdr.t0 + pdr.ntl]).view(np.float64).ravel()))
+                torch.cuda.synchronize()
+                def step():
+                    it, rr = pdr.step()
+                    return None, it, rr
+            except Exception as e:  # fall back to the NCCL all-to-all driver
+                print(f"bench: IPC transport unavailable ({e}); using NCCL all-to-all", file=sys.stderr)
+                transport, pdr = "nccl", None
+        if transport == "nccl":
+            ntl = nt // world
+            f_local = torch.from_numpy(f[rank * ntl:(rank + 1) * ntl].reshape(ntl, m * m).view(np.float64)
+                                       .reshape(ntl, m * m, 2)).to(f"cuda:{local}")
+            ops = GpuOps(n, nt, alpha, dt, cfg, local)
+            step = lambda: paradiag_step(f_local, n, nt, alpha, dt, ops)  # noqa: E731
     else:
         pd = ParadiagCirculant(n, nt, alpha, dt, cfg, device=local)
         d_f = torch.from_numpy(f.view(np.float64)).to(f"cuda:{local}")
@@ -370,7 +403,8 @@ def run_paradiag(args):
     # distributed driver whose kernels run on torch's current stream)
     from paper_2203_11154_b200 import _native as N
 
-    sh = N.lib().pdmg_stream(pd.solver_handle) if world == 1 else None
+    sh = (N.lib().pdmg_stream(pd.solver_handle) if world == 1 else
+          N.lib().pdmg_stream(pdr.solver_handle) if pdr is not None else None)
     stream = torch.cuda.ExternalStream(sh) if sh else torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world == 1:
@@ -462,7 +496,9 @@ def run_paradiag(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "gpu_launches": launches, "cpu_baseline": cpu, "parity": parity,
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": desc, "parallelism": f"time-sharded x{world} + NCCL all-to-all"},
+            "config": {"workload": desc, "parallelism": f"time-sharded x{world}" + (
+                "" if world == 1 else " + fused peer-memory (CUDA IPC) time transforms" if pdr is not None
+                else " + NCCL all-to-all")},
             "paradiag_steps_per_s": 1e3 / ms, "relres": relres, "cycles_total": iters_total,
             "host_wall_ms_per_step": wall_ms, "e2e": e2e, "roofline": roofline, "kernels": kern,
             "clocks": clk.summary()}), flush=True)
@@ -487,7 +523,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(**dist_backend(local))
     n, S, alpha, nt, dt, seed, nu1, nu2, desc = CONFIGS[args.config]
     if args.shifts:
         S = args.shifts

@@ -160,6 +160,22 @@ int pdmg_paradiag_create_general(int32_t n, int32_t nt, const pdmg_c128* lambdas
 int pdmg_paradiag_num_parts(const pdmg_paradiag* p);
 /* Shard `part`: first time slice, slice count, device. */
 int pdmg_paradiag_part_range(const pdmg_paradiag* p, int part, int32_t* t0, int32_t* count, int32_t* device);
+/* Rank mode: one process per GPU (torchrun).  This process owns time slices [rank*chunk, ...) of `nranks` contiguous
+ * chunks on `device`; the other ranks' slice buffers are opened from their CUDA IPC handles, so the transform kernels
+ * gather / scatter across processes through NVLink peer memory -- the all-to-all stays inside the transforms.
+ *   pdmg_paradiag_ipc_handles(p, h)      h: 4 x 64 bytes (cudaIpcMemHandle_t of f, g, w, u)
+ *   pdmg_paradiag_open_peers(p, all)     all: [nranks][4 x 64 bytes], every rank's handles (own entry ignored)
+ *   pdmg_paradiag_rank_buffer(p, which)  this rank's device buffers: 0 = f (input slices), 3 = u (output slices)
+ *   pdmg_paradiag_rank_phase(p, k, ...)  k = 1 step-1 transform, 2 shifted solves (report: this rank's slots at
+ *                                        their global indices), 3 step-3 transform, 4 residual sums
+ *                                        {||r||^2, ||f||^2} of this rank's slices; the caller barriers all ranks
+ *                                        between phases (each returns once its GPU work is complete). */
+int pdmg_paradiag_create_rank(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t rank,
+                              int32_t nranks, int32_t device, pdmg_paradiag** out);
+int pdmg_paradiag_ipc_handles(pdmg_paradiag* p, void* handles);
+int pdmg_paradiag_open_peers(pdmg_paradiag* p, const void* all_handles);
+int pdmg_paradiag_rank_phase(pdmg_paradiag* p, int32_t phase, pdmg_solve_report* report, double* sums);
+void* pdmg_paradiag_rank_buffer(pdmg_paradiag* p, int32_t which);
 /* Device-resident run of a sharded solver: d_f[p], d_u[p] = shard p's slices in its device's memory. */
 int pdmg_paradiag_run_shards(pdmg_paradiag* p, const void* const* d_f, void* const* d_u, pdmg_solve_report* report,
                              double* relres);

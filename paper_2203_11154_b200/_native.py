@@ -90,6 +90,12 @@ def lib() -> C.CDLL:
         "pdmg_paradiag_part_range": (C.c_int, [vp, C.c_int, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         "pdmg_paradiag_run_shards": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(SolveReport),
                                                C.POINTER(f64)]),
+        "pdmg_paradiag_create_rank": (C.c_int, [i32, i32, f64, f64, C.POINTER(MgConfig), i32, i32, i32,
+                                                C.POINTER(vp)]),
+        "pdmg_paradiag_ipc_handles": (C.c_int, [vp, vp]),
+        "pdmg_paradiag_open_peers": (C.c_int, [vp, vp]),
+        "pdmg_paradiag_rank_phase": (C.c_int, [vp, i32, C.POINTER(SolveReport), C.POINTER(f64)]),
+        "pdmg_paradiag_rank_buffer": (vp, [vp, i32]),
         "pdmg_paradiag_destroy": (None, [vp]),
         "pdmg_paradiag_solver": (vp, [vp]),
         "pdmg_paradiag_run": (C.c_int, [vp, vp, vp, C.POINTER(SolveReport), C.POINTER(f64)]),

@@ -291,6 +291,37 @@ int pdmg_paradiag_run_shards(pdmg_paradiag* P, const void* const* d_f, void* con
   });
 }
 
+int pdmg_paradiag_create_rank(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t rank,
+                              int32_t nranks, int32_t device, pdmg_paradiag** out) {
+  return paradiag_make(out, [&](Paradiag& p) {
+    if (!cfg) throw ConfigError("pdmg_paradiag_create_rank: NULL argument");
+    p.setup_rank(n, nt, alpha, dt, *cfg, rank, nranks, device);
+  });
+}
+int pdmg_paradiag_ipc_handles(pdmg_paradiag* P, void* handles) {
+  return guarded([&] {
+    if (!P || !handles) throw ConfigError("pdmg_paradiag_ipc_handles: NULL argument");
+    P->p.ipc_handles(handles);
+  });
+}
+int pdmg_paradiag_open_peers(pdmg_paradiag* P, const void* all_handles) {
+  return guarded([&] {
+    if (!P || !all_handles) throw ConfigError("pdmg_paradiag_open_peers: NULL argument");
+    P->p.open_peers(all_handles);
+  });
+}
+int pdmg_paradiag_rank_phase(pdmg_paradiag* P, int32_t phase, pdmg_solve_report* report, double* sums) {
+  return guarded([&] {
+    if (!P) throw ConfigError("pdmg_paradiag_rank_phase: NULL argument");
+    P->p.rank_phase(phase, report, sums);
+  });
+}
+void* pdmg_paradiag_rank_buffer(pdmg_paradiag* P, int32_t which) {
+  if (!P || P->p.local < 0 || which < 0 || which > 3) return nullptr;
+  const PdShard& s = *P->p.sh[P->p.local];
+  return which == 0 ? (void*)s.f : which == 1 ? (void*)s.g : which == 2 ? (void*)s.w : (void*)s.u;
+}
+
 int pdmg_paradiag_circulant(int32_t n, int32_t nt, double alpha, double dt, const pdmg_mg_config* cfg, int32_t device,
                             const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* rep, double* relres) {
   pdmg_paradiag* P = nullptr;

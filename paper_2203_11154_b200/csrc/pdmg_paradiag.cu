@@ -140,6 +140,11 @@ std::unique_ptr<DftTables> make_dft_tables(int nt, double alpha, int step, cudaS
 }
 
 PdShard::~PdShard() {
+  if (remote) {  // another rank's buffers, opened over IPC
+    for (double2* p : {f, g, w, u})
+      if (p) cudaIpcCloseMemHandle(p);
+    return;
+  }
   cudaSetDevice(device);
   for (double2* p : {f, g, w, u, y, V, Vi, B}) cudaFree(p);
   cudaFree(partial);
@@ -241,8 +246,60 @@ void Paradiag::setup_general(int n_, int nt_, const pdmg_c128* lambdas, const pd
 //   -> [g ready everywhere] -> the shard's shifted solves -> [w ready everywhere] -> step 3 transform
 //   -> [u ready everywhere] -> all-at-once residual of the shard's slices (the slice before t0 read from its
 //   owner) -> host sums of the partials.
+// Step k of one ParaDIAG run on shard p (tables: row tables of f, g, w, u over all shards), enqueued on the shard's
+// stream: 1 = step-1 transform, 2 = the shard's shifted solves, 3 = step-3 transform, 4 = the all-at-once residual of
+// the shard's slices (partials to s.h_partial).  Cross-shard ordering is the caller's (events + barriers, or a
+// process barrier in rank mode).
+void Paradiag::phase(int p, int k, const RowTab (&T)[4], pdmg_solve_report* rep) {
+  PdShard& s = *sh[p];
+  EngineBase& E = *s.eng;
+  cudaStream_t st = E.stream;
+  const double slice_bytes = sizeof(double2) * (double)npts;
+  const int P = (int)sh.size();
+  if (k == 1 || k == 3) {  // g = (V^{-1} (x) I) f (kron_time_solve, paradiag.cpp:135-139); u = (V (x) I) w (:129-133)
+    const RowTab &in = T[k == 1 ? 0 : 2], &out = T[k == 1 ? 1 : 3];
+    E.timed(general ? "time_gemm" : "time_dft", 2.0 * slice_bytes * nt * (double)(s.pt1 - s.pt0) / npts, [&] {
+      if (general) launch_gemm(k == 1 ? s.Vi : s.V, nt, in, out, 0, nt, 0, s.pt0, s.pt1, st);
+      else launch_dft(k == 1 ? *s.t1 : *s.t3, in, out, s.pt0, s.pt1, st);
+    });
+  } else if (k == 2) {  // the shard's shifted solves (paradiag.cpp:207-236)
+    pdmg_solve_report rc{};
+    if (rep) {
+      const int64_t Hn = E.cfg.max_iter + 1;
+      rc.iterations = rep->iterations ? rep->iterations + s.t0 : nullptr;
+      rc.converged = rep->converged ? rep->converged + s.t0 : nullptr;
+      rc.residual_history = rep->residual_history ? rep->residual_history + s.t0 * Hn : nullptr;
+      rc.rate = rep->rate ? rep->rate + s.t0 : nullptr;
+    }
+    E.solve_device(s.g, s.w, rep ? &rc : nullptr);
+  } else {  // relres = ||f - K u|| / ||f|| (paradiag.cpp:243-245)
+    double2* up = T[3].p[p];
+    const double2* fp = T[0].p[p];
+    E.timed("aao_residual", 3.0 * slice_bytes * s.cnt, [&] {
+      if (general) {
+        const RowTab Ty = rowtab({s.y}, s.cnt, npts);
+        launch_gemm(s.B, nt, T[3], Ty, s.t0, s.t0 + s.cnt, s.t0, 0, npts, st);  // (B (x) I) u on the shard's rows
+        k_aao_residual_dense<<<res_blocks, 256, 0, st>>>(up, s.y, fp, n, s.cnt, s.partial);
+      } else {
+        const int q = (p + P - 1) % P;  // owner of slice t0 - 1 (slice nt - 1 for t0 = 0)
+        const double2* prev = T[3].p[q] + (int64_t)(sh[q]->cnt - 1) * npts;
+        k_aao_residual<<<res_blocks, 256, 0, st>>>(up, prev, fp, n, s.cnt, s.t0, alpha, dt, s.partial);
+      }
+      CK(cudaGetLastError());
+    });
+    CK(cudaMemcpyAsync(s.h_partial, s.partial, sizeof(double) * 2 * res_blocks, cudaMemcpyDeviceToHost, st));
+  }
+}
+
+// One host thread per shard; the cross-device order of the phases is carried by events, recorded before a host
+// barrier and waited on after it:
+//   [input ready] -> step 1 transform (gather f columns from every shard, scatter g rows to their owners)
+//   -> [g ready everywhere] -> the shard's shifted solves -> [w ready everywhere] -> step 3 transform
+//   -> [u ready everywhere] -> all-at-once residual of the shard's slices (the slice before t0 read from its
+//   owner) -> host sums of the partials.
 void Paradiag::run_impl(const double2* const* f, double2* const* u, pdmg_solve_report* rep, double* relres,
                         const pdmg_c128* hf, pdmg_c128* hu) {
+  if (local >= 0) throw ConfigError("ParaDIAG: a per-rank solver runs through pdmg_paradiag_rank_phase");
   const int P = (int)sh.size();
   std::vector<double2*> fp(P), gp(P), wp(P), up(P);
   for (int p = 0; p < P; ++p) {
@@ -251,8 +308,7 @@ void Paradiag::run_impl(const double2* const* f, double2* const* u, pdmg_solve_r
     gp[p] = sh[p]->g, wp[p] = sh[p]->w;
   }
   const int rows = sh[0]->cnt;
-  const RowTab Tf = rowtab(fp, rows, npts), Tg = rowtab(gp, rows, npts), Tw = rowtab(wp, rows, npts),
-               Tu = rowtab(up, rows, npts);
+  const RowTab T[4] = {rowtab(fp, rows, npts), rowtab(gp, rows, npts), rowtab(wp, rows, npts), rowtab(up, rows, npts)};
   Barrier bar(P);
   std::vector<std::exception_ptr> err(P);
   std::vector<double> sums(2 * P, 0.0);
@@ -263,53 +319,15 @@ void Paradiag::run_impl(const double2* const* f, double2* const* u, pdmg_solve_r
     CK(cudaSetDevice(s.device));
     const double slice_bytes = sizeof(double2) * (double)npts;
     if (hf) CK(cudaMemcpyAsync(fp[p], hf + (int64_t)s.t0 * npts, slice_bytes * s.cnt, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(s.ev[0], st));
-    bar.wait();
-    for (auto& o : sh) CK(cudaStreamWaitEvent(st, o->ev[0], 0));
-    // step 1: g = (V^{-1} (x) I) f (kron_time_solve, paradiag.cpp:135-139)
-    E.timed(general ? "time_gemm" : "time_dft", 2.0 * slice_bytes * nt * (double)(s.pt1 - s.pt0) / npts, [&] {
-      if (general) launch_gemm(s.Vi, nt, Tf, Tg, 0, nt, 0, s.pt0, s.pt1, st);
-      else launch_dft(*s.t1, Tf, Tg, s.pt0, s.pt1, st);
-    });
-    CK(cudaEventRecord(s.ev[1], st));
-    bar.wait();
-    for (auto& o : sh) CK(cudaStreamWaitEvent(st, o->ev[1], 0));
-    // step 2: the shard's shifted solves (paradiag.cpp:207-236)
-    pdmg_solve_report rc{};
-    if (rep) {
-      const int64_t Hn = E.cfg.max_iter + 1;
-      rc.iterations = rep->iterations ? rep->iterations + s.t0 : nullptr;
-      rc.converged = rep->converged ? rep->converged + s.t0 : nullptr;
-      rc.residual_history = rep->residual_history ? rep->residual_history + s.t0 * Hn : nullptr;
-      rc.rate = rep->rate ? rep->rate + s.t0 : nullptr;
-    }
-    E.solve_device(s.g, s.w, rep ? &rc : nullptr);
-    CK(cudaEventRecord(s.ev[2], st));
-    bar.wait();
-    for (auto& o : sh) CK(cudaStreamWaitEvent(st, o->ev[2], 0));
-    // step 3: u = (V (x) I) w (kron_time_apply, paradiag.cpp:129-133)
-    E.timed(general ? "time_gemm" : "time_dft", 2.0 * slice_bytes * nt * (double)(s.pt1 - s.pt0) / npts, [&] {
-      if (general) launch_gemm(s.V, nt, Tw, Tu, 0, nt, 0, s.pt0, s.pt1, st);
-      else launch_dft(*s.t3, Tw, Tu, s.pt0, s.pt1, st);
-    });
-    CK(cudaEventRecord(s.ev[3], st));
-    bar.wait();
-    for (auto& o : sh) CK(cudaStreamWaitEvent(st, o->ev[3], 0));
-    if (hu) CK(cudaMemcpyAsync(hu + (int64_t)s.t0 * npts, up[p], slice_bytes * s.cnt, cudaMemcpyDeviceToHost, st));
-    if (relres) {  // relres = ||f - K u|| / ||f|| (paradiag.cpp:243-245)
-      E.timed("aao_residual", 3.0 * slice_bytes * s.cnt, [&] {
-        if (general) {
-          const RowTab Ty = rowtab({s.y}, s.cnt, npts);
-          launch_gemm(s.B, nt, Tu, Ty, s.t0, s.t0 + s.cnt, s.t0, 0, npts, st);  // (B (x) I) u on the shard's rows
-          k_aao_residual_dense<<<res_blocks, 256, 0, st>>>(up[p], s.y, fp[p], n, s.cnt, s.partial);
-        } else {
-          const int q = (p + P - 1) % P;  // owner of slice t0 - 1 (slice nt - 1 for t0 = 0)
-          const double2* prev = up[q] + (int64_t)(sh[q]->cnt - 1) * npts;
-          k_aao_residual<<<res_blocks, 256, 0, st>>>(up[p], prev, fp[p], n, s.cnt, s.t0, alpha, dt, s.partial);
-        }
-        CK(cudaGetLastError());
-      });
-      CK(cudaMemcpyAsync(s.h_partial, s.partial, sizeof(double) * 2 * res_blocks, cudaMemcpyDeviceToHost, st));
+    for (int k = 1; k <= 4; ++k) {
+      CK(cudaEventRecord(s.ev[k - 1], st));
+      bar.wait();
+      for (auto& o : sh) CK(cudaStreamWaitEvent(st, o->ev[k - 1], 0));
+      if (k == 4) {
+        if (hu) CK(cudaMemcpyAsync(hu + (int64_t)s.t0 * npts, up[p], slice_bytes * s.cnt, cudaMemcpyDeviceToHost, st));
+        if (!relres) break;
+      }
+      phase(p, k, T, rep);
     }
     CK(cudaStreamSynchronize(st));
     if (relres)
@@ -337,6 +355,98 @@ void Paradiag::run_impl(const double2* const* f, double2* const* u, pdmg_solve_r
     for (int p = 0; p < P; ++p) rr += sums[2 * p], ff += sums[2 * p + 1];
     *relres = ff > 0.0 ? std::sqrt(rr) / std::sqrt(ff) : std::sqrt(rr);
   }
+}
+
+// ---- rank mode: one process per GPU, the other shards' buffers opened over CUDA IPC ---------------------------------
+void Paradiag::setup_rank(int n_, int nt_, double alpha_, double dt_, const pdmg_mg_config& cfg, int rank,
+                          int nranks, int device) {
+  if (nt_ < 2) throw ConfigError("TimeDiscretization: need n >= 2 time steps");
+  if (!(dt_ > 0.0)) throw ConfigError("TimeDiscretization: tau must be positive");
+  if (!(alpha_ != 0.0)) throw ConfigError("alpha-circulant: alpha must be nonzero");
+  if (nranks < 1 || nranks > MAX_SHARDS || rank < 0 || rank >= nranks)
+    throw ConfigError("ParaDIAG: rank " + std::to_string(rank) + " of " + std::to_string(nranks) + " (1..16 ranks)");
+  const int chunk = (nt_ + nranks - 1) / nranks;
+  if ((int64_t)(nranks - 1) * chunk >= nt_)
+    throw ConfigError("ParaDIAG: " + std::to_string(nt_) + " time steps leave a rank without slices at " +
+                      std::to_string(nranks) + " ranks");
+  check_dft_size(nt_);
+  general = false, alpha = alpha_, dt = dt_;
+  n = n_, nt = nt_;
+  npts = (int64_t)(n - 1) * (n - 1);
+  local = rank;
+  std::vector<pdmg_c128> lam(nt);
+  pdmg_circulant_shifts(alpha, nt, dt, 0, nt, lam.data());
+  for (int t = 0; t < nranks; ++t) {
+    auto s = std::make_unique<PdShard>();
+    s->t0 = t * chunk, s->cnt = std::min(nt, s->t0 + chunk) - s->t0;
+    s->pt0 = npts * t / nranks, s->pt1 = npts * (t + 1) / nranks;
+    s->remote = t != rank;
+    s->device = t == rank ? device : -1;
+    sh.push_back(std::move(s));
+  }
+  PdShard& s = *sh[rank];
+  pdmg_batch_desc d{n, s.cnt, lam.data() + s.t0, cfg, PDMG_PREC_C128, device};
+  s.eng = make_engine_c128();
+  s.eng->device = -1;
+  s.eng->setup_host(d);
+  s.eng->setup_device(device);
+  CK(cudaSetDevice(device));
+  const size_t bytes = sizeof(double2) * (size_t)s.cnt * npts;
+  for (double2** q : {&s.f, &s.g, &s.w, &s.u}) CK(cudaMalloc(q, bytes));
+  CK(cudaMalloc(&s.partial, sizeof(double) * 2 * res_blocks));
+  CK(cudaMallocHost(&s.h_partial, sizeof(double) * 2 * res_blocks));
+  for (auto& e : s.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  dft_attr(device);
+  s.t1 = make_dft_tables(nt, alpha, 1, s.eng->stream);
+  s.t3 = make_dft_tables(nt, alpha, 3, s.eng->stream);
+}
+
+void Paradiag::ipc_handles(void* out) const {
+  if (local < 0) throw ConfigError("pdmg_paradiag_ipc_handles: not a per-rank solver");
+  const PdShard& s = *sh[local];
+  CK(cudaSetDevice(s.device));
+  cudaIpcMemHandle_t h[4];
+  const double2* bufs[4] = {s.f, s.g, s.w, s.u};
+  for (int k = 0; k < 4; ++k) CK(cudaIpcGetMemHandle(&h[k], const_cast<double2*>(bufs[k])));
+  std::memcpy(out, h, sizeof(h));
+}
+
+void Paradiag::open_peers(const void* all) {
+  if (local < 0) throw ConfigError("pdmg_paradiag_open_peers: not a per-rank solver");
+  CK(cudaSetDevice(sh[local]->device));
+  const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
+  for (size_t p = 0; p < sh.size(); ++p) {
+    if ((int)p == local) continue;
+    PdShard& s = *sh[p];
+    double2** bufs[4] = {&s.f, &s.g, &s.w, &s.u};
+    for (int k = 0; k < 4; ++k) {
+      if (*bufs[k]) CK(cudaIpcCloseMemHandle(*bufs[k]));
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, h[p * 4 + k], cudaIpcMemLazyEnablePeerAccess));
+      *bufs[k] = static_cast<double2*>(ptr);
+    }
+  }
+  peers_open = true;
+}
+
+void Paradiag::rank_phase(int k, pdmg_solve_report* rep, double* sums) {
+  if (local < 0) throw ConfigError("pdmg_paradiag_rank_phase: not a per-rank solver");
+  if (!peers_open && sh.size() > 1) throw ConfigError("pdmg_paradiag_rank_phase: peers not opened");
+  if (k < 1 || k > 4) throw ConfigError("pdmg_paradiag_rank_phase: phase must be 1..4");
+  const int P = (int)sh.size();
+  std::vector<double2*> fp(P), gp(P), wp(P), up(P);
+  for (int p = 0; p < P; ++p) fp[p] = sh[p]->f, gp[p] = sh[p]->g, wp[p] = sh[p]->w, up[p] = sh[p]->u;
+  const int rows = sh[0]->cnt;
+  const RowTab T[4] = {rowtab(fp, rows, npts), rowtab(gp, rows, npts), rowtab(wp, rows, npts), rowtab(up, rows, npts)};
+  PdShard& s = *sh[local];
+  CK(cudaSetDevice(s.device));
+  phase(local, k, T, rep);
+  CK(cudaStreamSynchronize(s.eng->stream));  // this rank's part of the phase is complete (peer writes included)
+  if (k == 4 && sums) {
+    sums[0] = sums[1] = 0.0;
+    for (int b = 0; b < res_blocks; ++b) sums[0] += s.h_partial[2 * b], sums[1] += s.h_partial[2 * b + 1];
+  }
+  s.eng->drain_stats();
 }
 
 void Paradiag::run_shards(const double2* const* f, double2* const* u, pdmg_solve_report* rep, double* relres) {

@@ -11,6 +11,8 @@
 
 namespace pdmg_b200 {
 
+struct RowTab;  // pdmg_time_kernels.cuh
+
 // alpha-scaled DFT tables over the time index (device arrays of one device)
 struct DftTables {
   double2* tw = nullptr;  // e^{dir 2 pi i q/nt}
@@ -38,6 +40,7 @@ struct PdShard {
   std::unique_ptr<DftTables> t1, t3; // circulant scheme
   double2 *V = nullptr, *Vi = nullptr, *B = nullptr;  // general scheme (nt x nt, this device)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // input ready, g ready, w ready, u ready
+  bool remote = false;  // rank mode: another process's shard (buffers opened over CUDA IPC, no engine)
   ~PdShard();
 };
 
@@ -60,9 +63,22 @@ struct Paradiag {
   void run_shards(const double2* const* f, double2* const* u, pdmg_solve_report* rep, double* relres);
   void run_device(const double2* f, double2* u, pdmg_solve_report* rep, double* relres);  // one shard
   void run_host(const pdmg_c128* f, pdmg_c128* u, pdmg_solve_report* rep, double* relres);
-  EngineBase* solver() { return sh.empty() ? nullptr : sh[0]->eng.get(); }
+  EngineBase* solver() { return sh.empty() ? nullptr : sh[local >= 0 ? local : 0]->eng.get(); }
+
+  // Rank mode (one process per GPU): this process owns shard `rank` of `nranks`; the other shards' f, g, w, u are
+  // opened from their CUDA IPC handles, so the transform kernels gather / scatter across processes through NVLink
+  // peer memory exactly as across the devices of one process.  The caller runs the four phases with a process
+  // barrier between them (each phase returns once its GPU work, peer writes included, is complete).
+  int local = -1;
+  bool peers_open = false;
+  void setup_rank(int n_, int nt_, double alpha_, double dt_, const pdmg_mg_config& cfg, int rank, int nranks,
+                  int device);
+  void ipc_handles(void* out) const;  // 4 cudaIpcMemHandle_t: f, g, w, u
+  void open_peers(const void* all);   // [nranks][4] handles
+  void rank_phase(int k, pdmg_solve_report* rep, double* sums);
 
  private:
+  void phase(int p, int k, const RowTab (&T)[4], pdmg_solve_report* rep);
   void setup_shards(int n_, int nt_, const std::vector<pdmg_c128>& lam, const pdmg_mg_config& cfg,
                     const std::vector<int>& devices);
   void run_impl(const double2* const* f, double2* const* u, pdmg_solve_report* rep, double* relres,

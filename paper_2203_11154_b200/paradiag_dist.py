@@ -1,5 +1,11 @@
-"""Multi-GPU ParaDIAG step (BASELINE config 5 on 1/2/4/8 GPUs): time slices sharded over ranks, NCCL
-all-to-all transposes around the alpha-scaled time DFT, the nt shifted solves sharded by frequency.
+"""Multi-GPU ParaDIAG step (BASELINE config 5 on 1/2/4/8 GPUs), one process per GPU.
+
+Two transports:
+  * `IpcParadiag` (default): every rank owns its time slices in libpdmg_b200 (pdmg_paradiag_create_rank); the
+    ranks exchange CUDA IPC handles of their slice buffers once, and the time-transform kernels gather each
+    spatial point's time column from every rank and scatter the results to their owners through NVLink peer
+    memory -- the all-to-all is inside the transform (the same kernels as the single-process device list).
+  * `paradiag_step` + `GpuOps`: NCCL all-to-all transposes around the alpha-scaled time DFT (below).
 
 Data movement; P = world size, nt divisible by P, points padded to P * pl:
     f  [t-shard][points]  --a2a-->  [t][point-shard]  --DFT step 1-->  [k][point-shard]
@@ -116,3 +122,68 @@ class GpuOps:
                                          u_local.data_ptr(), u_prev.data_ptr(), f_local.data_ptr(), sums,
                                          self._stream()))
         return sums[0], sums[1]
+
+
+class IpcParadiag:
+    """One rank's share of a ParaDIAG solver whose time slices are sharded over the ranks of the default process
+    group; peers' slice buffers are opened over CUDA IPC (pdmg_paradiag_create_rank / _ipc_handles / _open_peers).
+    `step()` runs the four phases with a process barrier between them and returns (iterations of this rank's
+    slots, relres)."""
+
+    def __init__(self, n: int, nt: int, alpha: float, dt: float, cfg, device: int):
+        import ctypes as C
+
+        from . import _native as N
+        from .multigrid import _check
+
+        self.N, self.C, self._check = N, C, _check
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.n, self.nt, self.cfg = n, nt, cfg
+        h = C.c_void_p()
+        c = cfg._c()
+        _check(N.lib().pdmg_paradiag_create_rank(n, nt, alpha, dt, C.byref(c), self.rank, self.world, device,
+                                                 C.byref(h)))
+        self._h = h
+        mine = (C.c_char * 256)()
+        _check(N.lib().pdmg_paradiag_ipc_handles(h, mine))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(mine))
+        buf = (C.c_char * (256 * self.world)).from_buffer_copy(b"".join(allh))
+        _check(N.lib().pdmg_paradiag_open_peers(h, buf))
+        self.chunk = -(-nt // self.world)
+        self.t0 = self.rank * self.chunk
+        self.ntl = min(nt, self.t0 + self.chunk) - self.t0
+        self.f_ptr = N.lib().pdmg_paradiag_rank_buffer(h, 0)
+        self.u_ptr = N.lib().pdmg_paradiag_rank_buffer(h, 3)
+        dist.barrier()
+
+    @property
+    def solver_handle(self):
+        return self.N.lib().pdmg_paradiag_solver(self._h)
+
+    def step(self, want_iterations: bool = True):
+        N, C, _check = self.N, self.C, self._check
+        H = self.cfg.max_iter + 1
+        it = np.zeros(self.nt, np.int32)
+        rep = N.SolveReport(it.ctypes.data, None, None, None, 0.0) if want_iterations else None
+        sums = (C.c_double * 2)()
+        dist.barrier()  # every rank's f slices are in place
+        for k in (1, 2, 3, 4):
+            _check(N.lib().pdmg_paradiag_rank_phase(self._h, k, C.byref(rep) if rep else None, sums))
+            if k < 4:
+                dist.barrier()
+        t = torch.tensor([sums[0], sums[1]], dtype=torch.float64)
+        if dist.get_backend() == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t)
+        rr, ff = float(t[0]), float(t[1])
+        relres = (rr ** 0.5) / (ff ** 0.5) if ff > 0 else rr ** 0.5
+        iters = it[self.t0:self.t0 + self.ntl].tolist() if want_iterations else None
+        del H
+        return iters, relres
+
+    def close(self):
+        if getattr(self, "_h", None):
+            dist.barrier()  # peers close their mappings of our buffers before we free them
+            self.N.lib().pdmg_paradiag_destroy(self._h)
+            self._h = None

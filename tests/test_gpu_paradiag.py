@@ -218,3 +218,24 @@ def test_heat_bvm_general_scheme_matches_oracle_solves(oracle, devices):
     u_ref = (dg.V @ ref["u"].reshape(nt, -1)).reshape(nt, m, m)
     assert rel(u, u_ref) < 1e-10
     assert relres < 1e-8
+
+
+def test_paradiag_ipc_ranks_match_single_process():
+    """Rank mode (one process per GPU): two torchrun ranks -- both on GPU 0 here, each owning half the time slices
+    in its own process -- exchange CUDA IPC handles and run the fused gather/scatter transforms across the two
+    processes (tests/ipc_paradiag_worker.py); the result is bitwise the single-process solver's."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "tests", "ipc_paradiag_worker.py")], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ipc paradiag ok" in r.stdout
