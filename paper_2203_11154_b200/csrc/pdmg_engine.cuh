@@ -453,6 +453,8 @@ struct Engine : EngineBase {
   void setup_device(int dev) override {
     device = dev;
     if (const char* e = std::getenv("PDMG_TAIL_MAX_N")) tail_max_n = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_MARCH2_MIN_N")) march2_min_n = std::atoi(e);  // (tuning)
+    if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);    // (tuning)
     if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
     auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
@@ -489,6 +491,11 @@ struct Engine : EngineBase {
         const Level& P = borrow->lv[l];
         const int64_t off = (int64_t)borrow_s0 * Lv.ss;
         Lv.u[0] = P.u[0] + off, Lv.u[1] = P.u[1] + off, Lv.b = P.b + off;
+        // Invariant every kernel keeps (the concurrent chunks run on these overlapping views at the same time): a
+        // pass writes only cells of its own shifts [s * ss, (s + 1) * ss), and any cell it reads outside them (halo
+        // or guard reads past the last shift, here the next chunk's first shift) only reaches results that are
+        // masked to its own interior.  tests/test_gpu_parity.py::test_chunked_host_solve_marching_passes checks
+        // the chunked results bitwise against one batch; PDMG_BOUNDS_CHECK builds assert the allocation bounds.
         if (borrow_s0 + S < borrow->S) Lv.elems = (size_t)Lv.ss * S;
         Lv.alloc_left = P.alloc_left - off;
       } else {
