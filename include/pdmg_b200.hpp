@@ -177,4 +177,95 @@ inline std::vector<cplx> random_rhs(Grid2D g, unsigned seed) {
   return b;
 }
 
+// ---- ParaDIAG (proj/include/pdmg/paradiag.hpp:95-113) -------------------------------------------------------------
+// ParadiagResult without the Eigen members: u (time slices stacked, reference layout), the per-slot shifts and
+// reports (in the order of the time matrix's eigenvalues), all_converged, relative_residual, seconds.
+struct ParadiagResult {
+  std::vector<cplx> u;
+  std::vector<Shift> shifts;
+  std::vector<SolveReport> reports;
+  bool all_converged = false;
+  double relative_residual = 0.0;
+  double seconds = 0.0;
+};
+
+namespace detail {
+inline ParadiagResult run_paradiag(pdmg_paradiag* p, const std::vector<cplx>& f, long slices, int max_iter) {
+  ParadiagResult r;
+  r.u.resize(f.size());
+  const int H = max_iter + 1;
+  std::vector<int32_t> it(slices);
+  std::vector<uint8_t> cv(slices);
+  std::vector<double> hist(static_cast<size_t>(slices) * H), rate(slices);
+  pdmg_solve_report rep{it.data(), cv.data(), hist.data(), rate.data(), 0.0};
+  const int st = pdmg_paradiag_run(p, reinterpret_cast<const pdmg_c128*>(f.data()),
+                                   reinterpret_cast<pdmg_c128*>(r.u.data()), &rep, &r.relative_residual);
+  pdmg_paradiag_destroy(p);
+  check(st);
+  r.reports.resize(slices);
+  r.all_converged = true;
+  for (long s = 0; s < slices; ++s) {
+    SolveReport& q = r.reports[s];
+    q.converged = cv[s] != 0, q.iterations = it[s], q.rate = rate[s], q.seconds = rep.seconds;
+    q.residual_history.assign(hist.begin() + s * H, hist.begin() + s * H + it[s] + 1);
+    r.all_converged = r.all_converged && q.converged;
+  }
+  r.seconds = rep.seconds;
+  return r;
+}
+}  // namespace detail
+
+// paradiag_solve (paradiag.cpp:185-248) for the alpha-circulant time matrix C_alpha = (1/tau)(I - Sigma_alpha):
+// the BASELINE preconditioner (alpha > 0) or, with alpha = -1/beta, the reference's BackwardHeatQBV (whose reports
+// this returns in the reference's eigenvalue order, paradiag.cpp:84-108).  f: `slices` time slices of the fine grid
+// stacked; devices: the reference's `threads` (time slices sharded over the devices, transforms through peer memory).
+inline ParadiagResult paradiag_solve_circulant(const std::vector<cplx>& f, Grid2D g, int slices, double alpha,
+                                               double tau, const MultigridConfig& cfg,
+                                               const std::vector<int>& devices = {0}) {
+  if (slices < 1 || f.size() != static_cast<size_t>(slices) * g.size())
+    throw ConfigError("paradiag_solve: expected " + std::to_string(slices) + " time slices");
+  const pdmg_mg_config c = cfg.c();
+  std::vector<int32_t> devs(devices.begin(), devices.end());
+  pdmg_paradiag* p = nullptr;
+  check(pdmg_paradiag_create_multi(g.n, slices, alpha, tau, &c, devs.data(), static_cast<int32_t>(devs.size()), &p));
+  ParadiagResult r = detail::run_paradiag(p, f, slices, cfg.max_iter);
+  std::vector<pdmg_c128> lam(slices);
+  pdmg_circulant_shifts(alpha, slices, tau, 0, slices, lam.data());
+  r.shifts.resize(slices);
+  for (int k = 0; k < slices; ++k) r.shifts[k] = Shift{cplx(lam[k].re, lam[k].im), k};
+  if (alpha < 0) {  // QBV: reference index k is circulant slot (m - k) mod m
+    std::vector<SolveReport> reps(slices);
+    std::vector<Shift> sh(slices);
+    for (int k = 0; k < slices; ++k) {
+      const int q = (slices - k) % slices;
+      reps[k] = r.reports[q], sh[k] = Shift{r.shifts[q].lambda, k};
+    }
+    r.reports.swap(reps), r.shifts.swap(sh);
+  }
+  return r;
+}
+
+// paradiag_solve with a general diagonalization B = V diag(lambdas) V^{-1} supplied by the caller (HeatBVM:
+// diagonalize_time_matrix, paradiag.cpp:71-82); V, Vinv complex and B real, nt x nt row-major.
+inline ParadiagResult paradiag_solve_general(const std::vector<cplx>& f, Grid2D g, const std::vector<cplx>& lambdas,
+                                             const std::vector<cplx>& V, const std::vector<cplx>& Vinv,
+                                             const std::vector<double>& B, const MultigridConfig& cfg,
+                                             const std::vector<int>& devices = {0}) {
+  const int nt = static_cast<int>(lambdas.size());
+  if (nt < 1 || f.size() != static_cast<size_t>(nt) * g.size() || V.size() != static_cast<size_t>(nt) * nt ||
+      Vinv.size() != V.size() || B.size() != V.size())
+    throw ConfigError("paradiag_solve: inconsistent time-matrix or right-hand-side sizes");
+  const pdmg_mg_config c = cfg.c();
+  std::vector<int32_t> devs(devices.begin(), devices.end());
+  pdmg_paradiag* p = nullptr;
+  check(pdmg_paradiag_create_general(g.n, nt, reinterpret_cast<const pdmg_c128*>(lambdas.data()),
+                                     reinterpret_cast<const pdmg_c128*>(V.data()),
+                                     reinterpret_cast<const pdmg_c128*>(Vinv.data()), B.data(), &c, devs.data(),
+                                     static_cast<int32_t>(devs.size()), &p));
+  ParadiagResult r = detail::run_paradiag(p, f, nt, cfg.max_iter);
+  r.shifts.resize(nt);
+  for (int k = 0; k < nt; ++k) r.shifts[k] = Shift{lambdas[k], k};
+  return r;
+}
+
 }  // namespace pdmg_b200

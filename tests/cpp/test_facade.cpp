@@ -58,6 +58,22 @@ int main(int argc, char** argv) {
   auto [u2, rep2] = multigrid_solve(random_rhs(g, 123), g, Shift{}, MultigridConfig{});
   CHECK(rep2.iterations == 14);
   CHECK(std::abs(rep2.rate - 0.273) < 1e-3);
-  std::printf("facade ok: C1 %d cycles, W(1,0) %d cycles rate %.4f\n", rep.iterations, rep2.iterations, rep2.rate);
+  // paradiag_solve through the facade: BASELINE's alpha-circulant preconditioner on one device and sharded over the
+  // device list {0, 0} (bitwise the same u), and the QBV scheme (alpha = -1/beta) in the reference's order
+  const Grid2D g32(32);
+  const int nt = 8;
+  std::vector<cplx> f(static_cast<size_t>(nt) * g32.size());
+  pdmg_random_rhs(4, -1.0, 1.0, (int64_t)f.size(), reinterpret_cast<pdmg_c128*>(f.data()));
+  const ParadiagResult p1 = paradiag_solve_circulant(f, g32, nt, 0.01, 1.0 / nt, cfg);
+  const ParadiagResult p2 = paradiag_solve_circulant(f, g32, nt, 0.01, 1.0 / nt, cfg, {0, 0});
+  CHECK(p1.all_converged && p1.relative_residual < 1e-8 && p1.u == p2.u);
+  const ParadiagResult q = paradiag_solve_circulant(f, g32, nt, -100.0, 1.0 / nt, cfg);
+  CHECK(q.all_converged && q.reports.size() == (size_t)nt);
+  // slot k holds (1 - gamma zeta^{-k}) / tau with gamma = 100^{1/nt} e^{i pi / nt}
+  const double pi = 3.14159265358979323846;
+  const cplx lam1 = (1.0 - std::polar(std::pow(100.0, 1.0 / nt), pi / nt - 2.0 * pi / nt)) * (double)nt;
+  CHECK(std::abs(q.shifts[1].lambda - lam1) <= 1e-12 * std::abs(lam1));
+  std::printf("facade ok: C1 %d cycles, W(1,0) %d cycles rate %.4f; paradiag relres %.2e\n", rep.iterations,
+              rep2.iterations, rep2.rate, p1.relative_residual);
   return 0;
 }
