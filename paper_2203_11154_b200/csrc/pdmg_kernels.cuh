@@ -1178,7 +1178,7 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
   constexpr int WOUT = 32 * LC - 2 * hA;  // stored columns per warp
   const int shift = blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
-  const int task = blockIdx.x * MARCH_WARPS + (threadIdx.x >> 5);
+  const int task = blockIdx.x * MARCH_WARPS + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform (see k_march2)
   if (task >= a.ntasks) return;
   const int lane = threadIdx.x & 31;
   const int tx = task % a.ntx, ty = task / a.ntx;
@@ -1490,7 +1490,10 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   constexpr int M2_CPF = PDMG_M2_CPF;
   const int shift = cp.shift0 + blockIdx.y;
   if (a.active != nullptr && a.active[shift] == 0) return;
-  const int task = blockIdx.x * march2_wpc(TWO) + (threadIdx.x >> 5);
+  // the warp index broadcast from lane 0, so the compiler knows that the task and everything derived from it
+  // (row ranges, loop bounds, row parity) is warp-uniform: uniform branches, no divergence guards (BRA.DIV)
+  // around the shuffles and no register moves into their fixed operands
+  const int task = blockIdx.x * march2_wpc(TWO) + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   if (task >= a.ntasks) return;
   const int lane = threadIdx.x & 31;
   const int tx = task % a.ntx, ty = task / a.ntx;
