@@ -15,6 +15,7 @@
 
 #include "pdmg_host.h"
 #include "pdmg_kernels.cuh"
+#include "pdmg_march2_table.h"
 
 // compile the hot marching passes with the level's n as a constant (n = 256, 512, 1024; complex128)
 #ifndef PDMG_MARCH2_NF
@@ -141,58 +142,27 @@ struct MarchTable {
   }
 };
 
-// fused Vanka passes (k_march2): key = loadu | prolong << 1 | post << 2 | norm_in << 4
+// fused Vanka passes (k_march2): key = loadu | prolong << 1 | post << 2 | norm_in << 4.  The kernels are instantiated
+// in their own translation units (pdmg_march2_units.cuh); the table is filled through pdmg_march2_table.h.
 template <class T>
 struct March2Table {
-  using Fn = void (*)(MarchArgs<T>, CoefPack);
+  using Fn = March2Fn<T>;
   Fn e[32] = {};   // two sweeps per pass
   Fn e1[32] = {};  // one sweep per pass (k_march2<..., TWO = false>)
   // the hot variants with the level's n compiled in (NF): [n = 256, 512, 1024][key]
   Fn eN[3][32] = {}, e1N[3][32] = {};
   static int nf_slot(int n) { return n == 256 ? 0 : n == 512 ? 1 : n == 1024 ? 2 : -1; }
-  template <bool LU, bool PR, int PO, bool NI, bool TWO, int NFV>
-  void regN() {
-    (TWO ? eN : e1N)[nf_slot(NFV)][key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI, TWO, NFV>;
-  }
-  template <int NFV>
-  void reg_hot() {
-#if PDMG_MARCH2_NF
-    regN<true, true, POST_NONE, false, true, NFV>();        // prolong+vanka2
-    regN<true, false, POST_RESTRICT, true, true, NFV>();    // vanka2+restrict+norm_in
-    regN<false, false, POST_RESTRICT, true, true, NFV>();   // zero+vanka2+restrict+norm_in
-    regN<false, false, POST_RESTRICT, false, true, NFV>();  // zero+vanka2+restrict (coarse levels)
-    regN<true, true, POST_NONE, false, false, NFV>();       // prolong+vanka (V(1,1))
-    regN<true, false, POST_RESTRICT, true, false, NFV>();   // vanka+restrict+norm_in (V(1,1))
-    regN<false, false, POST_RESTRICT, true, false, NFV>();  // zero+vanka+restrict+norm_in
-    regN<false, false, POST_RESTRICT, false, false, NFV>(); // zero+vanka+restrict
-#endif
-  }
-  static int key(bool lu, bool pr, int post, bool nin = false) {
-    return (lu ? 1 : 0) | (pr ? 2 : 0) | (post << 2) | (nin ? 16 : 0);
-  }
-  template <bool LU, bool PR, int PO, bool NI = false>
-  void reg() {
-    e[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI, true>;
-    e1[key(LU, PR, PO, NI)] = &k_march2<T, LU, PR, PO, NI, false>;
-  }
-  template <bool LU>
-  void reg_lu() {
-    reg<LU, false, POST_NONE>();
-    reg<LU, false, POST_RESTRICT>();
-    reg<LU, false, POST_NORM>();
-    reg<LU, true, POST_NONE>();
-    reg<LU, true, POST_NORM>();
-    reg<LU, false, POST_RESTRICT, true>();
-    reg<LU, false, POST_NONE, true>();
-  }
+  static int key(bool lu, bool pr, int post, bool nin = false) { return march2_key(lu, pr, post, nin); }
   March2Table() {
-    reg_lu<false>();
-    reg_lu<true>();
+    march2_fill_two(e);
+    march2_fill_one(e1);
+#if PDMG_MARCH2_NF
     if constexpr (std::is_same<T, double>::value) {
-      reg_hot<256>();
-      reg_hot<512>();
-      reg_hot<1024>();
+      march2_fill_hot_256(eN[0], e1N[0]);
+      march2_fill_hot_512(eN[1], e1N[1]);
+      march2_fill_hot_1024(eN[2], e1N[2]);
     }
+#endif
   }
 };
 
@@ -278,9 +248,9 @@ struct Engine : EngineBase {
       if (e.first == n) return e.second;
     const int def = n >= 512 ? 128 : n >= 256 ? 64 : 32;
     const int ha = march2_ha(post, two), ntx = (n + 63 - 2 * ha) / (64 - 2 * ha);
-    const int64_t slots = (int64_t)sm_count * (two ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB);
+    const int wpc = two ? m2_wpc : m1_wpc;
+    const int64_t slots = (int64_t)sm_count * (march2_warps_per_sm(two) / wpc);
     auto cost = [&](int hs) {
-      const int wpc = march2_wpc(two);
       const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + wpc - 1) / wpc) * S;
       return (double)((ctas + slots - 1) / slots) * (hs + 2 * ha);
     };
@@ -292,6 +262,7 @@ struct Engine : EngineBase {
     }
     return best;
   }
+  int m2_wpc = 4, m1_wpc = 4;  // warps per CTA of the two-sweep / one-sweep marching passes (PDMG_M2_WPC, PDMG_M1_WPC)
   bool march2_pre = true, march2_post = true;  // fuse the pre- / post-smoothing sweep pairs
   int march2_loopb_min_n = 128;  // (prolongating passes: shape (a), see march2_prolong_b)
   bool norm_next = true;  // fine-level convergence norm from the next cycle's first pass (see solve_device)
@@ -352,7 +323,7 @@ struct Engine : EngineBase {
       for (int c0 = 0; c0 < S; c0 += COEF_MAX) {  // one launch per COEF_MAX shifts (coefficients as parameters)
         const int cnt = std::min(COEF_MAX, S - c0);
         fill_pack(Lv, c0, cnt);
-        const int wpc = march2_wpc(two);
+        const int wpc = two ? m2_wpc : m1_wpc;
         dim3 grid((ma.ntasks + wpc - 1) / wpc, cnt);
         fn<<<grid, 32 * wpc, 0, stream>>>(ma, *cpack);
       }
@@ -469,6 +440,8 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH2_HS_R")) parse_hs(e, march2_hs_r);
     if (const char* e = std::getenv("PDMG_MARCH2_HS_P")) parse_hs(e, march2_hs_p);
     if (const char* e = std::getenv("PDMG_MARCH1")) march1 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PDMG_M2_WPC")) m2_wpc = std::max(1, std::min(8, std::atoi(e)));
+    if (const char* e = std::getenv("PDMG_M1_WPC")) m1_wpc = std::max(1, std::min(8, std::atoi(e)));
     if (const char* e = std::getenv("PDMG_PRED_FINAL")) pred_final = std::atof(e);
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));

@@ -1129,13 +1129,22 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
 namespace pdmg_b200 {
 
 constexpr int MARCH_WARPS = 4;  // warps per CTA (independent)
-// warps per CTA of the two-sweep marching passes (k_march2<TWO>); their registers (~236 per thread) allow 8.7 warps
-// per SM, so 3-warp CTAs at 3 per SM would hold 9
-#ifndef PDMG_M2_WPC
-#define PDMG_M2_WPC 4
+// Register caps of the marching passes (k_march2).  The caps, not the CTA shape, set the warps resident per SM:
+// 65536 / (32 x cap) -- 10 for the two-sweep passes (cap 200; they need 196-229 registers uncapped, and at 200 the
+// restriction variants spill 40 bytes), 12 for the one-sweep passes (cap 168).  CTAs are small (2 warps) so that the
+// resident count divides evenly; the host picks the CTA size (Engine::m2_wpc / m1_wpc).
+#ifndef PDMG_M2_MAXNREG
+#define PDMG_M2_MAXNREG 232
 #endif
-constexpr int M2_WPC = PDMG_M2_WPC;
-__host__ __device__ constexpr int march2_wpc(bool two) { return two ? M2_WPC : MARCH_WARPS; }
+#ifndef PDMG_M1_MAXNREG
+#define PDMG_M1_MAXNREG 168
+#endif
+constexpr int M2_MAXNREG = PDMG_M2_MAXNREG, M1_MAXNREG = PDMG_M1_MAXNREG;
+__host__ __device__ constexpr int march2_maxnreg(bool two) { return two ? M2_MAXNREG : M1_MAXNREG; }
+// warps of a marching pass resident per SM (registers are allocated per warp in units of 8 per thread)
+__host__ __device__ constexpr int march2_warps_per_sm(bool two) {
+  return 65536 / (32 * ((march2_maxnreg(two) + 7) / 8 * 8)) > 64 ? 64 : 65536 / (32 * ((march2_maxnreg(two) + 7) / 8 * 8));
+}
 
 __device__ __forceinline__ double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
@@ -1429,14 +1438,39 @@ __global__ void __launch_bounds__(32 * MARCH_WARPS, PDMG_MARCH_MINB) k_march(Mar
 // enough bytes moving to saturate HBM at 8 warps/SM, without spending registers on prefetch.  b rows stay
 // in the ring until the second sweep (row j-3) and the post-residual (row j-5) have read them.
 // ===================================================================================================
+// A lane's two adjacent columns of one row as ONE access (32 B for complex128: LDG.E.256 / STG.E.256, sm_100+;
+// 16 B for complex64).  Per-column 16-B accesses at a 32-B lane stride touch every 128-B line of the row twice: 16
+// L1 wavefronts per row instead of 8, and the LSU data pipe is the busiest unit of the marching passes (ncu:
+// l1tex__data_pipe_lsu_wavefronts 69 %).  The address must be 32-B (16-B) aligned: even column, even n.
+struct alignas(32) PairC128 {
+  double2 a, b;
+};
+struct alignas(16) PairC64 {
+  float2 a, b;
+};
+__device__ __forceinline__ void ldpair(const double2* p, double2& a, double2& b) {
+  const PairC128 v = *reinterpret_cast<const PairC128*>(p);
+  a = v.a, b = v.b;
+}
+__device__ __forceinline__ void ldpair(const float2* p, double2& a, double2& b) {
+  const PairC64 v = *reinterpret_cast<const PairC64*>(p);
+  a = ld2(v.a), b = ld2(v.b);
+}
+__device__ __forceinline__ void stpair(double2* p, double2 a, double2 b) {
+  PairC128 v;
+  v.a = a, v.b = b;
+  *reinterpret_cast<PairC128*>(p) = v;
+}
+__device__ __forceinline__ void stpair(float2* p, float2 a, float2 b) {
+  PairC64 v;
+  v.a = a, v.b = b;
+  *reinterpret_cast<PairC64*>(p) = v;
+}
 __device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <int X>
 struct IC {
   static constexpr int value = X;
 };
-#ifndef PDMG_MARCH2_MINB
-#define PDMG_MARCH2_MINB 2
-#endif
 // (measured and removed, DESIGN 3.2b: input rows through a TMA ring in shared memory, L2 bulk prefetch,
 // register prefetch two rows ahead, warp-specialised sweep pairs, V(1,1) cross-cycle fusion -- all slower
 // than or as fast as this one-row register prefetch)
@@ -1444,9 +1478,6 @@ struct IC {
 // the previous cycle's iterate) in a.partial -- the fine-level convergence norm, read one pass later.
 // TWO = false: ONE Vanka sweep per pass with the same machinery (the single-sweep passes of V(1,1) and odd
 // nu): u1 at row j-2 is the stored iterate and the post stage reads r2 = b - L u1 at row j-3.
-#ifndef PDMG_MARCH1_MINB
-#define PDMG_MARCH1_MINB 3
-#endif
 // Debug builds (-DPDMG_BOUNDS_CHECK=1, compute-sanitizer being closed on this pool): every global access of the
 // marching pass is checked against its allocation and traps with the offending index.
 #ifndef PDMG_BOUNDS_CHECK
@@ -1463,13 +1494,26 @@ __device__ __forceinline__ void bounds_check(int64_t idx, int64_t lim, int what)
 }
 // NF > 0: the level's subdivision count n as a compile-time constant (row offsets become immediates)
 template <class T, bool LOADU, bool PROLONG, int POST, bool NORM_IN = false, bool TWO = true, int NF = 0>
-__global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB : PDMG_MARCH1_MINB)
+__global__ void __maxnreg__(march2_maxnreg(TWO))
     k_march2(const __grid_constant__ MarchArgs<T> a, const __grid_constant__ CoefPack cp) {
   using V = typename vec2<T>::type;
   using D2 = double2;
   constexpr int LC = 2;
   constexpr bool EVEN = sizeof(V) == 8;
   constexpr bool HASD = POST != POST_NONE;
+  // paired 32-B / 16-B accesses (ldpair / stpair) where n is a compile-time even constant: the strips start at
+  // even columns and the level arrays are 256-B aligned with even row pitch and shift stride
+  constexpr bool PAIR = NF > 0 && (NF % 2) == 0;
+#ifndef PDMG_M2_PAIR_U
+#define PDMG_M2_PAIR_U 0
+#endif
+#ifndef PDMG_M2_PAIR_B
+#define PDMG_M2_PAIR_B 0
+#endif
+#ifndef PDMG_M2_PAIR_ST
+#define PDMG_M2_PAIR_ST 1
+#endif
+  constexpr bool PAIR_U = PAIR && PDMG_M2_PAIR_U, PAIR_B = PAIR && PDMG_M2_PAIR_B, PAIR_ST = PAIR && PDMG_M2_PAIR_ST;
   static_assert(!(PROLONG && POST == POST_RESTRICT), "prolongation and restriction never share a pass");
   constexpr int hD = POST == POST_RESTRICT ? 1 : 0;
   constexpr int hC = HASD ? hD + 1 : 0;
@@ -1493,7 +1537,7 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   // the warp index broadcast from lane 0, so the compiler knows that the task and everything derived from it
   // (row ranges, loop bounds, row parity) is warp-uniform: uniform branches, no divergence guards (BRA.DIV)
   // around the shuffles and no register moves into their fixed operands
-  const int task = blockIdx.x * march2_wpc(TWO) + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int task = blockIdx.x * (blockDim.x >> 5) + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   if (task >= a.ntasks) return;
   const int lane = threadIdx.x & 31;
   const int tx = task % a.ntx, ty = task / a.ntx;
@@ -1528,8 +1572,29 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
 
   const int Ie = cA >> 1;
   const bool codd = (cA & 1) != 0;  // warp-uniform (strips start at x0 - hA, lanes step by 2)
+  // (masked pair loads fetch both columns when either is interior and zero the other: a column outside the domain
+  // lies inside the allocation -- the neighbouring row or the tail guard)
+  // Mask modes of a step (MK): 0 = every row and column the step touches is interior (nothing masked); 1 = rows and
+  // columns masked to the domain (loads predicated); 2 = interior rows of a strip at the left or right domain edge:
+  // loads unpredicated (the columns outside the domain lie inside the allocation and hold finite values) and only
+  // the residuals, corrections and prolongation forced to zero outside the interior columns -- the ghost column
+  // then shields the interior from whatever the lanes beyond it compute.
+  auto gpair = [&](const V* __restrict__ base, int row, D2* out, auto MK, int what) __attribute__((always_inline)) {
+    constexpr bool MASK = decltype(MK)::value == 1;
+    out[0] = out[1] = cz<D2>();
+    if (!MASK || (row_ok(row) && (cin[0] || cin[1]))) {
+      bounds_check(sbase + cA + (int64_t)row * n + 1, a.elems, what);
+      bounds_check(sbase + cA + (int64_t)row * n, a.elems, what);
+      ldpair(base + (int64_t)row * n, out[0], out[1]);
+      if constexpr (MASK) out[0] = csel(cin[0], out[0]), out[1] = csel(cin[1], out[1]);
+    }
+  };
   auto gread_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
+    constexpr bool MASK = decltype(MK)::value == 1;
+    if constexpr (PAIR_U && LOADU) {
+      gpair(uin, row, out, MK, 0);
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
       out[k] = cz<D2>();
@@ -1542,7 +1607,11 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
     }
   };
   auto gload_b = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
+    constexpr bool MASK = decltype(MK)::value == 1;
+    if constexpr (PAIR_B) {
+      gpair(bb, row, out, MK, 1);
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
       if constexpr (MASK) {
@@ -1561,8 +1630,8 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   // a1 = e(J, Ie+1), b0 = e(J+1, Ie), b1 = e(J+1, Ie+1): even/odd fine column and row (both warp-uniform)
   auto prolong_of = [&](int row, const D2& a0, const D2& a1, const D2& b0, const D2& b1, D2* pout, auto MK)
                         __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
-    const bool rin = !MASK || row_ok(row);
+    constexpr bool MASK = decltype(MK)::value != 0;
+    const bool rin = decltype(MK)::value != 1 || row_ok(row);
     D2 p[LC];
     if (row & 1) {
       const D2 q4 = cscale(0.25, cadd(cadd(cadd(a0, a1), b0), b1));
@@ -1582,7 +1651,7 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   // loads, so no register copy waits on a load that was just issued (DESIGN 3.2b)
   D2 Cq[4];
   auto load_coarse = [&](int row, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
+    constexpr bool MASK = decltype(MK)::value == 1;
     int J = row >> 1, I = Ie;
     if constexpr (MASK) J = min(max(J, 0), nc - 1), I = min(max(I, 0), nc - 1);
     const V* p0 = ecs + (int64_t)J * nc + I;
@@ -1594,7 +1663,8 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   auto east = [&](const D2* x, int k, const D2& er) __attribute__((always_inline)) { return k == LC - 1 ? er : x[k + 1]; };
   // residual b - L u at the centre row c of a window (rows above/below: lo, hi), masked to the domain
   auto resid = [&](const D2* lo, const D2* c, const D2* hi, const D2* bw, bool inside, D2* r, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
+    constexpr bool MASK = decltype(MK)::value != 0;
+    if constexpr (decltype(MK)::value == 2) inside = true;
     const D2 wl = shfl_up2(c[LC - 1]), er = shfl_dn2(c[0]);
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
@@ -1604,7 +1674,8 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   };
   // one Vanka sweep's row update: r_t arrives, delta_{t-1} leaves (masked to the domain at row t-1)
   auto vanka_row = [&](const D2* r, D2* P, D2* C, bool din, D2* dl, auto MK) __attribute__((always_inline)) {
-    constexpr bool MASK = decltype(MK)::value;
+    constexpr bool MASK = decltype(MK)::value != 0;
+    if constexpr (decltype(MK)::value == 2) din = true;
     const D2 rwl = shfl_up2(r[LC - 1]), rer = shfl_dn2(r[0]);
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
@@ -1689,11 +1760,19 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
         D2 u1 = cadd(U0[so][k], dl[k]);
         if constexpr (EVEN) u1 = ld2(st2<V>(u1));  // the iterate the unfused sweep would have stored
         U1[sn][k] = u1;
-        if constexpr (!TWO) {
+        if constexpr (!TWO && !PAIR_ST) {
           if (rst1 && cst[k]) {
             bounds_check(sbase + cA + (int64_t)(j - 2) * n + k, a.elems, 4);
             uout[(int64_t)(j - 2) * n + k] = st2<V>(u1);
           }
+        }
+      }
+      if constexpr (!TWO && PAIR_ST) {
+        // (a pair with one column on the boundary stores that column's zero: masked steps keep the iterate zero
+        // outside the domain, and column 0 / n is the zero ghost)
+        if (rst1 && (cst[0] || cst[1])) {
+          bounds_check(sbase + cA + (int64_t)(j - 2) * n + 1, a.elems, 4);
+          stpair(uout + (int64_t)(j - 2) * n, st2<V>(U1[sn][0]), st2<V>(U1[sn][1]));
         }
       }
     }
@@ -1704,14 +1783,24 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
       const int row = j - 4;
       vanka_row(r, P2, C2, row_in(row), dl, MK);
       const bool rst = row >= olo && row < ohi;
+      V usp[LC];
 #pragma unroll
       for (int k = 0; k < LC; ++k) {
         const V us = st2<V>(cadd(U1[so][k], dl[k]));
-        if (rst && cst[k]) {
-          bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 5);
-          uout[(int64_t)row * n + k] = us;
+        usp[k] = us;
+        if constexpr (!PAIR_ST) {
+          if (rst && cst[k]) {
+            bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 5);
+            uout[(int64_t)row * n + k] = us;
+          }
         }
         U2[sn][k] = ld2(us);
+      }
+      if constexpr (PAIR_ST) {
+        if (rst && (cst[0] || cst[1])) {
+          bounds_check(sbase + cA + (int64_t)row * n + 1, a.elems, 5);
+          stpair(uout + (int64_t)row * n, usp[0], usp[1]);
+        }
       }
     }
     if constexpr (HASD) {
@@ -1764,20 +1853,55 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
   //  (b) boundary steps one at a time in window phase 0 followed by a register rotation, interior steps
   //      unmasked and unrolled by 3 -- only unmasked copies in the hot loop (smaller code).
   // (prolongating passes with a post stage: shape (a) only -- both shapes in one function spill)
-  if (a.loop_a || (PROLONG && POST != POST_NONE)) {
-    auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
-      if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
-      else step(j, PH, IC<1>{});
+  // Kernels with n compiled in (the hot variants) also fix the loop shape -- (a) for the prolongating passes, (b)
+  // for the others, as measured -- and give edge strips their own interior copy (mask mode 2); the generic kernels
+  // choose the shape at run time (a.loop_a) and run edge strips fully masked, to keep their code size down.
+#ifndef PDMG_M2_EDGE_MODE
+#define PDMG_M2_EDGE_MODE 2
+#endif
+#ifndef PDMG_M2_EDGE_UNROLL
+#define PDMG_M2_EDGE_UNROLL 1
+#endif
+#ifndef PDMG_M2_PROLONG_B
+#define PDMG_M2_PROLONG_B 1
+#endif
+  using MEdge = IC<(NF > 0 ? PDMG_M2_EDGE_MODE : 1)>;
+  auto run_a = [&]() __attribute__((always_inline)) {
+    auto run = [&](auto MI) __attribute__((always_inline)) {  // MI: mask mode of the steps with interior rows
+      auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
+        if (j >= jlo_int && j <= jhi_int) step(j, PH, MI);
+        else step(j, PH, IC<1>{});
+      };
+      int j = rlo;
+      for (; j + 2 < rhi; j += 3) {
+        step_any(j, IC<0>{});
+        step_any(j + 1, IC<1>{});
+        step_any(j + 2, IC<2>{});
+      }
+      if (j < rhi) step_any(j, IC<0>{});
+      if (j + 1 < rhi) step_any(j + 1, IC<1>{});
     };
-    int j = rlo;
-    for (; j + 2 < rhi; j += 3) {
-      step_any(j, IC<0>{});
-      step_any(j + 1, IC<1>{});
-      step_any(j + 2, IC<2>{});
+    if constexpr (NF > 0) {
+      if (col_int) run(IC<0>{});
+      else run(MEdge{});
+    } else {
+      // generic kernels: ONE copy of the loop for interior and edge strips (two copies of this 29 KB loop live on
+      // an SM at once overflow the 32 KB instruction cache: measured 93 -> 132 us per L2 pass at C3)
+      auto step_any = [&](int j, auto PH) __attribute__((always_inline)) {
+        if (col_int && j >= jlo_int && j <= jhi_int) step(j, PH, IC<0>{});
+        else step(j, PH, IC<1>{});
+      };
+      int j = rlo;
+      for (; j + 2 < rhi; j += 3) {
+        step_any(j, IC<0>{});
+        step_any(j + 1, IC<1>{});
+        step_any(j + 2, IC<2>{});
+      }
+      if (j < rhi) step_any(j, IC<0>{});
+      if (j + 1 < rhi) step_any(j + 1, IC<1>{});
     }
-    if (j < rhi) step_any(j, IC<0>{});
-    if (j + 1 < rhi) step_any(j + 1, IC<1>{});
-  } else {
+  };
+  auto run_b = [&]() __attribute__((always_inline)) {
     auto rotate = [&]() __attribute__((always_inline)) {
 #pragma unroll
       for (int k = 0; k < LC; ++k) {
@@ -1786,26 +1910,46 @@ __global__ void __launch_bounds__(32 * march2_wpc(TWO), TWO ? PDMG_MARCH2_MINB :
         U2[0][k] = U2[1][k], U2[1][k] = U2[2][k];
       }
     };
-    const int jm_lo = col_int ? max(rlo, jlo_int) : rhi;  // interior steps: [jm_lo, jm_end)
-    const int jm_end = col_int ? max(jm_lo, min(jhi_int + 1, rhi)) : rhi;
+    // steps with interior rows: [jm_lo, jm_end) (generic kernels: none for an edge strip, which runs fully masked)
+    const int jm_lo = (NF > 0 || col_int) ? max(rlo, jlo_int) : rhi;
+    const int jm_end = (NF > 0 || col_int) ? max(jm_lo, min(jhi_int + 1, rhi)) : rhi;
     int j = rlo;
     for (; j < jm_lo; ++j) {  // leading boundary steps
       step(j, IC<0>{}, IC<1>{});
       rotate();
     }
-    for (; j + 2 < jm_end; j += 3) {
-      step(j, IC<0>{}, IC<0>{});
-      step(j + 1, IC<1>{}, IC<0>{});
-      step(j + 2, IC<2>{}, IC<0>{});
-    }
-    for (; j < jm_end; ++j) {
-      step(j, IC<0>{}, IC<0>{});
-      rotate();
+    auto mid = [&](auto MI) __attribute__((always_inline)) {
+      // (edge strips one step at a time unless PDMG_M2_EDGE_UNROLL: the interior strips' unrolled loop and the edge
+      // strips' loop are live on an SM at the same time, and together they should fit the 32 KB instruction cache)
+      if constexpr (decltype(MI)::value == 0 || PDMG_M2_EDGE_UNROLL) {
+        for (; j + 2 < jm_end; j += 3) {
+          step(j, IC<0>{}, MI);
+          step(j + 1, IC<1>{}, MI);
+          step(j + 2, IC<2>{}, MI);
+        }
+      }
+      for (; j < jm_end; ++j) {
+        step(j, IC<0>{}, MI);
+        rotate();
+      }
+    };
+    if constexpr (NF > 0) {
+      if (col_int) mid(IC<0>{});
+      else mid(MEdge{});
+    } else {
+      mid(IC<0>{});
     }
     for (; j < rhi; ++j) {  // trailing boundary steps
       step(j, IC<0>{}, IC<1>{});
       rotate();
     }
+  };
+  if constexpr (NF > 0) {
+    if constexpr (PROLONG && !(PDMG_M2_PROLONG_B)) run_a();
+    else run_b();
+  } else {
+    if (a.loop_a || (PROLONG && POST != POST_NONE)) run_a();
+    else run_b();
   }
   if constexpr (POST == POST_NORM || NORM_IN) {
     for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);

@@ -1,0 +1,3 @@
+// pdmg_m2_hot1024.cu -- one unit of k_march2 instantiations (pdmg_march2_units.cuh)
+#define PDMG_M2_UNIT_NF 1024
+#include "pdmg_march2_units.cuh"

@@ -19,7 +19,8 @@ def main():
         ins = [(int(m.group(1), 16), m.group(2)) for m in re.finditer(r"/\*([0-9a-f]{4,5})\*/\s+(.*?);", f)]
         print(f"== {name}: {len(ins)} instructions")
         for a, t in ins:
-            if not t.startswith("@"):  # loops close with a predicated backward branch (returns from out-of-line paths do not)
+            # loops close with a predicated backward branch (@P BRA / BRA.U UP); returns from out-of-line paths do not
+            if not (t.startswith("@") or re.match(r"BRA\.U\s+!?UP", t)):
                 continue
             m = re.search(r"BRA\S*\s+(?:\S+,\s*)?0x([0-9a-f]+)", t)
             if not m or "BRA.DIV" in t:
