@@ -206,6 +206,13 @@ struct Engine : EngineBase {
     k_copy_words<<<std::max(blocks, 1), 256, 0, stream>>>((const uint32_t*)dsrc, (uint32_t*)(d_map + map_off), w);
   }
   cudaEvent_t ev_nactive[2] = {nullptr, nullptr};
+  // rolling host solve (solve_rolling): per-shift cycle counters and final-buffer indices, the identity table k_pack
+  // reads them through, the round's active flags in mapped memory (two slots of S ints after the counts)
+  int *d_kcur = nullptr, *d_fbuf = nullptr, *d_ident = nullptr;
+  bool rolling = false;
+  int roll_slot = 0;
+  cudaStream_t out_stream = nullptr;
+  size_t map_flags() const { return map_nact() + 8 * sizeof(int); }
   int n_active_host = 0;
   const KernelTable<T>* table = nullptr;
   int march_min_n = 64;  // levels with n >= this use the warp-marching sweep kernel (0 = never)
@@ -380,6 +387,10 @@ struct Engine : EngineBase {
     cudaFree(d_conv);
     cudaFree(d_nactive);
     cudaFree(d_parity);
+    cudaFree(d_kcur);
+    cudaFree(d_fbuf);
+    cudaFree(d_ident);
+    if (out_stream) cudaStreamDestroy(out_stream);
     cudaFree(d_ones);
     cudaFree(d_r0);
     cudaFree(d_hist);
@@ -427,6 +438,10 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_MARCH2_MIN_N")) march2_min_n = std::atoi(e);  // (tuning)
     if (const char* e = std::getenv("PDMG_MARCH_MIN_N")) march_min_n = std::atoi(e);    // (tuning)
     if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_IO_MODE")) io_mode = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_ROLL_LANES")) roll_lanes = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_ROLL_AHEAD")) roll_lookahead = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_ROLL_PIECE")) roll_piece = std::atoi(e);
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
     auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
       out.clear();
@@ -570,7 +585,13 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&d_norms, sizeof(double) * S));
     std::vector<int> ones(S, 1);
     CK(cudaMemcpyAsync(d_ones, ones.data(), sizeof(int) * S, cudaMemcpyHostToDevice, stream));
-    CK(cudaHostAlloc((void**)&h_map, map_nact() + 6 * sizeof(int), cudaHostAllocMapped));
+    CK(cudaMalloc(&d_kcur, sizeof(int) * S));
+    CK(cudaMalloc(&d_fbuf, sizeof(int) * S));
+    CK(cudaMalloc(&d_ident, sizeof(int) * 2));
+    const int ident[2] = {0, 1};
+    CK(cudaMemcpyAsync(d_ident, ident, sizeof(ident), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));  // (ident is a stack array)
+    CK(cudaHostAlloc((void**)&h_map, map_flags() + 2 * sizeof(int) * (size_t)S, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&d_map, h_map, 0));
     CK(cudaEventCreateWithFlags(&ev_nactive[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_nactive[1], cudaEventDisableTiming));
@@ -770,6 +791,16 @@ struct Engine : EngineBase {
   // wait = false the host does not block: the solve loop enqueues cycle k+1 before reading cycle k's count
   // (converged shifts are frozen on the device, so a speculative extra cycle leaves them untouched).
   void finalize(int k, int ntiles, bool wait = true, int cur = 0) {
+    if (rolling) {  // per-shift counters; the round's active flags go to the host (slot roll_slot)
+      const int slot = roll_slot;
+      CK(cudaMemsetAsync(d_nactive + slot, 0, sizeof(int), stream));
+      SolveState st{d_active, d_iters, d_conv, d_r0, d_hist, d_nactive + slot, S, cfg.max_iter, cfg.tol, nullptr, cur, nullptr};
+      const int threads = 256, blocks = (S * 32 + threads - 1) / threads;
+      timed("finalize", 0.0, [&] { k_finalize_roll<<<blocks, threads, 0, stream>>>(d_partial, ntiles, st, d_kcur, d_fbuf); });
+      to_host(d_active, map_flags() + sizeof(int) * (size_t)S * slot, sizeof(int) * (size_t)S);
+      CK(cudaEventRecord(ev_nactive[slot], stream));
+      return;
+    }
     const int slot = k & 1;
     unsigned long long* d_pred = reinterpret_cast<unsigned long long*>(d_nactive + 2) + slot;
     CK(cudaMemsetAsync(d_nactive + slot, 0, sizeof(int), stream));
@@ -922,7 +953,9 @@ struct Engine : EngineBase {
   }
 
   // Copy the per-shift report back; counts the smoother updates performed (sum over shifts of cycles).
-  void finish_report(pdmg_solve_report* rep, std::chrono::steady_clock::time_point t0, int H) {
+  // own: only the shifts with own[s] != 0 are this engine's (a lane of the rolling solve)
+  void finish_report(pdmg_solve_report* rep, std::chrono::steady_clock::time_point t0, int H,
+                     const std::vector<char>* own = nullptr) {
     to_host(d_iters, map_iters(), sizeof(int) * S);
     to_host(d_conv, map_conv(), sizeof(int) * S);
     const bool need_hist = rep && (rep->residual_history || rep->rate);
@@ -940,10 +973,12 @@ struct Engine : EngineBase {
       if (cfg.cycle == PDMG_CYCLE_W) visits *= 2;
     }
     double cycles_done = 0.0;
-    for (int s = 0; s < S; ++s) cycles_done += it[s];
+    for (int s = 0; s < S; ++s)
+      if (!own || (*own)[s]) cycles_done += it[s];
     last_updates = per_cycle * cycles_done;
     if (rep) {
       for (int s = 0; s < S; ++s) {
+        if (own && !(*own)[s]) continue;
         if (rep->iterations) rep->iterations[s] = it[s];
         if (rep->converged) rep->converged[s] = (uint8_t)cv[s];
         if (rep->residual_history)
@@ -1032,7 +1067,8 @@ struct Engine : EngineBase {
 
   cudaStream_t copy_stream = nullptr;
   int io_chunks = 0;  // 0 = automatic
-  int io_mode = 1;    // 1: chunks solve concurrently on sub-engines (own streams, priorities); 0: one stream
+  int io_mode = 2;    // 2: rolling batch (solve_rolling); 1: chunks solve concurrently on sub-engines (own streams,
+                      // priorities); 0: chunks on one stream (PDMG_IO_MODE)
   int stream_priority = 0;
   // sub-engine of a concurrent host solve: its level arrays are the shift range [borrow_s0, borrow_s0 + S)
   // of the parent engine's (a contiguous block of the shift-major storage), not allocations of its own
@@ -1090,6 +1126,7 @@ struct Engine : EngineBase {
     // chunks minimise exposed copy + overhead: 62 ms (4 equal) -> ~55 ms for C3 (serial: 78 ms).
     const bool auto_split = io_chunks <= 0;
     int nch = io_chunks > 0 ? io_chunks : (N * sizeof(double2) >= ((size_t)256 << 20) && S >= 8 ? 3 : 1);
+    if (io_mode == 2 && io_chunks <= 0 && roll_piece > 0) nch = std::max(nch, 2);
     nch = std::max(1, std::min(nch, S));
     auto pinned = [](const void* p) {
       cudaPointerAttributes a{};
@@ -1105,7 +1142,7 @@ struct Engine : EngineBase {
         const char* e = std::getenv("PDMG_PAGEABLE");
         return !(e && std::atoi(e) == 0);
       }();
-      if (stage_on && io_mode == 1) staged = true;
+      if (stage_on && io_mode >= 1) staged = true;
       else nch = 1;
     }
     if (nch == 1) {
@@ -1117,7 +1154,11 @@ struct Engine : EngineBase {
     }
     const auto t0 = std::chrono::steady_clock::now();
     if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-    if (io_mode == 1 && solve_concurrent(b, u, rep, st, N, per, staged)) {
+    if (io_mode == 2 && io_chunks <= 0 && solve_rolling(b, u, rep, st, N, per, staged)) {
+      if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return;
+    }
+    if (io_mode >= 1 && solve_concurrent(b, u, rep, st, N, per, staged)) {
       if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       return;
     }
@@ -1282,6 +1323,319 @@ struct Engine : EngineBase {
       CK(cudaEventSynchronize(B.ev[pend_k]));
       parallel_memcpy((char*)dst + pend_o, B.buf[pend_k], pend_len);
     }
+  }
+
+  // Rolling host solve: shifts join the batch as their right-hand sides arrive (pieces of ~32 MB on the copy
+  // stream) and leave it as they converge (packed and copied back on an output stream while the others keep
+  // cycling).  Every round is one multigrid cycle over the shifts active at that moment; each shift carries its own
+  // cycle counter (k_finalize_roll), so its iterates, history and cycle count are those of the batch solve.
+  // Compared with solving chunks on sub-engines, the GPU always works on everything that has arrived and results
+  // start flowing back after the first shifts' last cycle instead of after a whole chunk.  The pieces are dealt
+  // round-robin to `roll_lanes` lanes -- this engine and lane engines that work in the same level arrays (disjoint
+  // shifts) on their own streams and host threads -- so that one lane's latency-bound coarse levels overlap the
+  // other's fine-level passes.  Needs the norm-next scheme (the first fine pass of a round forms the convergence
+  // norm); otherwise the chunked pipelines below run.
+  int roll_lanes = 2;      // PDMG_ROLL_LANES
+  int roll_piece = 0;      // shifts per piece (0 = ~32 MB); > 0 also takes small batches through the rolling solve (tests)
+  int roll_lookahead = 0;  // pieces admitted ahead of their copy's completion (the stream waits for them), PDMG_ROLL_AHEAD
+  std::vector<std::unique_ptr<Engine<T>>> lanes;
+  struct RollShared {
+    const pdmg_c128* b;
+    pdmg_c128* u;
+    pdmg_solve_report* rep;
+    double2* st;
+    size_t N;
+    int64_t per;
+    bool staged;
+    std::vector<int> plo;  // piece p = shifts [plo[p], plo[p + 1])
+    std::vector<cudaEvent_t> in;
+    std::mutex mu;
+    std::condition_variable cv;
+    int in_ready = 0;
+    std::exception_ptr in_err;
+    std::chrono::steady_clock::time_point t0;
+  };
+  bool build_lanes(int nl) {
+    if ((int)lanes.size() + 1 == nl) {
+      for (auto& e : lanes) e->solve_path = solve_path, e->profiling = profiling;
+      return true;
+    }
+    lanes.clear();
+    std::vector<pdmg_c128> lam(S);
+    for (int s = 0; s < S; ++s) lam[s] = pdmg_c128{lambdas[s].real(), lambdas[s].imag()};
+    for (int l = 1; l < nl; ++l) {
+      auto e = std::make_unique<Engine<T>>();
+      pdmg_batch_desc d = desc_;
+      d.n_shifts = S;
+      d.lambdas = lam.data();
+      e->device = -1;
+      e->setup_host(d);
+      e->borrow = this;
+      e->borrow_s0 = 0;
+      e->setup_device(device);
+      e->solve_path = solve_path;
+      e->profiling = profiling;
+      lanes.push_back(std::move(e));
+    }
+    return true;
+  }
+
+  bool solve_rolling(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep, double2* st, size_t N, int64_t per,
+                     bool staged) {
+    if (!use_norm_next() || any_singular || use_small_path() || cfg.max_iter < 1) return false;
+    RollShared sh;
+    sh.b = b, sh.u = u, sh.rep = rep, sh.st = st, sh.N = N, sh.per = per, sh.staged = staged;
+    sh.t0 = std::chrono::steady_clock::now();
+    // pieces of whole shifts, ~32 MB each (C3: 8 shifts)
+    const int pshift = roll_piece > 0 ? std::min(roll_piece, S)
+                                      : (int)std::max<int64_t>(1, std::min<int64_t>(S, (int64_t)(kStagePiece / (per * sizeof(double2)))));
+    for (int s = 0; s < S; s += pshift) sh.plo.push_back(s);
+    const int np = (int)sh.plo.size();
+    sh.plo.push_back(S);
+    const int nl = std::max(1, std::min(std::min(roll_lanes, 4), np));
+    if (!build_lanes(nl)) return false;
+    sh.in.resize(np);
+    for (auto& e : sh.in) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // ---- input: all pieces queue on the copy stream (pageable: through the pinned bounce ring, on a thread) ----
+    std::thread in_thread;
+    if (staged) {
+      if (!bounce_in) bounce_in = std::make_unique<Bounce>();
+      bounce_in->ensure(kStageRing);
+      in_thread = std::thread([&] {
+        try {
+          CK(cudaSetDevice(device));
+          for (int p = 0; p < np; ++p) {
+            staged_h2d(st + sh.plo[p] * per, b + sh.plo[p] * per, sizeof(double2) * per * (sh.plo[p + 1] - sh.plo[p]),
+                       copy_stream);
+            CK(cudaEventRecord(sh.in[p], copy_stream));
+            std::lock_guard<std::mutex> lk(sh.mu);
+            sh.in_ready = p + 1;
+            sh.cv.notify_all();
+          }
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(sh.mu);
+          sh.in_err = std::current_exception();
+          sh.in_ready = np;
+          sh.cv.notify_all();
+        }
+      });
+    } else {
+      for (int p = 0; p < np; ++p) {
+        CK(cudaMemcpyAsync(st + sh.plo[p] * per, b + sh.plo[p] * per, sizeof(double2) * per * (sh.plo[p + 1] - sh.plo[p]),
+                           cudaMemcpyHostToDevice, copy_stream));
+        CK(cudaEventRecord(sh.in[p], copy_stream));
+      }
+      sh.in_ready = np;
+    }
+    std::vector<std::exception_ptr> err(nl);
+    std::vector<std::thread> th;
+    for (int l = 1; l < nl; ++l)
+      th.emplace_back([&, l] {
+        try {
+          CK(cudaSetDevice(device));
+          lanes[l - 1]->roll_lane(sh, l, nl);
+        } catch (...) {
+          err[l] = std::current_exception();
+        }
+      });
+    try {
+      roll_lane(sh, 0, nl);
+    } catch (...) {
+      err[0] = std::current_exception();
+    }
+    for (auto& t : th) t.join();
+    if (in_thread.joinable()) in_thread.join();
+    cudaStreamSynchronize(copy_stream);
+    for (auto e : sh.in) cudaEventDestroy(e);
+    for (auto& x : err)
+      if (x) std::rethrow_exception(x);
+    if (sh.in_err) std::rethrow_exception(sh.in_err);
+    for (auto& e : lanes) {  // (each lane drained its own events at the end of its solve)
+      last_updates += e->last_updates, launches += e->launches, e->launches = 0;
+      for (auto& kv : e->stats) {
+        Stat& q = stats[kv.first];
+        q.launches += kv.second.launches, q.ms += kv.second.ms, q.bytes += kv.second.bytes;
+        q.ubytes += kv.second.ubytes, q.updates += kv.second.updates;
+      }
+      e->stats.clear();
+    }
+    return true;
+  }
+
+  // One lane of the rolling solve: pieces lane, lane + nl, ... of sh (this engine's streams; the level arrays may be
+  // a parent's, shared with the other lanes, which touch other shifts).
+  void roll_lane(RollShared& sh, int lane, int nl) {
+    Level& F = lv[0];
+    const int H = cfg.max_iter + 1;
+    const int64_t per = sh.per;
+    const size_t N = sh.N;
+    double2* st = sh.st;
+    const bool staged = sh.staged;
+    const int np = (int)sh.in.size();
+    static const bool dbg = std::getenv("PDMG_IO_DEBUG") != nullptr;
+    if (!out_stream) CK(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+    std::vector<int> mine;  // this lane's pieces, in arrival order
+    for (int p = lane; p < np; p += nl) mine.push_back(p);
+    const int nm = (int)mine.size();
+    int n_mine = 0;
+    for (int p : mine) n_mine += sh.plo[p + 1] - sh.plo[p];
+    // ---- output: finished runs of shifts are packed on the output stream; pinned destinations are copied there,
+    // pageable ones by an output thread through two pinned bounce pieces ----
+    struct OutItem {
+      int s0, s1;
+      cudaEvent_t packed;
+    };
+    std::mutex out_mu;
+    std::condition_variable out_cv;
+    std::vector<OutItem> out_q;
+    bool out_stop = false;
+    std::exception_ptr out_err;
+    std::thread out_thread;
+    if (staged) {
+      if (!bounce_out) bounce_out = std::make_unique<Bounce>();
+      bounce_out->ensure(2);
+      out_thread = std::thread([&] {
+        try {
+          CK(cudaSetDevice(device));
+          cudaStream_t ds;
+          CK(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+          for (size_t next = 0;;) {
+            OutItem it;
+            {
+              std::unique_lock<std::mutex> lk(out_mu);
+              out_cv.wait(lk, [&] { return out_stop || next < out_q.size(); });
+              if (next >= out_q.size()) break;
+              it = out_q[next++];
+            }
+            CK(cudaStreamWaitEvent(ds, it.packed, 0));
+            staged_d2h(sh.u + it.s0 * per, st + N + it.s0 * per, sizeof(double2) * per * (it.s1 - it.s0), ds, *bounce_out);
+          }
+          CK(cudaStreamSynchronize(ds));
+          cudaStreamDestroy(ds);
+        } catch (...) {
+          out_err = std::current_exception();
+        }
+      });
+    }
+    std::vector<cudaEvent_t> packed_events;
+    auto emit = [&](int s0, int s1, cudaEvent_t after) {
+      CK(cudaStreamWaitEvent(out_stream, after, 0));
+      const int64_t total = (int64_t)(s1 - s0) * per;
+      const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+      k_pack<T><<<blocks, 256, 0, out_stream>>>(F.u[0] + (int64_t)s0 * F.ss, F.u[1] + (int64_t)s0 * F.ss, d_fbuf + s0,
+                                                 d_ident, st + N + s0 * per, F.n, F.ss, total);
+      ++launches;
+      if (!staged) {
+        CK(cudaMemcpyAsync(sh.u + s0 * per, st + N + s0 * per, sizeof(double2) * total, cudaMemcpyDeviceToHost, out_stream));
+      } else {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, out_stream));
+        packed_events.push_back(e);
+        std::lock_guard<std::mutex> lk(out_mu);
+        out_q.push_back({s0, s1, e});
+        out_cv.notify_all();
+      }
+    };
+    // ---- the rounds ----
+    CK(cudaMemsetAsync(d_active, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_iters, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_conv, 0, sizeof(int) * S, stream));
+    CK(cudaMemsetAsync(d_hist, 0, sizeof(double) * S * (size_t)H, stream));
+    F.cur = 0;
+    enum : char { WAITING = 0, ACTIVE = 1, DONE = 2 };
+    std::vector<char> state(S, WAITING);
+    int admitted = 0, n_active = 0, n_done = 0, round = 0;
+    std::exception_ptr err;
+    rolling = true;
+    try {
+      while (n_done < n_mine) {
+        // admit the pieces whose copies have landed, plus roll_lookahead more whose copies are queued (the stream
+        // waits for those: the round being enqueued starts about one round from now); with nothing active, wait
+        int ahead = 0;
+        for (; admitted < nm;) {
+          const int p = mine[admitted];
+          {
+            std::unique_lock<std::mutex> lk(sh.mu);
+            if (sh.in_ready <= p) {
+              if (n_active > 0) break;
+              sh.cv.wait(lk, [&] { return sh.in_ready > p; });
+            }
+            if (sh.in_err) std::rethrow_exception(sh.in_err);
+          }
+          if (n_active > 0 && cudaEventQuery(sh.in[p]) != cudaSuccess) {
+            (void)cudaGetLastError();
+            if (ahead >= roll_lookahead) break;
+            ++ahead;
+          }
+          const int s0 = sh.plo[p], s1 = sh.plo[p + 1];
+          CK(cudaStreamWaitEvent(stream, sh.in[p], 0));
+          {
+            const int64_t total = (int64_t)(s1 - s0) * per;
+            const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+            timed("unpack", (double)total * 2 * sizeof(V), [&] {
+              k_unpack<T><<<blocks, 256, 0, stream>>>(st + s0 * per, F.b + (int64_t)s0 * F.ss, F.n, F.ss, total);
+            });
+          }
+          CK(cudaMemsetAsync(F.u[F.cur] + (int64_t)s0 * F.ss, 0, sizeof(V) * (size_t)F.ss * (s1 - s0), stream));
+          k_admit<<<1, 256, 0, stream>>>(d_active, d_kcur, s0, s1);
+          ++launches;
+          for (int s = s0; s < s1; ++s) state[s] = ACTIVE;
+          n_active += s1 - s0;
+          ++admitted;
+        }
+        // one cycle over the active shifts; its first fine pass forms their convergence norms and k_finalize_roll
+        // retires the shifts that are done before the rest of the cycle runs
+        roll_slot = round & 1;
+        nin_k = 0;
+        F.uzero = false;
+        cycle_level(0, false, d_active, n_active, false);
+        // flags of this round (the GPU is still in the previous round's tail or this round's first pass)
+        CK(cudaEventSynchronize(ev_nactive[roll_slot]));
+        const volatile int* fl = (const volatile int*)(h_map + map_flags() + sizeof(int) * (size_t)S * roll_slot);
+        for (int s = 0; s < S;) {
+          if (!(state[s] == ACTIVE && fl[s] == 0)) {
+            ++s;
+            continue;
+          }
+          int e = s;
+          while (e < S && state[e] == ACTIVE && fl[e] == 0) state[e++] = DONE;
+          emit(s, e, ev_nactive[roll_slot]);
+          n_done += e - s, n_active -= e - s;
+          s = e;
+        }
+        if (dbg)
+          std::fprintf(stderr, "pdmg rolling lane %d round %d: %.2f ms admitted %d/%d active %d done %d\n", lane, round,
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - sh.t0).count(),
+                       admitted, nm, n_active, n_done);
+        ++round;
+      }
+    } catch (...) {
+      err = std::current_exception();
+    }
+    rolling = false;
+    nin_k = -1;
+    if (out_thread.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(out_mu);
+        out_stop = true;
+      }
+      out_cv.notify_all();
+      out_thread.join();
+    }
+    if (!err) {
+      try {
+        finish_report(sh.rep, sh.t0, H, &state);
+        CK(cudaStreamSynchronize(out_stream));
+      } catch (...) {
+        err = std::current_exception();
+      }
+    } else {
+      cudaStreamSynchronize(stream), cudaStreamSynchronize(out_stream);
+    }
+    for (auto e : packed_events) cudaEventDestroy(e);
+    if (err) std::rethrow_exception(err);
+    if (out_err) std::rethrow_exception(out_err);
   }
 
   bool solve_concurrent(const pdmg_c128* b, pdmg_c128* u, pdmg_solve_report* rep, double2* st, size_t N, int64_t per,

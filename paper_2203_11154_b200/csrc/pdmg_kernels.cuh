@@ -728,6 +728,47 @@ static __global__ void k_finalize(const double* __restrict__ partial, int ntiles
   }
 }
 
+// ---- rolling host solve (Engine::solve_rolling) -------------------------------------------------------------------
+// Shifts join the batch as their right-hand sides arrive from the host and leave it as they converge, so every shift
+// carries its own cycle counter: kcur[s] = cycles completed = index of the iterate whose residual norm the coming
+// round's first fine pass forms (norm-next).  k_admit starts shifts [s0, s1); k_finalize_roll is k_finalize with the
+// per-shift counter: it also records, for a shift that stops, which u buffer holds its final iterate (fbuf[s] = the
+// buffer the first pass read).
+static __global__ void k_admit(int* __restrict__ active, int* __restrict__ kcur, int s0, int s1) {
+  for (int s = s0 + blockIdx.x * blockDim.x + threadIdx.x; s < s1; s += gridDim.x * blockDim.x) active[s] = 1, kcur[s] = 0;
+}
+static __global__ void k_finalize_roll(const double* __restrict__ partial, int ntiles, SolveState st,
+                                       int* __restrict__ kcur, int* __restrict__ fbuf) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= st.S) return;
+  const int s = warp;
+  if (st.active[s] == 0) return;
+  double acc = 0.0;
+  for (int t = lane; t < ntiles; t += 32) acc += partial[(int64_t)s * ntiles + t];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane != 0) return;
+  const double r = sqrt(acc);
+  const int H = st.max_iter + 1, k = kcur[s];
+  int act = 1;
+  st.hist[(int64_t)s * H + k] = r;
+  st.iterations[s] = k;
+  if (k == 0) {  // multigrid.cpp:91-94
+    st.r0[s] = r;
+    if (r == 0.0 || st.tol >= 1.0) st.converged[s] = 1, act = 0;
+  } else if (r <= st.tol * st.r0[s]) {  // multigrid.cpp:96-105
+    st.converged[s] = 1, act = 0;
+  } else if (k >= st.max_iter) {
+    act = 0;
+  }
+  st.active[s] = act;
+  if (act) {
+    kcur[s] = k + 1;
+    atomicAdd(st.n_active, 1);
+  } else {
+    fbuf[s] = st.cur;
+  }
+}
+
 // Device -> mapped pinned host words, written by SMs over PCIe: small result copies that never queue
 // behind bulk transfers on the copy engines (the chunked host solve keeps those busy).
 static __global__ void k_copy_words(const uint32_t* __restrict__ src, volatile uint32_t* dst, int64_t n) {

@@ -396,6 +396,53 @@ def test_chunked_host_solve_marching_passes(oracle, monkeypatch, chunks):
         assert r.iterations == q.iterations and list(r.residual_history) == list(q.residual_history)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("cyc,lanes,pageable", [((2, 2), 2, False), ((2, 2), 1, True), ((1, 1), 2, False), ((2, 1), 3, True)])
+def test_rolling_host_solve_matches_batch(oracle, monkeypatch, cyc, lanes, pageable):
+    """The rolling host solve (shifts join the batch as their right-hand sides arrive and leave it as they converge,
+    each with its own cycle counter; pieces dealt to lanes that share the level arrays): bitwise the batch solve's
+    iterates, identical cycle counts and residual histories, and the oracle's cycle counts (multigrid.cpp:85-110).
+    Shifts with different cycle counts leave in different rounds; one right-hand side is zero (leaves at once)."""
+    import ctypes
+
+    from paper_2203_11154_b200 import _native as N
+
+    n, S = 256, 9
+    lams = np.array(oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, 256))[[0, 1, 3, 40, 77, 128, 200, 254, 255]]
+    lams[2], lams[6] = 1.0e6, 3.0e4 + 2.0e5j  # strongly shifted systems: fewer cycles, so they leave the batch early
+    cfg = mgcfg(Cfg(nu1=cyc[0], nu2=cyc[1]))
+    b = P.random_rhs(n, 8, count=S)
+    b[5] = 0.0
+    monkeypatch.setenv("PDMG_PRED_FINAL", "0")  # every norm of the batch solve through the same fused pass
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        u_ref, reps_ref = H.solve(b)
+    assert len({r.iterations for r in reps_ref}) > 2
+    monkeypatch.setenv("PDMG_ROLL_PIECE", "2")
+    monkeypatch.setenv("PDMG_ROLL_LANES", str(lanes))
+    with P.BatchedMultigridHierarchy(P.Grid2D(n), lams, cfg) as H:
+        if pageable:
+            u, reps = H.solve(b)
+        else:
+            nbytes = b.nbytes
+            hb, hu = N.lib().pdmg_host_alloc(nbytes), N.lib().pdmg_host_alloc(nbytes)
+            try:
+                ctypes.memmove(hb, b.ctypes.data, nbytes)
+                rep, it, cv, hist, rate = H._report_bufs()
+                assert N.lib().pdmg_solve(H._h, hb, hu, ctypes.byref(rep)) == 0, N.lib().pdmg_last_error()
+                u = np.empty_like(b)
+                ctypes.memmove(u.ctypes.data, hu, nbytes)
+                reps = H._reports(rep, it, cv, hist, rate)
+            finally:
+                N.lib().pdmg_host_free(hb)
+                N.lib().pdmg_host_free(hu)
+    assert np.array_equal(u, u_ref)
+    for r, q in zip(reps, reps_ref):
+        assert r.iterations == q.iterations and r.converged == q.converged
+        assert list(r.residual_history) == list(q.residual_history)
+    ref = oracle.solve_batch(n, lams, Cfg(nu1=cyc[0], nu2=cyc[1]), b, threads=8)
+    assert [r.iterations for r in reps] == list(ref["iterations"])
+
+
 def test_device_list_matches_single_device(oracle):
     """One context sharded over a device list (three shards sharing GPU 0, chunks of ceil(S / 3),
     paradiag.cpp:222): host solve, device-resident shard solve, cycle and level operators are bitwise the
