@@ -238,10 +238,18 @@ struct Engine : EngineBase {
   static int march2_ha(int post, bool two) {  // = k_march2's hA
     return ((two ? 4 : 2) + (post == POST_RESTRICT ? 2 : post == POST_NORM ? 1 : 0) + 1) & ~1;
   }
-  int march2_tasks(int n, int post, bool two, bool prolong) const {  // warp tasks per shift of a k_march2 pass
-    const int wout = 64 - 2 * march2_ha(post, two), hs = march2_hs_for(n, prolong, post, two);
-    return ((n + wout - 1) / wout) * ((n + hs - 1) / hs);
+  // strips across a row of a k_march2 pass: 64 columns each, WOUT = 64 - 2 hA apart, the last one ending at the
+  // domain edge (k_march2's sA)
+  static int march2_ntx(int n, int ha) {
+    const int wout = 64 - 2 * ha;
+    return n <= 64 ? 1 : 1 + (n - 64 + wout - 1) / wout;
   }
+  int march2_tasks(int n, int post, bool two, bool prolong) const {  // warp tasks per shift of a k_march2 pass
+    const int hs = march2_hs_for(n, prolong, post, two);
+    return march2_ntx(n, march2_ha(post, two)) * ((n + hs - 1) / hs);
+  }
+  int wave_S = 0;  // shifts the wave model sizes a pass for (0 = the batch; the rolling solve sets its active count)
+  bool roll_adapt = false;  // rolling solve: strip heights from the active count of each round (PDMG_ROLL_ADAPT)
   static constexpr int kMinStrip = 16;  // smallest strip height the wave model may pick (partial-buffer sizing)
   int sm_count = 148;
   // Strip height of a k_march2 pass.  The measured defaults (128 rows for n >= 512, 64 for n = 256, 32 below;
@@ -254,11 +262,11 @@ struct Engine : EngineBase {
     for (auto& e : prolong ? march2_hs_p : march2_hs_r)
       if (e.first == n) return e.second;
     const int def = n >= 512 ? 128 : n >= 256 ? 64 : 32;
-    const int ha = march2_ha(post, two), ntx = (n + 63 - 2 * ha) / (64 - 2 * ha);
+    const int ha = march2_ha(post, two), ntx = march2_ntx(n, ha);
     const int wpc = two ? m2_wpc : m1_wpc;
     const int64_t slots = (int64_t)sm_count * (march2_warps_per_sm(two) / wpc);
     auto cost = [&](int hs) {
-      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + wpc - 1) / wpc) * S;
+      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + wpc - 1) / wpc) * (wave_S > 0 ? wave_S : S);
       return (double)((ctas + slots - 1) / slots) * (hs + 2 * ha);
     };
     int best = def;
@@ -306,11 +314,10 @@ struct Engine : EngineBase {
     ma.nc = (l + 1 < (int)lv.size()) ? lv[l + 1].n : Lv.n / 2;
     ma.ss = Lv.ss, ma.ssc = (l + 1 < (int)lv.size()) ? lv[l + 1].ss : 0;
     ma.elems = Lv.alloc_left, ma.elems_c = (l + 1 < (int)lv.size()) ? lv[l + 1].alloc_left : 0;
-    const int wout = 64 - 2 * march2_ha(post, two);
     ma.Hs = march2_hs_for(Lv.n, prolong, post, two);
     // loop shape (a) for prolongating passes unless march2_prolong_b (measured, DESIGN 3.2b)
     ma.loop_a = Lv.n < march2_loopb_min_n || (prolong && !march2_prolong_b);
-    ma.ntx = (Lv.n + wout - 1) / wout;
+    ma.ntx = march2_ntx(Lv.n, march2_ha(post, two));
     ma.ntasks = ma.ntx * ((Lv.n + ma.Hs - 1) / ma.Hs);
     if (ma.ntasks != march2_tasks(Lv.n, post, two, prolong)) throw std::logic_error("pdmg_b200: march2 task count");
     const int key2 = March2Table<T>::key(loadu, prolong, post, norm_in);
@@ -442,6 +449,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_ROLL_LANES")) roll_lanes = std::atoi(e);
     if (const char* e = std::getenv("PDMG_ROLL_AHEAD")) roll_lookahead = std::atoi(e);
     if (const char* e = std::getenv("PDMG_ROLL_PIECE")) roll_piece = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_ROLL_ADAPT")) roll_adapt = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
     auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
       out.clear();
@@ -566,8 +574,8 @@ struct Engine : EngineBase {
       for (int post : {POST_NONE, POST_NORM, POST_RESTRICT}) {
         maxtiles = std::max(maxtiles, march_tasks((int)l, post));
         for (int two = 0; two < 2; ++two) {  // (any strip height the wave model may pick, any batch size)
-          const int n = lv[l].n, wout = 64 - 2 * march2_ha(post, two != 0);
-          maxtiles = std::max(maxtiles, ((n + wout - 1) / wout) * ((n + kMinStrip - 1) / kMinStrip));
+          const int n = lv[l].n;
+          maxtiles = std::max(maxtiles, march2_ntx(n, march2_ha(post, two != 0)) * ((n + kMinStrip - 1) / kMinStrip));
           for (int pr = 0; pr < 2; ++pr) maxtiles = std::max(maxtiles, march2_tasks(n, post, two != 0, pr != 0));
         }
       }
@@ -1587,6 +1595,7 @@ struct Engine : EngineBase {
         // one cycle over the active shifts; its first fine pass forms their convergence norms and k_finalize_roll
         // retires the shifts that are done before the rest of the cycle runs
         roll_slot = round & 1;
+        wave_S = roll_adapt ? std::max(1, n_active) : 0;
         nin_k = 0;
         F.uzero = false;
         cycle_level(0, false, d_active, n_active, false);
@@ -1614,6 +1623,7 @@ struct Engine : EngineBase {
       err = std::current_exception();
     }
     rolling = false;
+    wave_S = 0;
     nin_k = -1;
     if (out_thread.joinable()) {
       {

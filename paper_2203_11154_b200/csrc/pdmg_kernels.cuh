@@ -145,6 +145,19 @@ __device__ __forceinline__ double2 cmad2(double2 k0, double2 x, double2 k1, doub
   return make_double2(re, im);
 }
 
+// a + k0 x + k1 y (complex): the accumulator starts the FMA chains
+__device__ __forceinline__ double2 cmad2_acc(double2 a, double2 k0, double2 x, double2 k1, double2 y) {
+  double re = fma(k0.x, x.x, a.x);
+  re = fma(-k0.y, x.y, re);
+  re = fma(k1.x, y.x, re);
+  re = fma(-k1.y, y.y, re);
+  double im = fma(k0.x, x.y, a.y);
+  im = fma(k0.y, x.x, im);
+  im = fma(k1.x, y.y, im);
+  im = fma(k1.y, y.x, im);
+  return make_double2(re, im);
+}
+
 // Per (level, shift) operator coefficients, precomputed on the host in fp64 (multigrid.cpp:47-58).
 struct LevelCoef {
   double2 d;      // 4 + eta, eta = lambda h^2              (grid.cpp:73)
@@ -1583,9 +1596,16 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   const int lane = threadIdx.x & 31;
   const int tx = task % a.ntx, ty = task / a.ntx;
   const int n = NF ? NF : a.n, m = n - 1, Hs = a.Hs, nc = NF ? NF / 2 : a.nc;
-  const int x0 = tx * WOUT, r0 = ty * Hs;
+  // Strip tx covers the 64 columns from sA = min(tx * WOUT, n - 64): the first strip starts at the ghost column 0
+  // and the last one ends at the domain edge (no lanes spent beyond it), the others sit WOUT apart.  It stores
+  // columns [xlo, xhi): its 64 columns less hA on each side, up to the domain edge for the first and last strips.
+  // ntx = 1 + ceil((n - 64) / WOUT) strips cover a row (Engine::march2_ntx): 9 instead of 10 for the prolongating
+  // pair at n = 512.
+  const int r0 = ty * Hs;
+  const int sA = min(tx * WOUT, max(((n + 1) & ~1) - 32 * LC, 0));
+  const int xlo = tx == 0 ? 0 : tx * WOUT + hA, xhi = tx == a.ntx - 1 ? n + 1 : (tx + 1) * WOUT + hA;
   const int64_t sbase = (int64_t)shift * (NF ? (int64_t)(NF + 1) * NF : a.ss);
-  const int cA = x0 - hA + LC * lane;
+  const int cA = sA + LC * lane;
   V* __restrict__ uout = a.u_out + sbase + cA;  // per-lane column pointer (row 0)
   const V* __restrict__ ecs = a.ec + (int64_t)shift * (NF ? (int64_t)(NF / 2 + 1) * (NF / 2) : a.ssc);
   const LevelCoef cf = coef_of(cp);
@@ -1595,9 +1615,11 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   for (int k = 0; k < LC; ++k) {
     const int c = cA + k;
     cin[k] = (unsigned)(c - 1) < (unsigned)m;
-    cst[k] = cin[k] && c >= x0 && c < x0 + WOUT;
+    cst[k] = cin[k] && c >= xlo && c < xhi;
   }
-  const int rlo = r0 - hA, rhi = r0 + Hs + hA;
+  // rows marched: the strip and its halo, clamped to the domain (rows above row 0 are zero, as the windows start;
+  // past row m + 5 nothing is stored or restricted any more)
+  const int rlo = max(r0 - hA, 0), rhi = min(r0 + Hs + hA, m + 6);
   const int olo = max(r0, 1), ohi = min(r0 + Hs, m + 1);
   auto row_in = [&](int row) __attribute__((always_inline)) { return (unsigned)(row - 1) < (unsigned)m; };
   // rows before rlo are never loaded: they read as zero (they only reach halo rows, which are not stored)
@@ -1605,14 +1627,17 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   const V* __restrict__ uin = a.u_in + sbase + cA;  // per-lane column pointers
   const V* __restrict__ bb = a.b + sbase + cA;
   // warp-uniform: every column of the strip (and its coarse prolongation columns) is interior
-  const bool col_int = (x0 - hA >= 1) && (x0 - hA + 32 * LC + 1 <= m - 1);
+  const bool col_int = (sA >= 1) && (sA + 32 * LC + 1 <= m - 1);
   // steps j in [jlo_int, jhi_int] touch only interior rows (loads j-5 .. j+1, coarse rows up to (j+1)/2+1)
   const int jlo_int = max(6, rlo + 5), jhi_int = m - 3;  // (register path: loads reach j+1 and j-4)
   // (one sweep: the b rows read are j-1 and j-3 only)
   constexpr bool NEED_B3 = TWO || HASD, NEED_B5 = TWO && HASD;
 
   const int Ie = cA >> 1;
-  const bool codd = (cA & 1) != 0;  // warp-uniform (strips start at x0 - hA, lanes step by 2)
+  // the last strip ends at column m = n - 1 (even n): lane 31's east neighbour is the ghost column n, which no lane
+  // holds -- its shuffled value is replaced by zero (masked steps only: an edge strip never runs unmasked ones)
+  const bool east_ghost = tx == a.ntx - 1 && lane == 31;
+  const bool codd = (cA & 1) != 0;  // warp-uniform (strips start at sA, lanes step by 2)
   // (masked pair loads fetch both columns when either is interior and zero the other: a column outside the domain
   // lies inside the allocation -- the neighbouring row or the tail guard)
   // Mask modes of a step (MK): 0 = every row and column the step touches is interior (nothing masked); 1 = rows and
@@ -1706,7 +1731,9 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   auto resid = [&](const D2* lo, const D2* c, const D2* hi, const D2* bw, bool inside, D2* r, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value != 0;
     if constexpr (decltype(MK)::value == 2) inside = true;
-    const D2 wl = shfl_up2(c[LC - 1]), er = shfl_dn2(c[0]);
+    const D2 wl = shfl_up2(c[LC - 1]);
+    D2 er = shfl_dn2(c[0]);
+    if constexpr (MASK) er = csel(!east_ghost, er);
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
       const D2 v = res5(bw[k], cf.inv_h2, cf.dd, c[k], west(c, k, wl), east(c, k, er), lo[k], hi[k]);
@@ -1717,15 +1744,16 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   auto vanka_row = [&](const D2* r, D2* P, D2* C, bool din, D2* dl, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value != 0;
     if constexpr (decltype(MK)::value == 2) din = true;
-    const D2 rwl = shfl_up2(r[LC - 1]), rer = shfl_dn2(r[0]);
+    const D2 rwl = shfl_up2(r[LC - 1]);
+    D2 rer = shfl_dn2(r[0]);
+    if constexpr (MASK) rer = csel(!east_ghost, rer);
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
       const D2 s = cadd(west(r, k, rwl), east(r, k, rer));
       const D2 c = cmad2(cf.k1, r[k], cf.k2, s);
-      const D2 d = cmad2(cf.k0, r[k], cf.k1, s);
       const D2 v = cadd(P[k], c);
       dl[k] = MASK ? csel(din && cin[k], v) : v;
-      P[k] = cadd(C[k], d);
+      P[k] = cmad2_acc(C[k], cf.k0, r[k], cf.k1, s);  // C + d, d = k0 r + k1 s, as one FMA chain per component
       C[k] = c;
     }
   };
@@ -1867,12 +1895,14 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
           }
           const int J = (row - 1) >> 1;
           // (shuffles outside the task-dependent test: no divergence check around them)
-          const D2 vwl = shfl_up2(v[LC - 1]), ver = shfl_dn2(v[0]);
+          const D2 vwl = shfl_up2(v[LC - 1]);
+          D2 ver = shfl_dn2(v[0]);
+          if constexpr (decltype(MK)::value != 0) ver = csel(!east_ghost, ver);
           if (row >= r0 + 1 && row <= r0 + Hs && J >= 1 && J <= nc - 1) {
 #pragma unroll
             for (int k = 0; k < LC; ++k) {
               const int c = cA + k;
-              if (!(c & 1) && c >= x0 && c < x0 + WOUT) {
+              if (!(c & 1) && c >= xlo && c < xhi) {
                 const int I = c >> 1;
                 if (I >= 1 && I <= nc - 1) {
                   const D2 s = cadd(cadd(west(v, k, vwl), cscale(2.0, v[k])), east(v, k, ver));
@@ -1884,7 +1914,7 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < LC; ++k) Vp[k] = cadd(Vp[k], cscale(2.0, r2[k]));
+          for (int k = 0; k < LC; ++k) Vp[k] = make_double2(fma(2.0, r2[k].x, Vp[k].x), fma(2.0, r2[k].y, Vp[k].y));
         }
       }
     }
