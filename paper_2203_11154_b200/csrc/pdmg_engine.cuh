@@ -157,11 +157,9 @@ struct March2Table {
     march2_fill_two(e);
     march2_fill_one(e1);
 #if PDMG_MARCH2_NF
-    if constexpr (std::is_same<T, double>::value) {
-      march2_fill_hot_256(eN[0], e1N[0]);
-      march2_fill_hot_512(eN[1], e1N[1]);
-      march2_fill_hot_1024(eN[2], e1N[2]);
-    }
+    march2_fill_hot_256(eN[0], e1N[0]);
+    march2_fill_hot_512(eN[1], e1N[1]);
+    march2_fill_hot_1024(eN[2], e1N[2]);
 #endif
   }
 };
@@ -339,7 +337,7 @@ struct Engine : EngineBase {
         fill_pack(Lv, c0, cnt);
         const int wpc = two ? m2_wpc : m1_wpc;
         dim3 grid((ma.ntasks + wpc - 1) / wpc, cnt);
-        fn<<<grid, 32 * wpc, 0, stream>>>(ma, *cpack);
+        fn<<<grid, 32 * wpc, (size_t)wpc * M2_SMEM_PER_WARP, stream>>>(ma, *cpack);
       }
     }, pts * ubpp, (two ? 2 : 1) * pts);
     last_partials = ma.ntasks;
@@ -605,6 +603,15 @@ struct Engine : EngineBase {
     CK(cudaEventCreateWithFlags(&ev_nactive[1], cudaEventDisableTiming));
     for (auto& kv : table->e)
       if (kv.fn) CK(cudaFuncSetAttribute(kv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.smem));
+    {  // the b-row rings of the fused Vanka passes: up to 8 warps per CTA (m2_wpc / m1_wpc)
+      const March2Table<T>& mt = marches2();
+      auto opt_in = [&](const typename March2Table<T>::Fn* f, int cnt) {
+        for (int i = 0; i < cnt; ++i)
+          if (f[i]) CK(cudaFuncSetAttribute(f[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * M2_SMEM_PER_WARP));
+      };
+      opt_in(mt.e, 32), opt_in(mt.e1, 32);
+      for (int q = 0; q < 3; ++q) opt_in(mt.eN[q], 32), opt_in(mt.e1N[q], 32);
+    }
     CK(cudaStreamSynchronize(stream));
   }
 

@@ -1194,6 +1194,8 @@ constexpr int MARCH_WARPS = 4;  // warps per CTA (independent)
 #define PDMG_M1_MAXNREG 168
 #endif
 constexpr int M2_MAXNREG = PDMG_M2_MAXNREG, M1_MAXNREG = PDMG_M1_MAXNREG;
+constexpr int M2_RING = 8;  // slots of the per-warp b-row ring of k_march2 (rows j-1 .. j-5 live); 8 KB per warp
+constexpr int M2_SMEM_PER_WARP = M2_RING * 2 * 32 * 16;
 __host__ __device__ constexpr int march2_maxnreg(bool two) { return two ? M2_MAXNREG : M1_MAXNREG; }
 // warps of a marching pass resident per SM (registers are allocated per warp in units of 8 per thread)
 __host__ __device__ constexpr int march2_warps_per_sm(bool two) {
@@ -1632,6 +1634,22 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   const int jlo_int = max(6, rlo + 5), jhi_int = m - 3;  // (register path: loads reach j+1 and j-4)
   // (one sweep: the b rows read are j-1 and j-3 only)
   constexpr bool NEED_B3 = TWO || HASD, NEED_B5 = TWO && HASD;
+  // The b rows j-3 and j-5 (second sweep, closing residual) come back from a per-warp ring in shared memory that each
+  // lane fills with its own two columns when row j-1 is first used: lane-private slots, so no synchronisation and no
+  // bank conflicts, 4 L1 wavefronts per 16-B access instead of the 8 of a strided global re-read, and no prefetch
+  // registers (and their copies) for the re-read rows.  M2_RING slots x 2 columns x 32 lanes x 16 B = 8 KB per warp.
+#ifndef PDMG_M2_BRING
+#define PDMG_M2_BRING 1
+#endif
+  // (measured: the ring pays in the passes with a post stage -- C3 L0 vanka2+restrict 962 -> 905 us, C5 L0
+  // vanka+restrict 180 -> 167 us -- and costs in the prolongating pair, which re-reads one row and has no post
+  // stage -- C3 L0 prolong+vanka2 712 -> 755 us; PDMG_M2_BRING = 2 rings every variant that re-reads, 0 none)
+  constexpr bool BRING = PDMG_M2_BRING == 2 ? NEED_B3 : PDMG_M2_BRING == 1 ? HASD : false;
+  extern __shared__ __align__(16) unsigned char m2_smem[];
+  D2* const ring = reinterpret_cast<D2*>(m2_smem) + ((threadIdx.x >> 5) * M2_RING * LC) * 32 + (threadIdx.x & 31);
+  auto ring_at = [&](int row, int k) __attribute__((always_inline)) -> D2& {
+    return ring[((row & (M2_RING - 1)) * LC + k) * 32];
+  };
 
   const int Ie = cA >> 1;
   // the last strip ends at column m = n - 1 (even n): lane 31's east neighbour is the ghost column n, which no lane
@@ -1772,8 +1790,15 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   double nacc = 0.0;
   gread_u(rlo, Unx, IC<1>{});
   gload_b(rlo - 1, Bn, IC<1>{});
-  if constexpr (NEED_B3) gload_b(rlo - 3, B3n, IC<1>{});
-  if constexpr (NEED_B5) gload_b(rlo - 5, B5n, IC<1>{});
+  if constexpr (BRING) {  // rows before rlo read as zero
+#pragma unroll
+    for (int q = 0; q < M2_RING; ++q)
+#pragma unroll
+      for (int k = 0; k < LC; ++k) ring_at(q, k) = cz<D2>();
+  } else {
+    if constexpr (NEED_B3) gload_b(rlo - 3, B3n, IC<1>{});
+    if constexpr (NEED_B5) gload_b(rlo - 5, B5n, IC<1>{});
+  }
   if constexpr (PROLONG) load_coarse(rlo, IC<1>{});
 
   // one step at row j; window slot of (oldest, middle, newest) row = ((PH + 0, 1, 2) % 3)
@@ -1786,8 +1811,14 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
     for (int k = 0; k < LC; ++k) {
       Un[k] = Unx[k];
       Bc[k] = Bn[k];
-      if constexpr (NEED_B3) B3[k] = B3n[k];
-      if constexpr (NEED_B5) B5[k] = B5n[k];
+      if constexpr (BRING) {
+        ring_at(j - 1, k) = Bc[k];
+        if constexpr (NEED_B3) B3[k] = ring_at(j - 3, k);
+        if constexpr (NEED_B5) B5[k] = ring_at(j - 5, k);
+      } else {
+        if constexpr (NEED_B3) B3[k] = B3n[k];
+        if constexpr (NEED_B5) B5[k] = B5n[k];
+      }
     }
     if constexpr (PROLONG) {  // u row j += P e_c (coarse values loaded last step)
       D2 Pc[LC];
@@ -1803,11 +1834,20 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
       gread_u(j + 1, Unx, MK);
       gload_b(j, Bn, MK);
       if constexpr (PROLONG) {
-        if constexpr (M2_CPF > 0) l2_prefetch(ecs + (int64_t)min((j + 1 + 2 * M2_CPF) >> 1, nc) * nc + Ie);
-        load_coarse(j + 1, MK);
+        // coarse rows J, J + 1 serve the fine rows 2J and 2J + 1: loaded once per pair, when the even row is next
+        // (j is warp-uniform, so this is a uniform branch; the values stay in Cq for two steps)
+#ifndef PDMG_M2_COARSE_PAIR
+#define PDMG_M2_COARSE_PAIR 1
+#endif
+        if (!PDMG_M2_COARSE_PAIR || ((j + 1) & 1) == 0) {
+          if constexpr (M2_CPF > 0) l2_prefetch(ecs + (int64_t)min((j + 1 + 2 * M2_CPF) >> 1, nc) * nc + Ie);
+          load_coarse(j + 1, MK);
+        }
       }
-      if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
-      if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
+      if constexpr (!BRING) {
+        if constexpr (NEED_B3) gload_b(j - 2, B3n, MK);
+        if constexpr (NEED_B5) gload_b(j - 4, B5n, MK);
+      }
     }
 #pragma unroll
     for (int k = 0; k < LC; ++k) U0[sn][k] = Un[k];

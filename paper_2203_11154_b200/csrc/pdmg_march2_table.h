@@ -17,5 +17,8 @@ void march2_fill_one(March2Fn<float>* e);
 void march2_fill_hot_256(March2Fn<double>* eN, March2Fn<double>* e1N);
 void march2_fill_hot_512(March2Fn<double>* eN, March2Fn<double>* e1N);
 void march2_fill_hot_1024(March2Fn<double>* eN, March2Fn<double>* e1N);
+void march2_fill_hot_256(March2Fn<float>* eN, March2Fn<float>* e1N);
+void march2_fill_hot_512(March2Fn<float>* eN, March2Fn<float>* e1N);
+void march2_fill_hot_1024(March2Fn<float>* eN, March2Fn<float>* e1N);
 
 }  // namespace pdmg_b200
