@@ -1522,7 +1522,14 @@ __device__ __forceinline__ void stpair(float2* p, float2 a, float2 b) {
   v.a = a, v.b = b;
   *reinterpret_cast<PairC64*>(p) = v;
 }
-__device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// (PDMG_M2_PF_LANES: a lane's hint covers its own 32 B; with 2 / 4 only every 2nd / 4th lane issues one -- 64 / 128 B
+// apart -- which cuts the hints' L1 wavefronts if the prefetch granularity is a 64 / 128 B line)
+#ifndef PDMG_M2_PF_LANES
+#define PDMG_M2_PF_LANES 1
+#endif
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+  if (PDMG_M2_PF_LANES == 1 || (threadIdx.x & (PDMG_M2_PF_LANES - 1)) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 template <int X>
 struct IC {
   static constexpr int value = X;
