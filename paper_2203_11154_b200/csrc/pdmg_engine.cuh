@@ -246,8 +246,6 @@ struct Engine : EngineBase {
     const int hs = march2_hs_for(n, prolong, post, two);
     return march2_ntx(n, march2_ha(post, two)) * ((n + hs - 1) / hs);
   }
-  int wave_S = 0;  // shifts the wave model sizes a pass for (0 = the batch; the rolling solve sets its active count)
-  bool roll_adapt = false;  // rolling solve: strip heights from the active count of each round (PDMG_ROLL_ADAPT)
   static constexpr int kMinStrip = 16;  // smallest strip height the wave model may pick (partial-buffer sizing)
   int sm_count = 148;
   // Strip height of a k_march2 pass.  The measured defaults (128 rows for n >= 512, 64 for n = 256, 32 below;
@@ -264,7 +262,7 @@ struct Engine : EngineBase {
     const int wpc = two ? m2_wpc : m1_wpc;
     const int64_t slots = (int64_t)sm_count * (march2_warps_per_sm(two) / wpc);
     auto cost = [&](int hs) {
-      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + wpc - 1) / wpc) * (wave_S > 0 ? wave_S : S);
+      const int64_t ctas = (int64_t)((ntx * ((n + hs - 1) / hs) + wpc - 1) / wpc) * S;
       return (double)((ctas + slots - 1) / slots) * (hs + 2 * ha);
     };
     int best = def;
@@ -445,9 +443,7 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_IO_CHUNKS")) io_chunks = std::atoi(e);
     if (const char* e = std::getenv("PDMG_IO_MODE")) io_mode = std::atoi(e);
     if (const char* e = std::getenv("PDMG_ROLL_LANES")) roll_lanes = std::atoi(e);
-    if (const char* e = std::getenv("PDMG_ROLL_AHEAD")) roll_lookahead = std::atoi(e);
     if (const char* e = std::getenv("PDMG_ROLL_PIECE")) roll_piece = std::atoi(e);
-    if (const char* e = std::getenv("PDMG_ROLL_ADAPT")) roll_adapt = std::atoi(e) != 0;
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
     auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
       out.clear();
@@ -1352,7 +1348,6 @@ struct Engine : EngineBase {
   // norm); otherwise the chunked pipelines below run.
   int roll_lanes = 2;      // PDMG_ROLL_LANES
   int roll_piece = 0;      // shifts per piece (0 = ~32 MB); > 0 also takes small batches through the rolling solve (tests)
-  int roll_lookahead = 0;  // pieces admitted ahead of their copy's completion (the stream waits for them), PDMG_ROLL_AHEAD
   std::vector<std::unique_ptr<Engine<T>>> lanes;
   struct RollShared {
     const pdmg_c128* b;
@@ -1565,9 +1560,8 @@ struct Engine : EngineBase {
     rolling = true;
     try {
       while (n_done < n_mine) {
-        // admit the pieces whose copies have landed, plus roll_lookahead more whose copies are queued (the stream
-        // waits for those: the round being enqueued starts about one round from now); with nothing active, wait
-        int ahead = 0;
+        // admit the pieces whose copies have landed; with nothing active, wait for the next one (admitting pieces
+        // ahead of their copy, with the stream waiting for them, measured no faster)
         for (; admitted < nm;) {
           const int p = mine[admitted];
           {
@@ -1580,8 +1574,7 @@ struct Engine : EngineBase {
           }
           if (n_active > 0 && cudaEventQuery(sh.in[p]) != cudaSuccess) {
             (void)cudaGetLastError();
-            if (ahead >= roll_lookahead) break;
-            ++ahead;
+            break;
           }
           const int s0 = sh.plo[p], s1 = sh.plo[p + 1];
           CK(cudaStreamWaitEvent(stream, sh.in[p], 0));
@@ -1602,7 +1595,6 @@ struct Engine : EngineBase {
         // one cycle over the active shifts; its first fine pass forms their convergence norms and k_finalize_roll
         // retires the shifts that are done before the rest of the cycle runs
         roll_slot = round & 1;
-        wave_S = roll_adapt ? std::max(1, n_active) : 0;
         nin_k = 0;
         F.uzero = false;
         cycle_level(0, false, d_active, n_active, false);
@@ -1630,7 +1622,6 @@ struct Engine : EngineBase {
       err = std::current_exception();
     }
     rolling = false;
-    wave_S = 0;
     nin_k = -1;
     if (out_thread.joinable()) {
       {
