@@ -701,12 +701,13 @@ struct Engine : EngineBase {
   // Block size of the one-CTA-per-shift kernels (64 registers/thread: 1024 threads fill an SM's register
   // file).  Smaller blocks once S exceeds the SM count keep every shift resident in a single wave.
   int small_threads_env = 0;
-  int small_threads() const {
+  // (count: the CTAs that do work -- the batch, or the active shifts of a rolling round, whose other CTAs exit)
+  int small_threads(int count = 0) const {
     if (small_threads_env > 0) return small_threads_env;
-    int sms = 148;
-    return S <= sms ? SMALL_THREADS : S <= 2 * sms ? SMALL_THREADS / 2 : SMALL_THREADS / 4;
+    if (count <= 0) count = S;
+    return count <= sm_count ? SMALL_THREADS : count <= 2 * sm_count ? SMALL_THREADS / 2 : SMALL_THREADS / 4;
   }
-  void tail_cycle(int l, const int* active, bool zero) {
+  void tail_cycle(int l, const int* active, bool zero, int n_act = 0) {
     SmallArgs<T> sa{};
     for (size_t q = l; q < lv.size(); ++q)
       sa.lv[q - l] = SmallLevel<T>{lv[q].u[0], lv[q].u[1], lv[q].b, lv[q].coef, lv[q].n, lv[q].ss};
@@ -715,7 +716,7 @@ struct Engine : EngineBase {
     sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
     sa.ainv = d_ainv, sa.coarse_N = coarse_N, sa.active = active, sa.tail_zero = zero ? 1 : 0;
     timed("coarse_tail", 0.0,
-          [&] { k_small_cycle<T><<<S, small_threads(), coarse_N * sizeof(double2), stream>>>(sa); });
+          [&] { k_small_cycle<T><<<S, small_threads(rolling ? n_act : 0), coarse_N * sizeof(double2), stream>>>(sa); });
     for (size_t q = l; q < lv.size(); ++q) lv[q].cur = 0, lv[q].uzero = false;
   }
 
@@ -724,7 +725,7 @@ struct Engine : EngineBase {
     const int L = (int)lv.size();
     const bool jac = cfg.smoother == PDMG_SMOOTHER_JACOBI;
     if (l > 0 && l == tail_level()) {  // the whole coarse tail in one launch (each visit of a W-cycle)
-      tail_cycle(l, active, zero);
+      tail_cycle(l, active, zero, n_act);
       return false;
     }
     if (l + 1 == L) {

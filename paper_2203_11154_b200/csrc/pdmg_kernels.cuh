@@ -1183,10 +1183,10 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
 namespace pdmg_b200 {
 
 constexpr int MARCH_WARPS = 4;  // warps per CTA (independent)
-// Register caps of the marching passes (k_march2).  The caps, not the CTA shape, set the warps resident per SM:
-// 65536 / (32 x cap) -- 10 for the two-sweep passes (cap 200; they need 196-229 registers uncapped, and at 200 the
-// restriction variants spill 40 bytes), 12 for the one-sweep passes (cap 168).  CTAs are small (2 warps) so that the
-// resident count divides evenly; the host picks the CTA size (Engine::m2_wpc / m1_wpc).
+// Register caps of the marching passes (k_march2).  The caps, not the CTA shape, set the warps resident per SM
+// (registers are allocated in units of 16 per thread: 8 warps for the two-sweep passes at cap 232 -- 198-218 used --
+// and 12 for the one-sweep passes at cap 168).  Lower caps for 9 or 10 warps were measured slower (DESIGN 3.2d).
+// The host picks the CTA size (Engine::m2_wpc / m1_wpc, 4 warps).
 #ifndef PDMG_M2_MAXNREG
 #define PDMG_M2_MAXNREG 232
 #endif
