@@ -37,7 +37,8 @@ RowTab rowtab(const std::vector<double2*>& p, int rows, int64_t ld) {
 
 void launch_dft(const DftTables& T, const RowTab& in, const RowTab& out, int64_t pt0, int64_t pt1, cudaStream_t st) {
   const int P = dft_points_per_cta(T.nt);
-  const size_t smem = (size_t)T.nt * P * sizeof(double2);
+  // data + (radix-2 path) the nt/2 twiddles
+  const size_t smem = (size_t)T.nt * P * sizeof(double2) + (T.log2nt >= 0 ? (size_t)(T.nt / 2) * sizeof(double2) : 0);
   const int64_t blocks = (pt1 - pt0 + P - 1) / P;
   if (blocks > 0)
     k_time_dft<<<(unsigned)blocks, DFT_THREADS, smem, st>>>(in, out, T.nt, T.log2nt, pt0, pt1, P, T.tw, T.pre, T.post);
@@ -110,7 +111,8 @@ void enable_peers(const std::vector<int>& devs) {
 }  // namespace
 
 void check_dft_size(int nt) {
-  if ((size_t)nt * dft_points_per_cta(nt) * sizeof(double2) > (size_t)DFT_SMEM_MAX)
+  const bool pow2 = nt > 0 && (nt & (nt - 1)) == 0;  // (the radix-2 path also holds nt/2 twiddles)
+  if ((size_t)nt * dft_points_per_cta(nt) * sizeof(double2) + (pow2 ? (size_t)(nt / 2) * sizeof(double2) : 0) > (size_t)DFT_SMEM_MAX)
     throw ConfigError("time DFT: nt = " + std::to_string(nt) + " needs more than " + std::to_string(DFT_SMEM_MAX) +
                       " B of shared memory per transform (nt <= 6144)");
 }

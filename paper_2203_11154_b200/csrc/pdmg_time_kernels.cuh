@@ -21,6 +21,7 @@ struct RowTab {
   int64_t ld;              // elements per row
 };
 __device__ __forceinline__ double2* row_ptr(const RowTab& T, int r) {
+  if (r < T.rows) return T.p[0] + (int64_t)r * T.ld;  // first (or only) shard: no division
   const int s = r / T.rows;
   return T.p[s] + (int64_t)(r - s * T.rows) * T.ld;
 }
@@ -46,9 +47,17 @@ __global__ void __launch_bounds__(DFT_THREADS) k_time_dft(const RowTab in, const
   const int64_t p0 = pt0 + (int64_t)blockIdx.x * P;
   const int np = (int)min((int64_t)P, pt1 - p0);
   const int tid = threadIdx.x;
+  // (radix-2 path: nt and P are powers of two, so the index splits are shifts and masks, not divisions)
+  const int lp = log2nt >= 0 ? 31 - __clz(P) : 0;
+  // radix-2 path: the nt/2 twiddles the butterflies use sit in shared memory behind the data (a global load per
+  // butterfly, even an L1 hit, stalled every one of them: 56 % of the kernel's stall samples)
+  double2* stw = buf + (size_t)nt * P;
+  if (log2nt >= 0)
+    for (int q = tid; q < (nt >> 1); q += blockDim.x) stw[q] = tw[q];
   // load (bit-reversed time order for the radix-2 path), with the pre-scaling
+#pragma unroll 4
   for (int q = tid; q < nt * P; q += blockDim.x) {
-    const int t = q / P, pl = q - t * P;
+    const int t = log2nt >= 0 ? q >> lp : q / P, pl = q - t * P;
     double2 v = make_double2(0.0, 0.0);
     if (pl < np) v = cmul(pre[t], row_ptr(in, t)[p0 + pl]);
     const int dst = log2nt >= 0 ? (int)(__brev((unsigned)t) >> (32 - log2nt)) : t;
@@ -56,22 +65,47 @@ __global__ void __launch_bounds__(DFT_THREADS) k_time_dft(const RowTab in, const
   }
   __syncthreads();
   if (log2nt >= 0) {
-    for (int len = 2; len <= nt; len <<= 1) {
-      const int half = len >> 1, tstep = nt / len;
+    // Two radix-2 stages per pass over shared memory (a thread carries four elements through both: the same
+    // butterflies in the same order, half the shared-memory traffic and barriers); a last single stage if log2 nt
+    // is odd.
+    auto cmulw = [](double2 w, double2 b) { return make_double2(w.x * b.x - w.y * b.y, w.x * b.y + w.y * b.x); };
+    int lh = 0;
+    for (; lh + 1 < log2nt; lh += 2) {
+      const int h = 1 << lh, t1 = nt >> (lh + 1), t2 = nt >> (lh + 2);
+      for (int q = tid; q < (nt >> 2) * P; q += blockDim.x) {
+        const int bf = q >> lp, pl = q & (P - 1);
+        const int grp = bf >> lh, jj = bf & (h - 1);
+        const int i0 = (grp * 4 * h + jj) * P + pl, st = h * P;
+        const double2 w1 = stw[jj * t1], w2 = stw[jj * t2], w3 = stw[(jj + h) * t2];
+        const double2 a = buf[i0], b = buf[i0 + st], c = buf[i0 + 2 * st], d = buf[i0 + 3 * st];
+        const double2 wb = cmulw(w1, b), wd = cmulw(w1, d);
+        const double2 a1 = make_double2(a.x + wb.x, a.y + wb.y), b1 = make_double2(a.x - wb.x, a.y - wb.y);
+        const double2 c1 = make_double2(c.x + wd.x, c.y + wd.y), d1 = make_double2(c.x - wd.x, c.y - wd.y);
+        const double2 wc = cmulw(w2, c1), we = cmulw(w3, d1);
+        buf[i0] = make_double2(a1.x + wc.x, a1.y + wc.y);
+        buf[i0 + 2 * st] = make_double2(a1.x - wc.x, a1.y - wc.y);
+        buf[i0 + st] = make_double2(b1.x + we.x, b1.y + we.y);
+        buf[i0 + 3 * st] = make_double2(b1.x - we.x, b1.y - we.y);
+      }
+      __syncthreads();
+    }
+    for (; lh < log2nt; ++lh) {
+      const int half = 1 << lh, len = half << 1, tstep = nt >> (lh + 1);
       for (int q = tid; q < (nt >> 1) * P; q += blockDim.x) {
-        const int bf = q / P, pl = q - bf * P;
-        const int grp = bf / half, j = bf - grp * half;
-        const int i0 = grp * len + j, i1 = i0 + half;
-        const double2 w = tw[j * tstep];
+        const int bf = q >> lp, pl = q & (P - 1);
+        const int grp = bf >> lh, jj = bf & (half - 1);
+        const int i0 = grp * len + jj, i1 = i0 + half;
+        const double2 w = stw[jj * tstep];
         const double2 a = buf[i0 * P + pl], b = buf[i1 * P + pl];
-        const double2 wb = make_double2(w.x * b.x - w.y * b.y, w.x * b.y + w.y * b.x);
+        const double2 wb = cmulw(w, b);
         buf[i0 * P + pl] = make_double2(a.x + wb.x, a.y + wb.y);
         buf[i1 * P + pl] = make_double2(a.x - wb.x, a.y - wb.y);
       }
       __syncthreads();
     }
+#pragma unroll 4
     for (int q = tid; q < nt * P; q += blockDim.x) {
-      const int k = q / P, pl = q - k * P;
+      const int k = q >> lp, pl = q & (P - 1);
       if (pl < np) row_ptr(out, k)[p0 + pl] = cmul(post[k], buf[k * P + pl]);
     }
   } else {
