@@ -149,9 +149,9 @@ struct March2Table {
   using Fn = March2Fn<T>;
   Fn e[32] = {};   // two sweeps per pass
   Fn e1[32] = {};  // one sweep per pass (k_march2<..., TWO = false>)
-  // the hot variants with the level's n compiled in (NF): [n = 256, 512, 1024][key]
-  Fn eN[3][32] = {}, e1N[3][32] = {};
-  static int nf_slot(int n) { return n == 256 ? 0 : n == 512 ? 1 : n == 1024 ? 2 : -1; }
+  // the hot variants with the level's n compiled in (NF): [n = 256, 512, 1024, 128][key]
+  Fn eN[4][32] = {}, e1N[4][32] = {};
+  static int nf_slot(int n) { return n == 256 ? 0 : n == 512 ? 1 : n == 1024 ? 2 : n == 128 ? 3 : -1; }
   static int key(bool lu, bool pr, int post, bool nin = false) { return march2_key(lu, pr, post, nin); }
   March2Table() {
     march2_fill_two(e);
@@ -160,6 +160,7 @@ struct March2Table {
     march2_fill_hot_256(eN[0], e1N[0]);
     march2_fill_hot_512(eN[1], e1N[1]);
     march2_fill_hot_1024(eN[2], e1N[2]);
+    march2_fill_hot_128(eN[3], e1N[3]);
 #endif
   }
 };
@@ -606,7 +607,7 @@ struct Engine : EngineBase {
           if (f[i]) CK(cudaFuncSetAttribute(f[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * M2_SMEM_PER_WARP));
       };
       opt_in(mt.e, 32), opt_in(mt.e1, 32);
-      for (int q = 0; q < 3; ++q) opt_in(mt.eN[q], 32), opt_in(mt.e1N[q], 32);
+      for (int q = 0; q < 4; ++q) opt_in(mt.eN[q], 32), opt_in(mt.e1N[q], 32);
     }
     CK(cudaStreamSynchronize(stream));
   }

@@ -1,0 +1,3 @@
+// pdmg_m2_hot128.cu -- one unit of k_march2 instantiations (pdmg_march2_units.cuh)
+#define PDMG_M2_UNIT_NF 128
+#include "pdmg_march2_units.cuh"

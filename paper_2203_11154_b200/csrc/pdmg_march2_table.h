@@ -14,9 +14,11 @@ void march2_fill_two(March2Fn<double>* e);
 void march2_fill_one(March2Fn<double>* e);
 void march2_fill_two(March2Fn<float>* e);
 void march2_fill_one(March2Fn<float>* e);
+void march2_fill_hot_128(March2Fn<double>* eN, March2Fn<double>* e1N);
 void march2_fill_hot_256(March2Fn<double>* eN, March2Fn<double>* e1N);
 void march2_fill_hot_512(March2Fn<double>* eN, March2Fn<double>* e1N);
 void march2_fill_hot_1024(March2Fn<double>* eN, March2Fn<double>* e1N);
+void march2_fill_hot_128(March2Fn<float>* eN, March2Fn<float>* e1N);
 void march2_fill_hot_256(March2Fn<float>* eN, March2Fn<float>* e1N);
 void march2_fill_hot_512(March2Fn<float>* eN, March2Fn<float>* e1N);
 void march2_fill_hot_1024(March2Fn<float>* eN, March2Fn<float>* e1N);
