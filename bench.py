@@ -204,17 +204,15 @@ def kernels_summary(stats: dict, top: int = 12) -> dict:
 
 
 def so_sha16() -> str:
-    import hashlib
-
+    """Identity of the running build: the hash of the library's sources (a rebuilt .so is not byte-identical)."""
     from paper_2203_11154_b200 import _native as N
 
-    with open(N.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
+    return N.source_sha16()
 
 
 def traffic_for(config: str, kernel: str) -> dict:
     """ncu DRAM traffic per launch of `kernel` (dram__bytes_read.sum + dram__bytes_write.sum, one `ncu --set full`
-    capture, profiles/traffic.json).  Each capture is stamped with the sha256 of the libpdmg_b200.so it profiled;
+    capture, profiles/traffic.json).  Each capture is stamped with the sha256 of the library sources it was built from;
     a capture of another build is not reported as this build's traffic."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -225,8 +223,8 @@ def traffic_for(config: str, kernel: str) -> dict:
     if not isinstance(ent, dict):
         return {"traffic": None, "traffic_note": f"no ncu capture of {kernel} for {config}"}
     cur = so_sha16()
-    if ent.get("so_sha16") != cur:
-        return {"traffic": None, "traffic_note": f"ncu capture is of build {ent.get('so_sha16')}, this build is {cur}",
+    if ent.get("src_sha16", ent.get("so_sha16")) != cur:
+        return {"traffic": None, "traffic_note": f"ncu capture is of build {ent.get('src_sha16', ent.get('so_sha16'))}, this build is {cur}",
                 "traffic_stale": ent.get("bytes")}
     return {"traffic": ent["bytes"], "traffic_source": ent.get("source", "profiles/traffic.json"),
             "traffic_build": cur}

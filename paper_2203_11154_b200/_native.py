@@ -144,3 +144,18 @@ def lib() -> C.CDLL:
 
 def ptr(a: np.ndarray) -> int:
     return a.ctypes.data
+
+
+def source_sha16() -> str:
+    """sha256[:16] over the library's sources (csrc/*.cu, *.cuh, *.h, Makefile, by name): the identity of a build that
+    survives a rebuild (the linked .so is not byte-reproducible).  profiles/traffic.json stamps ncu captures with it."""
+    import hashlib
+
+    d = os.path.join(PKG_DIR, "csrc")
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(d)):
+        if name.endswith((".cu", ".cuh", ".h")) or name == "Makefile":
+            h.update(name.encode())
+            with open(os.path.join(d, name), "rb") as f:
+                h.update(f.read())
+    return h.hexdigest()[:16]

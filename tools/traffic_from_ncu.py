@@ -4,7 +4,7 @@
     python tools/traffic_from_ncu.py <raw.csv from `ncu -i X.ncu-rep --page raw --csv`> <config> <kernel class> <source note>
 
 Takes the mean of dram__bytes_read.sum + dram__bytes_write.sum over the captured launches and records it with the
-sha256[:16] of the libpdmg_b200.so in the tree (the build the capture must have profiled); bench.py reports the
+sha256[:16] of the library sources in the tree (the build the capture must have profiled); bench.py reports the
 figure only while that build is the one it runs.
 """
 import csv
@@ -31,10 +31,13 @@ def main():
             pass
     if not vals:
         sys.exit("no dram__bytes rows in " + raw)
-    sha = hashlib.sha256(open(os.path.join(ROOT, "paper_2203_11154_b200", "libpdmg_b200.so"), "rb").read()).hexdigest()[:16]
+    sys.path.insert(0, ROOT)
+    from paper_2203_11154_b200 import _native as N
+
+    sha = N.source_sha16()
     p = os.path.join(ROOT, "profiles", "traffic.json")
     tj = json.load(open(p)) if os.path.exists(p) else {}
-    tj.setdefault(config, {})[kernel] = {"bytes": sum(vals) / len(vals), "so_sha16": sha, "source": note,
+    tj.setdefault(config, {})[kernel] = {"bytes": sum(vals) / len(vals), "src_sha16": sha, "source": note,
                                          "launches_captured": len(vals)}
     json.dump(tj, open(p, "w"), indent=1)
     print(config, kernel, sum(vals) / len(vals), sha)
