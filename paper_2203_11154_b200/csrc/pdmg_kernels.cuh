@@ -943,6 +943,10 @@ struct SmallSolver {
   double2* cb;  // coarsest rhs staging (shared, coarse_N)
 
   __device__ __forceinline__ V* ptr(V* base, int l) const { return base + (int64_t)s * a.lv[l].ss; }
+  // Block-wide passes walk the m x m interior as rows of W = 2^lw >= m slots (node index = slot >> lw, slot & (W - 1)):
+  // shifts and masks instead of a division by m per node and pass (the passes are instruction-bound: 55 % of what
+  // they issued was index arithmetic); the W - m slots past a row's end idle.
+  __device__ __forceinline__ static int row_bits(int m) { return m > 1 ? 32 - __clz(m - 1) : 0; }
   __device__ __forceinline__ LevelCoef coef(int l) const { return a.lv[l].coef[s]; }
 
   // r = b - (A + lambda I) u on level l (grid.cpp:69-100); returns the block-reduced ||r||^2 if wanted
@@ -954,9 +958,11 @@ struct SmallSolver {
     const V* b = ptr(L.b, l);
     V* r = ptr(L.r, l);
     double acc2 = 0.0;
-    for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
-      const int j = q / m + 1, i = q - (j - 1) * m + 1;
-      const int64_t p = (int64_t)j * n + i;
+    const int lw = row_bits(m);
+    for (int q = threadIdx.x; q < (m << lw); q += blockDim.x) {
+      const int j = (q >> lw) + 1, i = (q & ((1 << lw) - 1)) + 1;
+      if (i > m) continue;
+      const int p = j * n + i;
       double2 rv = ld2(b[p]);
       if (!zero_u) {
         double2 acc = cmul(cf.d, ld2(u[p]));
@@ -993,9 +999,11 @@ struct SmallSolver {
     const LevelCoef cf = coef(l);
     V* u = ptr(L.u, l);
     const V* r = ptr(L.r, l);
-    for (int q = threadIdx.x; q < m * m; q += blockDim.x) {
-      const int j = q / m + 1, i = q - (j - 1) * m + 1;
-      const int64_t p = (int64_t)j * n + i;
+    const int lw = row_bits(m);
+    for (int q = threadIdx.x; q < (m << lw); q += blockDim.x) {
+      const int j = (q >> lw) + 1, i = (q & ((1 << lw) - 1)) + 1;
+      if (i > m) continue;
+      const int p = j * n + i;
       double2 dl;
       if (a.jacobi) {
         dl = cmul(cf.k0, ld2(r[p]));
@@ -1017,9 +1025,11 @@ struct SmallSolver {
     const int nf = F.n, nc = Cc.n, mc = nc - 1;
     const V* r = ptr(F.r, l);
     V* bc = ptr(Cc.b, l + 1);
-    for (int q = threadIdx.x; q < mc * mc; q += blockDim.x) {
-      const int J = q / mc + 1, I = q - (J - 1) * mc + 1;
-      const int64_t c = (int64_t)(2 * J) * nf + 2 * I;
+    const int lw = row_bits(mc);
+    for (int q = threadIdx.x; q < (mc << lw); q += blockDim.x) {
+      const int J = (q >> lw) + 1, I = (q & ((1 << lw) - 1)) + 1;
+      if (I > mc) continue;
+      const int c = (2 * J) * nf + 2 * I;
       double2 sum = ld2(r[c - nf - 1]);
       sum = cadd(sum, cscale(2.0, ld2(r[c - nf])));
       sum = cadd(sum, ld2(r[c - nf + 1]));
@@ -1029,7 +1039,7 @@ struct SmallSolver {
       sum = cadd(sum, ld2(r[c + nf - 1]));
       sum = cadd(sum, cscale(2.0, ld2(r[c + nf])));
       sum = cadd(sum, ld2(r[c + nf + 1]));
-      bc[(int64_t)J * nc + I] = st2<V>(cscale(1.0 / 16.0, sum));
+      bc[J * nc + I] = st2<V>(cscale(1.0 / 16.0, sum));
     }
     __syncthreads();
   }
@@ -1041,15 +1051,17 @@ struct SmallSolver {
     const int nf = F.n, mf = nf - 1, nc = Cc.n;
     V* u = ptr(F.u, l);
     const V* e = ptr(Cc.u, l + 1);
-    for (int q = threadIdx.x; q < mf * mf; q += blockDim.x) {
-      const int j = q / mf + 1, i = q - (j - 1) * mf + 1;
-      const V* e0 = e + (int64_t)(j >> 1) * nc + (i >> 1);
+    const int lw = row_bits(mf);
+    for (int q = threadIdx.x; q < (mf << lw); q += blockDim.x) {
+      const int j = (q >> lw) + 1, i = (q & ((1 << lw) - 1)) + 1;
+      if (i > mf) continue;
+      const V* e0 = e + (j >> 1) * nc + (i >> 1);
       double2 pv;
       if (!(i & 1) && !(j & 1)) pv = ld2(e0[0]);
       else if ((i & 1) && !(j & 1)) pv = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[1])));
       else if (!(i & 1) && (j & 1)) pv = cscale(0.5, cadd(ld2(e0[0]), ld2(e0[nc])));
       else pv = cscale(0.25, cadd(cadd(cadd(ld2(e0[0]), ld2(e0[1])), ld2(e0[nc])), ld2(e0[nc + 1])));
-      const int64_t p = (int64_t)j * nf + i;
+      const int p = j * nf + i;
       u[p] = st2<V>(zero_u ? pv : cadd(ld2(u[p]), pv));
     }
     __syncthreads();
