@@ -443,6 +443,20 @@ def test_rolling_host_solve_matches_batch(oracle, monkeypatch, cyc, lanes, pagea
     assert [r.iterations for r in reps] == list(ref["iterations"])
 
 
+@pytest.mark.parametrize("n,coarsest", [(72, 9), (88, 11), (104, 13), (112, 7), (144, 9), (176, 11), (208, 13), (224, 7),
+                                        (288, 9), (352, 11), (416, 13), (448, 7), (576, 9)])
+@pytest.mark.parametrize("cyc", [(2, 2), (1, 1)])
+def test_strip_geometry_ragged_sizes(oracle, n, coarsest, cyc):
+    """Edge-aligned strips of the marching passes (first strip from the ghost column, last strip ending at column m,
+    1 + ceil((n - 64) / WOUT) strips per row, marched rows clamped to the domain) on level sizes that are not powers
+    of two: every level of these hierarchies has a different strip count, last-strip overlap and row remainder.
+    Cycle counts, histories and iterates against the oracle (multigrid.cpp:85-110)."""
+    m = n - 1
+    lams = oracle.circulant_shifts(1e-3, 256, 1 / 256, 0, 256)[[0, 17, 200]]
+    b = oracle.random_complex(n, 3 * m * m).reshape(3, m, m)
+    _check_solve(oracle, n, lams, b, Cfg(nu1=cyc[0], nu2=cyc[1], coarsest_n=coarsest), path="batched")
+
+
 def test_device_list_matches_single_device(oracle):
     """One context sharded over a device list (three shards sharing GPU 0, chunks of ceil(S / 3),
     paradiag.cpp:222): host solve, device-resident shard solve, cycle and level operators are bitwise the
