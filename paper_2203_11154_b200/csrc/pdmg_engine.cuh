@@ -446,6 +446,8 @@ struct Engine : EngineBase {
     if (const char* e = std::getenv("PDMG_ROLL_LANES")) roll_lanes = std::atoi(e);
     if (const char* e = std::getenv("PDMG_ROLL_PIECE")) roll_piece = std::atoi(e);
     if (const char* e = std::getenv("PDMG_SMALL_THREADS")) small_threads_env = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_SMALL_CLUSTER")) small_cluster = std::atoi(e);
+    if (const char* e = std::getenv("PDMG_SMALL_CLUSTER_NODES")) small_cluster_min_nodes = std::atoi(e);
     auto parse_hs = [](const char* e, std::vector<std::pair<int, int>>& out) {
       out.clear();
       for (const char* q = e; *q;) {
@@ -708,6 +710,35 @@ struct Engine : EngineBase {
     if (count <= 0) count = S;
     return count <= sm_count ? SMALL_THREADS : count <= 2 * sm_count ? SMALL_THREADS / 2 : SMALL_THREADS / 4;
   }
+  // Thread-block cluster size of a one-CTA-per-shift launch: when the shifts that do work are fewer than the SMs, a
+  // cluster of 2, 4 or 8 full-size CTAs shares each shift (SmallSolver), as many as still fit one CTA per SM.
+  int small_cluster = 8;  // largest cluster size (PDMG_SMALL_CLUSTER; 0 or 1: always one CTA per shift)
+  int small_cluster_min_nodes = 8192;  // (PDMG_SMALL_CLUSTER_NODES) top-level nodes from which a cluster pays
+  int small_cluster_size(int count, int threads, int top_n) const {
+    if (small_cluster <= 1 || threads != SMALL_THREADS) return 1;
+    if ((top_n - 1) * (top_n - 1) < small_cluster_min_nodes) return 1;
+    if (count <= 0) count = S;
+    // (clusters of 8 need 8 free SMs of one GPC each: only when they fill at most half the GPU -- 16 clusters of 8
+    // measured no faster than single CTAs, 16 clusters of 4 1.5x faster;
+    // and 36 clusters of 4 -- 144 of 148 SMs -- do not all fit their GPCs at once: 2.0 vs 1.7 ms)
+    for (int c : {8, 4, 2})
+      if (c <= small_cluster && (int64_t)count * c <= (c == 8 ? sm_count / 2 : c == 4 ? sm_count * 7 / 8 : sm_count)) return c;
+    return 1;
+  }
+  template <class K>
+  void launch_small(K kernel, int threads, int csize, size_t smem, const SmallArgs<T>& sa) {
+    if (csize <= 1) {
+      kernel<<<S, threads, smem, stream>>>(sa);
+      return;
+    }
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)S * csize), lc.blockDim = dim3(threads), lc.dynamicSmemBytes = smem, lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    lc.attrs = at, lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, kernel, sa));
+  }
   void tail_cycle(int l, const int* active, bool zero, int n_act = 0) {
     SmallArgs<T> sa{};
     for (size_t q = l; q < lv.size(); ++q)
@@ -716,8 +747,10 @@ struct Engine : EngineBase {
     sa.nu1 = cfg.nu1, sa.nu2 = cfg.nu2, sa.gamma = cfg.cycle == PDMG_CYCLE_W ? 2 : 1;
     sa.jacobi = cfg.smoother == PDMG_SMOOTHER_JACOBI, sa.max_iter = cfg.max_iter, sa.tol = cfg.tol;
     sa.ainv = d_ainv, sa.coarse_N = coarse_N, sa.active = active, sa.tail_zero = zero ? 1 : 0;
-    timed("coarse_tail", 0.0,
-          [&] { k_small_cycle<T><<<S, small_threads(rolling ? n_act : 0), coarse_N * sizeof(double2), stream>>>(sa); });
+    const int cnt = (rolling || active == nullptr) ? n_act : 0, thr = small_threads(cnt);
+    timed("coarse_tail", 0.0, [&] {
+      launch_small(k_small_cycle<T>, thr, small_cluster_size(cnt, thr, lv[l].n), coarse_N * sizeof(double2), sa);
+    });
     for (size_t q = l; q < lv.size(); ++q) lv[q].cur = 0, lv[q].uzero = false;
   }
 
@@ -891,7 +924,7 @@ struct Engine : EngineBase {
       const double per_shift_bytes = 0.0;
       (void)per_shift_bytes;
       timed("small_solve", 0.0, [&] {
-        k_small_solve<T><<<S, small_threads(), coarse_N * sizeof(double2), stream>>>(sa);
+        launch_small(k_small_solve<T>, small_threads(), small_cluster_size(S, small_threads(), lv[0].n), coarse_N * sizeof(double2), sa);
       });
       CK(cudaGetLastError());
       CK(cudaMemsetAsync(d_parity, 0, sizeof(int) * H, stream));

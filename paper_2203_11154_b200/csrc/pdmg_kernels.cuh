@@ -17,6 +17,7 @@
 // each stage keeps a RING-row circular buffer in shared memory (wide enough for its halo), so global
 // memory is read ~once per pass: u, b, e_c in; u_out, b_c out.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -941,6 +942,17 @@ struct SmallSolver {
   int s;
   double* red;  // [33] block reduction scratch (shared)
   double2* cb;  // coarsest rhs staging (shared, coarse_N)
+  // A shift may be worked on by a thread-block CLUSTER of csize CTAs (small batches: BASELINE configs 1-2, the coarse
+  // tail of a strong-scaling share or of a rolling round -- fewer shifts than SMs).  The passes stride over the
+  // cluster's threads, a pass ends with a cluster barrier (release / acquire at cluster scope: the level arrays live
+  // in global memory and the next pass reads nodes another CTA wrote), block reductions are combined over distributed
+  // shared memory, and the coarsest solve runs on the cluster's first CTA.  csize = 1 is the one-CTA form.
+  int crank = 0, csize = 1;
+  int tid = 0, nthr = 0;  // this thread's rank among, and the number of, the threads that share the shift
+  __device__ __forceinline__ void sync() const {
+    if (csize > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else __syncthreads();
+  }
 
   __device__ __forceinline__ V* ptr(V* base, int l) const { return base + (int64_t)s * a.lv[l].ss; }
   // Block-wide passes walk the m x m interior as rows of W = 2^lw >= m slots (node index = slot >> lw, slot & (W - 1)):
@@ -959,7 +971,7 @@ struct SmallSolver {
     V* r = ptr(L.r, l);
     double acc2 = 0.0;
     const int lw = row_bits(m);
-    for (int q = threadIdx.x; q < (m << lw); q += blockDim.x) {
+    for (int q = tid; q < (m << lw); q += nthr) {
       const int j = (q >> lw) + 1, i = (q & ((1 << lw) - 1)) + 1;
       if (i > m) continue;
       const int p = j * n + i;
@@ -975,8 +987,10 @@ struct SmallSolver {
       r[p] = st2<V>(rv);
       if (want_norm) acc2 += rv.x * rv.x + rv.y * rv.y;
     }
-    __syncthreads();
-    if (!want_norm) return 0.0;
+    if (!want_norm) {
+      sync();
+      return 0.0;
+    }
     for (int o = 16; o > 0; o >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc2;
     __syncthreads();
@@ -986,9 +1000,14 @@ struct SmallSolver {
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       if (threadIdx.x == 0) red[32] = tot;
     }
-    __syncthreads();
-    tot = red[32];
-    __syncthreads();
+    sync();  // (also ends the pass: r is complete)
+    if (csize > 1) {  // the CTAs' partial sums, in rank order, over distributed shared memory
+      tot = 0.0;
+      for (int q = 0; q < csize; ++q) tot += *cooperative_groups::this_cluster().map_shared_rank(&red[32], q);
+    } else {
+      tot = red[32];
+    }
+    sync();
     return tot;
   }
 
@@ -1000,7 +1019,7 @@ struct SmallSolver {
     V* u = ptr(L.u, l);
     const V* r = ptr(L.r, l);
     const int lw = row_bits(m);
-    for (int q = threadIdx.x; q < (m << lw); q += blockDim.x) {
+    for (int q = tid; q < (m << lw); q += nthr) {
       const int j = (q >> lw) + 1, i = (q & ((1 << lw) - 1)) + 1;
       if (i > m) continue;
       const int p = j * n + i;
@@ -1015,7 +1034,7 @@ struct SmallSolver {
       }
       u[p] = st2<V>(zero_u ? dl : cadd(ld2(u[p]), dl));
     }
-    __syncthreads();
+    sync();
   }
 
   // b_{l+1} = R r_l (grid.cpp:102-121) and e_{l+1} = 0
@@ -1026,7 +1045,7 @@ struct SmallSolver {
     const V* r = ptr(F.r, l);
     V* bc = ptr(Cc.b, l + 1);
     const int lw = row_bits(mc);
-    for (int q = threadIdx.x; q < (mc << lw); q += blockDim.x) {
+    for (int q = tid; q < (mc << lw); q += nthr) {
       const int J = (q >> lw) + 1, I = (q & ((1 << lw) - 1)) + 1;
       if (I > mc) continue;
       const int c = (2 * J) * nf + 2 * I;
@@ -1041,7 +1060,7 @@ struct SmallSolver {
       sum = cadd(sum, ld2(r[c + nf + 1]));
       bc[J * nc + I] = st2<V>(cscale(1.0 / 16.0, sum));
     }
-    __syncthreads();
+    sync();
   }
 
   // u_l += P e_{l+1} (grid.cpp:123-153); u_l := P e when zero_u
@@ -1052,7 +1071,7 @@ struct SmallSolver {
     V* u = ptr(F.u, l);
     const V* e = ptr(Cc.u, l + 1);
     const int lw = row_bits(mf);
-    for (int q = threadIdx.x; q < (mf << lw); q += blockDim.x) {
+    for (int q = tid; q < (mf << lw); q += nthr) {
       const int j = (q >> lw) + 1, i = (q & ((1 << lw) - 1)) + 1;
       if (i > mf) continue;
       const V* e0 = e + (j >> 1) * nc + (i >> 1);
@@ -1064,7 +1083,7 @@ struct SmallSolver {
       const int p = j * nf + i;
       u[p] = st2<V>(zero_u ? pv : cadd(ld2(u[p]), pv));
     }
-    __syncthreads();
+    sync();
   }
 
   __device__ void coarse_solve(int l) const {
@@ -1072,15 +1091,17 @@ struct SmallSolver {
     const int n = L.n, m = n - 1, N = a.coarse_N;
     const V* b = ptr(L.b, l);
     V* u = ptr(L.u, l);
-    for (int q = threadIdx.x; q < N; q += blockDim.x) cb[q] = ld2(b[(int64_t)(q / m + 1) * n + (q % m + 1)]);
-    __syncthreads();
-    const double2* A = a.ainv + (int64_t)s * N * N;
-    for (int rr = threadIdx.x; rr < N; rr += blockDim.x) {
-      double2 acc = cz<double2>();
-      for (int c = 0; c < N; ++c) acc = cadd(acc, cmul(A[(int64_t)rr * N + c], cb[c]));
-      u[(int64_t)(rr / m + 1) * n + (rr % m + 1)] = st2<V>(acc);
+    if (crank == 0) {  // (the staged right-hand side lives in this CTA's shared memory)
+      for (int q = threadIdx.x; q < N; q += blockDim.x) cb[q] = ld2(b[(int64_t)(q / m + 1) * n + (q % m + 1)]);
+      __syncthreads();
+      const double2* A = a.ainv + (int64_t)s * N * N;
+      for (int rr = threadIdx.x; rr < N; rr += blockDim.x) {
+        double2 acc = cz<double2>();
+        for (int c = 0; c < N; ++c) acc = cadd(acc, cmul(A[(int64_t)rr * N + c], cb[c]));
+        u[(int64_t)(rr / m + 1) * n + (rr % m + 1)] = st2<V>(acc);
+      }
     }
-    __syncthreads();
+    sync();
   }
 
   // cycle_on_level (multigrid.cpp:63-77) as an explicit state machine (no device recursion): st[l] counts
@@ -1137,8 +1158,11 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_cycle(SmallArgs<T> a
   using V = typename vec2<T>::type;
   __shared__ double red[33];
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (a.active != nullptr && a.active[blockIdx.x] == 0) return;
-  SmallSolver<T> S{a, (int)blockIdx.x, red, reinterpret_cast<double2*>(smem_raw)};
+  const int csize = (int)cooperative_groups::this_cluster().num_blocks();
+  const int crank = (int)cooperative_groups::this_cluster().block_rank(), s = (int)blockIdx.x / csize;
+  if (a.active != nullptr && a.active[s] == 0) return;  // (the whole cluster)
+  SmallSolver<T> S{a, s, red, reinterpret_cast<double2*>(smem_raw), crank, csize,
+                   crank * (int)blockDim.x + (int)threadIdx.x, csize * (int)blockDim.x};
   S.cycle(a.tail_zero != 0);
 }
 
@@ -1147,12 +1171,15 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
   using V = typename vec2<T>::type;
   __shared__ double red[33];
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SmallSolver<T> S{a, (int)blockIdx.x, red, reinterpret_cast<double2*>(smem_raw)};
-  const int s = blockIdx.x;
+  const int csize = (int)cooperative_groups::this_cluster().num_blocks();
+  const int crank = (int)cooperative_groups::this_cluster().block_rank(), s = (int)blockIdx.x / csize;
+  SmallSolver<T> S{a, s, red, reinterpret_cast<double2*>(smem_raw), crank, csize,
+                   crank * (int)blockDim.x + (int)threadIdx.x, csize * (int)blockDim.x};
+  const bool lead = crank == 0 && threadIdx.x == 0;
   const int H = a.max_iter + 1;
   // u = 0 (multigrid.cpp:90), r0 = ||b|| (:91)
   const double r0 = sqrt(S.residual(0, true, true));
-  if (threadIdx.x == 0) {
+  if (lead) {
     a.r0[s] = r0;
     a.hist[(int64_t)s * H] = r0;
     a.iterations[s] = 0;
@@ -1162,19 +1189,19 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_solve(SmallArgs<T> a
     const SmallLevel<T>& L0 = a.lv[0];
     V* u = S.ptr(L0.u, 0);
     const int n = L0.n, m = n - 1;
-    for (int q = threadIdx.x; q < m * m; q += blockDim.x) u[(int64_t)(q / m + 1) * n + (q % m + 1)] = st2<V>(cz<double2>());
-    __syncthreads();
+    for (int q = S.tid; q < m * m; q += S.nthr) u[(int64_t)(q / m + 1) * n + (q % m + 1)] = st2<V>(cz<double2>());
+    S.sync();
   }
   if (r0 == 0.0 || a.tol >= 1.0) return;
   for (int k = 1; k <= a.max_iter; ++k) {
     S.cycle(k == 1);
     const double rk = sqrt(S.residual(0, false, true));
-    if (threadIdx.x == 0) {
+    if (lead) {
       a.hist[(int64_t)s * H + k] = rk;
       a.iterations[s] = k;
     }
     if (rk <= a.tol * r0) {
-      if (threadIdx.x == 0) a.converged[s] = 1;
+      if (lead) a.converged[s] = 1;
       break;
     }
   }

@@ -457,6 +457,25 @@ def test_strip_geometry_ragged_sizes(oracle, n, coarsest, cyc):
     _check_solve(oracle, n, lams, b, Cfg(nu1=cyc[0], nu2=cyc[1], coarsest_n=coarsest), path="batched")
 
 
+@pytest.mark.parametrize("S", [3, 20, 50])
+def test_small_solve_cluster_matches_single_cta(oracle, monkeypatch, S):
+    """The one-CTA-per-shift solve with a thread-block cluster per shift (8, 4 or 2 CTAs sharing a shift's passes,
+    cluster barriers between them, the norm combined over distributed shared memory): the iterates are bitwise those
+    of the single-CTA kernel, cycle counts identical, histories equal to rounding (the norm's summation order differs);
+    both against the oracle (multigrid.cpp:85-110)."""
+    n, m = 128, 127
+    lams = oracle.circulant_shifts(0.01, 32, 1 / 32, 0, 32)[np.arange(S) % 32]
+    b = oracle.random_complex(5, S * m * m).reshape(S, m, m)
+    monkeypatch.setenv("PDMG_SMALL_CLUSTER", "1")
+    u1, reps1, _ = _check_solve(oracle, n, lams, b, Cfg(), path="small", expect_kernel="small_solve")
+    monkeypatch.setenv("PDMG_SMALL_CLUSTER", "8")
+    u8, reps8, _ = _check_solve(oracle, n, lams, b, Cfg(), path="small", expect_kernel="small_solve")
+    assert np.array_equal(u1, u8)
+    for r1, r8 in zip(reps1, reps8):
+        assert r1.iterations == r8.iterations
+        assert np.allclose(r1.residual_history, r8.residual_history, rtol=1e-12, atol=0)
+
+
 def test_device_list_matches_single_device(oracle):
     """One context sharded over a device list (three shards sharing GPU 0, chunks of ceil(S / 3),
     paradiag.cpp:222): host solve, device-resident shard solve, cycle and level operators are bitwise the
