@@ -12,6 +12,9 @@
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "pdmg_host.h"
 #include "pdmg_kernels.cuh"
@@ -1276,6 +1279,41 @@ struct Engine : EngineBase {
   std::unique_ptr<Bounce> bounce_in, bounce_out;
   // Host copies of the bounce pipeline run on one persistent pool of worker threads shared by the input and all
   // output streams (no per-piece thread creation, no oversubscription of the host cores).
+  // Host copy of a bounce-pipeline slice with non-temporal stores (AVX2, checked at run time): the destination is
+  // either a pinned piece the DMA engine reads next or the caller's result buffer, neither of which is wanted in the
+  // cache, and a plain memcpy of a 2 MB slice pays a read-for-ownership of every destination line.
+#if defined(__x86_64__)
+  __attribute__((target("avx2"))) static void stream_copy_avx2(void* dst, const void* src, size_t len) {
+    char* d = (char*)dst;
+    const char* q = (const char*)src;
+    const size_t head = (32 - ((uintptr_t)d & 31)) & 31;
+    if (head >= len) {
+      std::memcpy(d, q, len);
+      return;
+    }
+    std::memcpy(d, q, head);
+    d += head, q += head, len -= head;
+    size_t i = 0;
+    for (; i + 128 <= len; i += 128) {
+      const __m256i a = _mm256_loadu_si256((const __m256i*)(q + i)), b = _mm256_loadu_si256((const __m256i*)(q + i + 32));
+      const __m256i c = _mm256_loadu_si256((const __m256i*)(q + i + 64)), e = _mm256_loadu_si256((const __m256i*)(q + i + 96));
+      _mm256_stream_si256((__m256i*)(d + i), a), _mm256_stream_si256((__m256i*)(d + i + 32), b);
+      _mm256_stream_si256((__m256i*)(d + i + 64), c), _mm256_stream_si256((__m256i*)(d + i + 96), e);
+    }
+    _mm_sfence();
+    std::memcpy(d + i, q + i, len - i);
+  }
+#endif
+  static void stream_copy(void* dst, const void* src, size_t len) {
+#if defined(__x86_64__)
+    static const bool avx2 = __builtin_cpu_supports("avx2") && !std::getenv("PDMG_NO_STREAM_COPY");
+    if (avx2 && len >= 4096) {
+      stream_copy_avx2(dst, src, len);
+      return;
+    }
+#endif
+    std::memcpy(dst, src, len);
+  }
   struct CopyPool {
     std::mutex mu;
     std::condition_variable cv;
@@ -1300,7 +1338,7 @@ struct Engine : EngineBase {
               t = q.back();
               q.pop_back();
             }
-            std::memcpy(t.dst, t.src, t.len);
+            stream_copy(t.dst, t.src, t.len);
             t.left->fetch_sub(1, std::memory_order_acq_rel);
           }
         });
@@ -1314,7 +1352,10 @@ struct Engine : EngineBase {
       for (auto& x : th) x.join();
     }
     static CopyPool& get() {
-      static CopyPool pool(std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2)));
+      static CopyPool pool([] {
+        if (const char* e = std::getenv("PDMG_COPY_THREADS")) return std::max(1, std::atoi(e));
+        return std::max(1, std::min(12, (int)std::thread::hardware_concurrency() * 3 / 4));  // (8 -> 12 of 16: ~8 % faster)
+      }());
       return pool;
     }
   };
