@@ -147,14 +147,15 @@ def ptr(a: np.ndarray) -> int:
 
 
 def source_sha16() -> str:
-    """sha256[:16] over the library's sources (csrc/*.cu, *.cuh, *.h, Makefile, by name): the identity of a build that
-    survives a rebuild (the linked .so is not byte-reproducible).  profiles/traffic.json stamps ncu captures with it."""
+    """sha256[:16] over the kernel sources (csrc/*.cuh and the Makefile with its flags, by name): the identity of the
+    device code that survives a rebuild (the linked .so is not byte-reproducible) and host-only changes.
+    profiles/traffic.json stamps ncu captures with it."""
     import hashlib
 
     d = os.path.join(PKG_DIR, "csrc")
     h = hashlib.sha256()
     for name in sorted(os.listdir(d)):
-        if name.endswith((".cu", ".cuh", ".h")) or name == "Makefile":
+        if (name.endswith(".cuh") and name != "pdmg_engine.cuh") or name == "Makefile":
             h.update(name.encode())
             with open(os.path.join(d, name), "rb") as f:
                 h.update(f.read())

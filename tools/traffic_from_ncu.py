@@ -4,7 +4,7 @@
     python tools/traffic_from_ncu.py <raw.csv from `ncu -i X.ncu-rep --page raw --csv`> <config> <kernel class> <source note>
 
 Takes the mean of dram__bytes_read.sum + dram__bytes_write.sum over the captured launches and records it with the
-sha256[:16] of the library sources in the tree (the build the capture must have profiled); bench.py reports the
+sha256[:16] of the kernel sources in the tree (the build the capture must have profiled); bench.py reports the
 figure only while that build is the one it runs.
 """
 import csv
