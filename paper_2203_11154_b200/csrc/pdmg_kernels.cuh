@@ -1552,6 +1552,11 @@ __device__ __forceinline__ void ldpair(const float2* p, double2& a, double2& b) 
   const PairC64 v = *reinterpret_cast<const PairC64*>(p);
   a = ld2(v.a), b = ld2(v.b);
 }
+__device__ __forceinline__ void ldpair_raw(const double2* p, double2& a, double2& b) { ldpair(p, a, b); }
+__device__ __forceinline__ void ldpair_raw(const float2* p, float2& a, float2& b) {
+  const PairC64 v = *reinterpret_cast<const PairC64*>(p);
+  a = v.a, b = v.b;
+}
 __device__ __forceinline__ void stpair(double2* p, double2 a, double2 b) {
   PairC128 v;
   v.a = a, v.b = b;
@@ -1710,17 +1715,23 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   // loads unpredicated (the columns outside the domain lie inside the allocation and hold finite values) and only
   // the residuals, corrections and prolongation forced to zero outside the interior columns -- the ghost column
   // then shields the interior from whatever the lanes beyond it compute.
-  auto gpair = [&](const V* __restrict__ base, int row, D2* out, auto MK, int what) __attribute__((always_inline)) {
+  // The prefetched rows stay in the STORAGE type (V) until the step that consumes them: widening a complex64 value
+  // where it is loaded made the conversion wait for the load it was meant to run ahead of (ncu: 39 % of the c64
+  // pass's stall samples sat on those F2F instructions).
+  auto gpair = [&](const V* __restrict__ base, int row, V* out, auto MK, int what) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value == 1;
-    out[0] = out[1] = cz<D2>();
+    out[0] = out[1] = cz<V>();
     if (!MASK || (row_ok(row) && (cin[0] || cin[1]))) {
       bounds_check(sbase + cA + (int64_t)row * n + 1, a.elems, what);
       bounds_check(sbase + cA + (int64_t)row * n, a.elems, what);
-      ldpair(base + (int64_t)row * n, out[0], out[1]);
-      if constexpr (MASK) out[0] = csel(cin[0], out[0]), out[1] = csel(cin[1], out[1]);
+      ldpair_raw(base + (int64_t)row * n, out[0], out[1]);
+      if constexpr (MASK) {
+        if (!cin[0]) out[0] = cz<V>();
+        if (!cin[1]) out[1] = cz<V>();
+      }
     }
   };
-  auto gread_u = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
+  auto gread_u = [&](int row, V* out, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value == 1;
     if constexpr (PAIR_U && LOADU) {
       gpair(uin, row, out, MK, 0);
@@ -1728,16 +1739,16 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
     }
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
-      out[k] = cz<D2>();
+      out[k] = cz<V>();
       if constexpr (LOADU) {
         if (!MASK || (row_ok(row) && cin[k])) {
           bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 0);
-          out[k] = ld2(uin[(int64_t)row * n + k]);
+          out[k] = uin[(int64_t)row * n + k];
         }
       }
     }
   };
-  auto gload_b = [&](int row, D2* out, auto MK) __attribute__((always_inline)) {
+  auto gload_b = [&](int row, V* out, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value == 1;
     if constexpr (PAIR_B) {
       gpair(bb, row, out, MK, 1);
@@ -1746,14 +1757,14 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
       if constexpr (MASK) {
-        out[k] = cz<D2>();
+        out[k] = cz<V>();
         if (row_ok(row) && cin[k]) {
           bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 1);
-          out[k] = ld2(bb[(int64_t)row * n + k]);
+          out[k] = bb[(int64_t)row * n + k];
         }
       } else {
         bounds_check(sbase + cA + (int64_t)row * n + k, a.elems, 2);
-        out[k] = ld2(bb[(int64_t)row * n + k]);
+        out[k] = bb[(int64_t)row * n + k];
       }
     }
   };
@@ -1780,7 +1791,7 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   // are loaded unconditionally (indices clamped into the array; out-of-domain points are masked when the
   // prolongation is formed) one step before the row is consumed: no window rotation, no branch around the
   // loads, so no register copy waits on a load that was just issued (DESIGN 3.2b)
-  D2 Cq[4];
+  V Cq[4];  // (storage type: widened where the prolongation is formed, one step after the loads)
   auto load_coarse = [&](int row, auto MK) __attribute__((always_inline)) {
     constexpr bool MASK = decltype(MK)::value == 1;
     int J = row >> 1, I = Ie;
@@ -1788,7 +1799,7 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
     const V* p0 = ecs + (int64_t)J * nc + I;
     bounds_check((p0 - a.ec) + nc + 1, a.elems_c, 3);
     bounds_check(p0 - a.ec, a.elems_c, 3);
-    Cq[0] = ld2(p0[0]), Cq[1] = ld2(p0[1]), Cq[2] = ld2(p0[nc]), Cq[3] = ld2(p0[nc + 1]);
+    Cq[0] = p0[0], Cq[1] = p0[1], Cq[2] = p0[nc], Cq[3] = p0[nc + 1];
   };
   auto west = [&](const D2* x, int k, const D2& wl) __attribute__((always_inline)) { return k == 0 ? wl : x[k - 1]; };
   auto east = [&](const D2* x, int k, const D2& er) __attribute__((always_inline)) { return k == LC - 1 ? er : x[k + 1]; };
@@ -1827,7 +1838,7 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
   D2 P1[LC], C1[LC], P2[LC], C2[LC], Vp[LC];
   // rows prefetched one step ahead (indexing these by window phase, so a step reads one slot and loads the
   // next, was measured to make ptxas keep three copies live and spill)
-  D2 Unx[LC], Bn[LC], B3n[LC], B5n[LC];
+  V Unx[LC], Bn[LC], B3n[LC], B5n[LC];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -1856,20 +1867,20 @@ __global__ void __maxnreg__(march2_maxnreg(TWO))
     D2 B3[LC], B5[LC], Bc[LC], Un[LC];
 #pragma unroll
     for (int k = 0; k < LC; ++k) {
-      Un[k] = Unx[k];
-      Bc[k] = Bn[k];
+      Un[k] = ld2(Unx[k]);
+      Bc[k] = ld2(Bn[k]);
       if constexpr (BRING) {
         ring_at(j - 1, k) = Bc[k];
         if constexpr (NEED_B3) B3[k] = ring_at(j - 3, k);
         if constexpr (NEED_B5) B5[k] = ring_at(j - 5, k);
       } else {
-        if constexpr (NEED_B3) B3[k] = B3n[k];
-        if constexpr (NEED_B5) B5[k] = B5n[k];
+        if constexpr (NEED_B3) B3[k] = ld2(B3n[k]);
+        if constexpr (NEED_B5) B5[k] = ld2(B5n[k]);
       }
     }
     if constexpr (PROLONG) {  // u row j += P e_c (coarse values loaded last step)
       D2 Pc[LC];
-      prolong_of(j, Cq[0], Cq[1], Cq[2], Cq[3], Pc, MK);
+      prolong_of(j, ld2(Cq[0]), ld2(Cq[1]), ld2(Cq[2]), ld2(Cq[3]), Pc, MK);
 #pragma unroll
       for (int k = 0; k < LC; ++k) Un[k] = cadd(Un[k], Pc[k]);
     }
